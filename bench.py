@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark: quantize+dequantize HBM GB/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the largest single-GPU microbench shape):
+fp32 activations 64M x 128 (32 GB, far larger than the 126 MB L2, so no L2
+flush is needed), INT2, group 64, stochastic rounding with the fast
+Philox4x32 noise.  One step = one fused quantize+pack (K1) plus one
+unpack+dequantize (K2) pass over the whole tensor through the public API.
+
+Bytes are algorithmic: per element 4 (fp32) + b/8 (codes)
++ 8/G (fp32 range and offset per group), counted once for K1 and once for K2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun every rank quantizes its own 64M x 128 shard (row offset =
+rank * rows, so the noise keys are global): weak scaling, no collective on
+the data path.  ``--impl reference`` times the CPU port of the reference
+algorithm (oracle/, compat Philox4x64 stream) on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantize+dequantize HBM GB/s (%peak); KGAT epoch/s and activation MB at INT2"
+UNIT = "GB/s"
+
+
+def algo_bytes_per_elem(bits, group):
+    return 4.0 + bits / 8.0 + 8.0 / group
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_port_run(rows, cols, bits, group, threads, seed=1, tid=0, min_seconds=0.0, max_reps=1):
+    """The oracle port of the reference quantize/dequantize (compat stream) on
+    host cores.  Returns (GB/s, seconds, reps)."""
+    from oracle import oracle as orc
+    x = np.random.default_rng(0).standard_normal((rows * cols // group, group), dtype=np.float32)
+    orc.lib()
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        c, r, o = orc.quantize(x, group, bits, orc.MODE_SR_COMPAT, seed, tid + reps, threads=threads)
+        orc.dequantize(c, r, o, group, bits, threads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if reps >= max_reps or (el >= min_seconds and reps >= 1):
+            break
+    el = time.perf_counter() - t0
+    gb = 2 * rows * cols * algo_bytes_per_elem(bits, group) * reps / 1e9
+    return gb / el, el, reps
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    rows = args.ref_rows
+    cfg = workload_config(args)
+    cfg["sample"] = f"{rows}x{args.cols} fp32 per step (bounded sample of the workload)"
+    for _ in range(args.warmup):
+        cpu_port_run(rows, args.cols, args.bits, args.group, threads)
+    times = []
+    for s in range(args.steps):
+        gbs, el, _ = cpu_port_run(rows, args.cols, args.bits, args.group, threads, tid=1000 + s)
+        times.append(el)
+    total_gb = 2 * rows * args.cols * algo_bytes_per_elem(args.bits, args.group) * args.steps / 1e9
+    value = total_gb / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": cfg["sample"] + "; oracle/kgq_oracle.c restatement of "
+                         "quantize_tensor/dequantize_tensor with the reference's numpy "
+                         "Philox4x64 stream, pthreads over groups"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args):
+    return {"workload": f"quantize+dequantize microbench (configs[1]) {args.rows}x{args.cols} fp32, "
+                        f"INT{args.bits}, group {args.group}, SR rng={args.rng}",
+            "rows_per_gpu": args.rows, "cols": args.cols, "bits": args.bits, "group": args.group,
+            "rounding": "stochastic", "rng": args.rng,
+            "l2": "inputs (%.1f GB/GPU) larger than the 126 MB L2; no flush needed"
+                  % (args.rows * args.cols * 4 / 1e9)}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args)
+    import paper_2212_04540_b200 as kgq
+    from paper_2212_04540_b200 import _lib
+
+    rows, cols, bits, group = args.rows, args.cols, args.bits, args.group
+    free, _ = torch.cuda.mem_get_info()
+    need = rows * cols * 4 * 2.3
+    if need > free:
+        rows = int(rows * free / need) // 1024 * 1024
+    n = rows * cols
+    bpe = algo_bytes_per_elem(bits, group)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randn((rows, cols), device="cuda", generator=g)
+    cfg = kgq.QuantConfig(bits=bits, group=group, rng=args.rng)
+    stream = kgq.RandomStream(1)
+    row_off = rank * rows
+    goff = row_off * cols // group
+
+    def step(tid):
+        q = kgq.quantize_tensor(x, cfg, stream, tensor_id=tid, group_offset=goff)
+        out = kgq.dequantize_tensor(q)
+        return q, out
+
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(cur)
+        for s in range(args.steps):
+            e0, e1, e2 = ev[s]
+            e0.record(cur)
+            q = kgq.quantize_tensor(x, cfg, stream, tensor_id=100 + s, group_offset=goff)
+            e1.record(cur)
+            out = kgq.dequantize_tensor(q)
+            e2.record(cur)
+            del q, out
+        t_end.record(cur)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_total = t_start.elapsed_time(t_end)
+    ms_total = max_over_ranks(ms_total, world)
+    q_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    d_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev]
+    peak, peak_src = load_peaks()
+    step_bytes = 2 * n * bpe
+    value = world * step_bytes * args.steps / (ms_total / 1e3) / 1e9
+    q_avg = sum(q_ms) / len(q_ms)
+    d_avg = sum(d_ms) / len(d_ms)
+    q_gbs = n * bpe / (q_avg / 1e3) / 1e9
+    d_gbs = n * bpe / (d_avg / 1e3) / 1e9
+    traffic = load_traffic()
+
+    # compat-stream (reference-identical noise) quantize, a few launches
+    comp = None
+    if not args.skip_compat:
+        ccfg = kgq.QuantConfig(bits=bits, group=group, rng="compat")
+        kgq.quantize_tensor(x, ccfg, stream, tensor_id=7)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for s in range(3):
+            kgq.quantize_tensor(x, ccfg, stream, tensor_id=200 + s, group_offset=goff)
+        b.record(cur)
+        torch.cuda.synchronize()
+        c_ms = a.elapsed_time(b) / 3
+        comp = {"quantize_ms": round(c_ms, 3), "quantize_GBps": round(n * bpe / (c_ms / 1e3) / 1e9, 1),
+                "frac": round(n * bpe / (c_ms / 1e3) / 1e9 / peak, 4)}
+
+    # end to end through the public API with host buffers (pinned), a
+    # bounded slice of the workload: H2D of the fp32 activations, quantize,
+    # dequantize, D2H of the reconstructed activations, every step.
+    e2e = None
+    if not args.skip_e2e:
+        e_rows = min(rows, args.e2e_rows)
+        xh = torch.empty((e_rows, cols), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x[:e_rows].cpu())
+        oh = torch.empty_like(xh, pin_memory=True)
+        del x
+        torch.cuda.empty_cache()
+
+        def e2e_step(tid):
+            xd = xh.to("cuda", non_blocking=True)
+            q = kgq.quantize_tensor(xd, cfg, stream, tensor_id=tid, group_offset=goff)
+            out = kgq.dequantize_tensor(q)
+            oh.copy_(out, non_blocking=True)
+
+        for w in range(2):
+            e2e_step(300 + w)
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        ke = max(2, min(args.steps, 5))
+        for s in range(ke):
+            e2e_step(400 + s)
+        b.record(cur)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(a.elapsed_time(b), world)
+        e_val = world * 2 * e_rows * cols * bpe * ke / (e_ms / 1e3) / 1e9
+        e2e = {"value": round(e_val, 3), "unit": UNIT, "h2d_bytes_per_step": e_rows * cols * 4,
+               "d2h_bytes_per_step": e_rows * cols * 4,
+               "sample": f"{e_rows}x{cols} fp32 per GPU per step (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        threads = os.cpu_count() or 1
+        gbs, el, reps = cpu_port_run(args.cpu_rows, cols, bits, group, threads, min_seconds=10.0,
+                                     max_reps=50)
+        cpu = {"value": round(gbs, 4), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{reps} x ({args.cpu_rows}x{cols} fp32 quantize+dequantize, compat "
+                         f"Philox4x64 stream) in {el:.1f}s; oracle/kgq_oracle.c, pthreads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_total / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch.randn fp32 activations)",
+            "config": dict(workload_config(args), rows_per_gpu=rows,
+                           parallelism=f"row shards x{world}, no data-path collective"),
+            "frac_of_peak": round(value / world / peak, 4),
+            "roofline": {"bound": "hbm", "kernel": "quantize_t4_kernel (K1, fused quantize+pack)",
+                         "achieved": round(q_gbs, 1), "peak": peak, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": round(q_gbs / peak, 4),
+                         "traffic": traffic.get("quantize"),
+                         "algorithmic_bytes_per_launch": int(n * bpe)},
+            "kernels": {
+                "quantize": {"ms": round(q_avg, 4), "GBps": round(q_gbs, 1), "frac": round(q_gbs / peak, 4)},
+                "dequantize": {"ms": round(d_avg, 4), "GBps": round(d_gbs, 1), "frac": round(d_gbs / peak, 4),
+                               "traffic": traffic.get("dequantize")},
+                "quantize_compat_rng": comp,
+            },
+            "clocks": clk.summary(),
+            "gpu_launches": 2 * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "native_lib": os.path.relpath(_lib.LIB_PATH, ROOT),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--rows", type=int, default=64 << 20)
+    ap.add_argument("--cols", type=int, default=128)
+    ap.add_argument("--bits", type=int, default=2)
+    ap.add_argument("--group", type=int, default=64)
+    ap.add_argument("--rng", default="fast", choices=["fast", "compat"])
+    ap.add_argument("--e2e-rows", type=int, default=8 << 20)
+    ap.add_argument("--cpu-rows", type=int, default=1 << 20)
+    ap.add_argument("--ref-rows", type=int, default=2 << 20)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-compat", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not os.environ.get("KGQ_ALLOW_SHORT_WARMUP"):
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

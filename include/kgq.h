@@ -1,0 +1,136 @@
+/*
+ * kgq.h -- C ABI of libkgq (sm_100a), the B200 activation-compression hot path.
+ *
+ * Every entry point takes plain device pointers, element counts and a CUDA
+ * stream (as void*, i.e. a cudaStream_t / CUstream; NULL = legacy default
+ * stream).  The caller allocates every buffer; no function allocates device
+ * memory, keeps global state, synchronises the stream, or throws.  Every
+ * function is stream-ordered and CUDA-graph capturable.  Return value is a
+ * kgq_status (0 = OK).
+ *
+ * The reference (kgact, pure numpy) has no FFI; each entry point below names
+ * the reference function whose semantics it replaces.  The Python host layer
+ * (paper_2212_04540_b200/) binds these through ctypes and
+ * maps status codes back to the reference's exception classes.
+ *
+ * Data layout ("group" = one quantization unit = one row of the (-1, G) view
+ * of a row-major fp32 tensor; G = cols reproduces the reference's per-row
+ * quantizer, quantize.py:184-186):
+ *   codes   : uint8  [n_groups][ceil(G*bits/8)]  LSB-first, groups byte aligned
+ *             (pack_codes, quantize.py:213-233)
+ *   ranges  : fp32   [n_groups]   R = max - min   (quantize.py:185)
+ *   offsets : fp32   [n_groups]   Z = min         (quantize.py:184)
+ */
+#ifndef KGQ_H_
+#define KGQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifndef KGQ_API
+#define KGQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum kgq_status {
+    KGQ_OK = 0,
+    KGQ_ERR_INVALID_ARG = 1,      /* -> ValueError                     */
+    KGQ_ERR_UNSUPPORTED_BITS = 2, /* -> ValueError / EncodingError     */
+    KGQ_ERR_CUDA = 3,             /* -> RuntimeError (kgq_last_cuda_error) */
+    KGQ_ERR_MISALIGNED = 4,       /* -> ValueError                     */
+    KGQ_ERR_SHAPE = 5             /* -> ShapeMismatchError             */
+};
+
+/* Rounding modes (QuantConfig.rounding, quantize.py:25-26, :48-49). */
+enum kgq_rounding {
+    KGQ_ROUND_NEAREST = 0,    /* np.rint, round-half-even (quantize.py:129-130)           */
+    KGQ_ROUND_SR_FAST = 1,    /* stochastic, Philox4x32-10 16-bit uniforms    */
+    KGQ_ROUND_SR_COMPAT = 2,  /* stochastic, numpy Philox4x64-10 stream (quantize.py:61-102) */
+    KGQ_ROUND_SR_NOISE = 3    /* stochastic, caller-supplied float64 uniforms (test seam)  */
+};
+
+KGQ_API int kgq_version(void);
+KGQ_API const char *kgq_status_string(int status);
+/* cudaError_t of the last KGQ_ERR_CUDA returned on this thread. */
+KGQ_API int kgq_last_cuda_error(void);
+
+/* quantize_tensor(x, QuantConfig(bits, rounding), RandomStream(seed), tensor_id)
+ * quantize.py:177-196 (+ _scale_rows :116-125, _round_block :128-132,
+ * pack_codes :213-233, RandomStream :61-102).
+ * bits in {1,2,4,8}; noise (n_groups*group float64) only for KGQ_ROUND_SR_NOISE.
+ * group_offset: global index of group 0 (row-partitioned tensors key their
+ * noise by global row, so any partitioning gives byte-identical codes).   */
+KGQ_API int kgq_quantize_f32(const float *x, int64_t n_groups, int32_t group, int32_t bits,
+                     int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                     int64_t group_offset, const double *noise, uint8_t *codes, float *ranges, float *offsets,
+                     void *stream);
+
+/* dequantize_tensor(q, float32), quantize.py:199-210 (+ unpack_codes :236-247). */
+KGQ_API int kgq_dequantize_f32(const uint8_t *codes, const float *ranges, const float *offsets,
+                       int64_t n_groups, int32_t group, int32_t bits, float *out,
+                       void *stream);
+
+/* Export the exact SR noise a quantize call consumes (exported-noise parity route).
+ * fast:   u16 per element, uniform = u16 / 65536.
+ * compat: (raw >> 11) per element, uniform = value * 2^-53
+ *         (== RandomStream(seed).matrix_uniforms(tid, n_groups, group)). */
+KGQ_API int kgq_fast_noise_u16(uint64_t seed, uint64_t tensor_id, int64_t group_offset,
+                       int64_t n_groups, int32_t group, uint16_t *out, void *stream);
+KGQ_API int kgq_compat_noise_raw53(uint64_t seed, uint64_t tensor_id, int64_t group_offset,
+                           int64_t n_groups, int32_t group, uint64_t *out, void *stream);
+
+/* pack_codes / unpack_codes, quantize.py:213-247 (rows byte-aligned, LSB-first).
+ * pack: codes uint8 [rows][cols] -> packed [rows][ceil(cols*bits/8)]; a code
+ * >= 2^bits sets *overflow (device int32, caller-zeroed) -> EncodingError. */
+KGQ_API int kgq_pack_codes(const uint8_t *codes, int64_t rows, int32_t cols, int32_t bits,
+                   uint8_t *packed, int32_t *overflow, void *stream);
+KGQ_API int kgq_unpack_codes(const uint8_t *packed, int64_t rows, int32_t cols, int32_t bits,
+                     uint8_t *codes, void *stream);
+
+/* spmm(A, X) with A in CSR (int32 indptr/indices, fp32 values), X [n_cols][d]
+ * row-major: out[i] = sum_{jj in row i, ascending} vals[jj] * X[indices[jj]],
+ * accumulated in column order with separate mul and add (tensorops.py:37-50,
+ * bit-identical to scipy csr_matvecs).  For the symmetric A_hat this is also
+ * spmm_t (tape.py:217-218).  Row i of the output uses indptr[i]..indptr[i+1]
+ * as given, so a row-partitioned CSR (global column ids) works unchanged.    */
+KGQ_API int kgq_spmm_csr_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
+                     int64_t n_rows, const float *x, int32_t d, float *out, void *stream);
+
+/* relu + BitMask.from_bool, tensorops.py:84-92 / tape.py:122-126:
+ * out = max(x, 0), mask bit i = x[i] > 0, LSB-first flat, ceil(n/8) bytes.  */
+KGQ_API int kgq_relu_mask_f32(const float *x, int64_t n, float *out, uint8_t *mask, void *stream);
+
+/* ReLU backward, tape.py:224-225: out = g * mask (mask as above). */
+KGQ_API int kgq_mask_apply_f32(const float *g, const uint8_t *mask, int64_t n, float *out,
+                       void *stream);
+
+/* Fused decompressor -> weight gradient, tape.py:220-222:
+ *   dtheta (+)= dequantize(codes, ranges, offsets)^T @ g
+ * codes are per-row groups (group == d), g is [rows][d] fp32, dtheta [d][d].
+ * The dequantized activation is never written to memory.  workspace must
+ * hold kgq_dequant_gemm_workspace_bytes(rows, d) bytes.  accumulate != 0
+ * adds into dtheta.  Deterministic (fixed reduction order). */
+KGQ_API size_t kgq_dequant_gemm_workspace_bytes(int64_t rows, int32_t d);
+KGQ_API int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges, const float *offsets,
+                            int64_t rows, int32_t d, int32_t bits, const float *g,
+                            float *dtheta, void *workspace, size_t workspace_bytes,
+                            int32_t accumulate, void *stream);
+
+/* Fused KGNN layer forward (model.py:81-85 + tape.py:101-126), one pass:
+ *   H = spmm(A, E); ctx = quantize(H) (group = d); J = H @ theta;
+ *   E_next = relu(J); mask = J > 0.
+ * H and J are never written to memory.  h_out (optional, may be NULL) receives
+ * H for debugging/parity.  d in {32, 64, 128}. */
+KGQ_API int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
+                          int64_t n_rows, const float *e, int32_t d, const float *theta,
+                          int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                          int64_t row_offset, uint8_t *codes, float *ranges, float *offsets, float *e_next,
+                          uint8_t *mask, float *h_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KGQ_H_ */

@@ -1,0 +1,204 @@
+// kgq_gemm.cu -- K3: fused decompressor -> weight gradient (tape.py:219-222)
+//   dtheta (+)= dequantize(ctx)^T @ g,   ctx = per-row quantized H [rows][d]
+// The dequantized activation only ever exists in shared memory.
+//
+// Each CTA owns a fixed set of 32-row chunks (deterministic grid), stages the
+// chunk's g rows (fp32) and its dequantized H rows (bit-exact with
+// dequantize_tensor) in shared memory, and accumulates the full d x d product
+// in registers: an 8x8 register tile per thread, (d/8)^2 threads per tile,
+// 256/(d/8)^2 row slices per CTA.  Slices and CTAs are reduced in a fixed
+// order, so the result is run-to-run deterministic.
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+constexpr int kGemmThreads = 256;
+constexpr int kChunkRows = 32;
+
+static inline int dq_gemm_grid(int64_t rows) {
+    int64_t chunks = (rows + kChunkRows - 1) / kChunkRows;
+    int64_t g = chunks < (int64_t)kSMs * 2 ? chunks : (int64_t)kSMs * 2;
+    return g < 1 ? 1 : (int)g;
+}
+
+template <int D, int BITS>
+__global__ void __launch_bounds__(kGemmThreads)
+dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
+                       const float *__restrict__ offsets, int64_t rows,
+                       const float *__restrict__ g, float *__restrict__ partial) {
+    constexpr int T8 = D / 8;               // 8x8 tiles per dimension
+    constexpr int TT = T8 * T8;             // threads per full d x d tile
+    constexpr int S = kGemmThreads / TT;    // row slices
+    constexpr int RB = D * BITS / 8;        // packed bytes per row
+    constexpr float Bf = (float)((1u << BITS) - 1u);
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    extern __shared__ __align__(16) float sm[];
+    float *hs = sm;                          // [kChunkRows][D]
+    float *gs = sm + kChunkRows * D;         // [kChunkRows][D]
+
+    const int t = threadIdx.x;
+    const int slice = t / TT, tt = t % TT;
+    const int ti = tt / T8, tj = tt % T8;
+    float acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 8; b++) acc[a][b] = 0.0f;
+
+    const int64_t n_chunks = (rows + kChunkRows - 1) / kChunkRows;
+    for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+        const int64_t r0 = ch * kChunkRows;
+        const int nr = (int)imin64(kChunkRows, rows - r0);
+        // g rows -> smem (float4)
+        for (int i = t; i < kChunkRows * D / 4; i += kGemmThreads) {
+            const int rr = (i * 4) / D;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rr < nr) v = __ldg(reinterpret_cast<const float4 *>(g + r0 * D) + i);
+            reinterpret_cast<float4 *>(gs)[i] = v;
+        }
+        // dequantize H rows -> smem: (R*c)/B + Z, R == 0 -> Z (quantize.py:206-209)
+        for (int i = t; i < kChunkRows * D; i += kGemmThreads) {
+            const int rr = i / D, k = i % D;
+            float v = 0.0f;
+            if (rr < nr) {
+                const int64_t row = r0 + rr;
+                const int bit = k * BITS;
+                const uint32_t c = (__ldg(codes + row * RB + (bit >> 3)) >> (bit & 7)) & MASK;
+                const float r = __ldg(ranges + row), z = __ldg(offsets + row);
+                v = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+            }
+            hs[i] = v;
+        }
+        __syncthreads();
+        for (int rr = slice; rr < kChunkRows; rr += S) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(hs + rr * D + ti * 8);
+            const float4 a1 = *reinterpret_cast<const float4 *>(hs + rr * D + ti * 8 + 4);
+            const float4 b0 = *reinterpret_cast<const float4 *>(gs + rr * D + tj * 8);
+            const float4 b1 = *reinterpret_cast<const float4 *>(gs + rr * D + tj * 8 + 4);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 8; b++) acc[a][b] = __fmaf_rn(av[a], bv[b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+    // reduce the S slices in order (reuse the staging smem: needs D*D floats)
+    float *red = sm;
+    for (int s = 0; s < S; s++) {
+        if (slice == s) {
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 8; b++) {
+                    float *p = red + (ti * 8 + a) * D + tj * 8 + b;
+                    *p = (s == 0) ? acc[a][b] : __fadd_rn(*p, acc[a][b]);
+                }
+        }
+        __syncthreads();
+    }
+    float *dst = partial + (int64_t)blockIdx.x * D * D;
+    for (int i = t; i < D * D; i += kGemmThreads) dst[i] = red[i];
+}
+
+__global__ void reduce_partials_kernel(const float *__restrict__ partial, int nparts, int dd,
+                                       float *__restrict__ out, int accumulate) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dd; i += gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int p = 0; p < nparts; p++) s = __fadd_rn(s, partial[(int64_t)p * dd + i]);
+        out[i] = accumulate ? __fadd_rn(out[i], s) : s;
+    }
+}
+
+// any d (correctness path): thread per output element, rows in order.
+__global__ void dequant_gemm_generic_kernel(const uint8_t *__restrict__ codes,
+                                            const float *__restrict__ ranges,
+                                            const float *__restrict__ offsets, int64_t rows,
+                                            int d, int bits, const float *__restrict__ g,
+                                            float *__restrict__ out, int accumulate) {
+    const int RB = (d * bits + 7) / 8;
+    const float Bf = (float)((1u << bits) - 1u);
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < d * d; o += gridDim.x * blockDim.x) {
+        const int i = o / d, jj = o % d;
+        float s = 0.0f;
+        const int bit = i * bits;
+        for (int64_t n = 0; n < rows; n++) {
+            const uint32_t c = (codes[n * RB + (bit >> 3)] >> (bit & 7)) & mask;
+            const float r = ranges[n], z = offsets[n];
+            const float h = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+            s = __fmaf_rn(h, g[n * d + jj], s);
+        }
+        out[o] = accumulate ? __fadd_rn(out[o], s) : s;
+    }
+}
+
+template <int D>
+static int launch_dq_gemm(int bits, const uint8_t *codes, const float *ranges, const float *offsets,
+                          int64_t rows, const float *g, float *partial, cudaStream_t s) {
+    const int grid = dq_gemm_grid(rows);
+    size_t smem = (size_t)2 * kChunkRows * D * sizeof(float);
+    if (smem < (size_t)D * D * sizeof(float)) smem = (size_t)D * D * sizeof(float);
+    void (*kern)(const uint8_t *, const float *, const float *, int64_t, const float *, float *);
+    switch (bits) {
+        case 1: kern = dequant_gemm_tn_kernel<D, 1>; break;
+        case 2: kern = dequant_gemm_tn_kernel<D, 2>; break;
+        case 4: kern = dequant_gemm_tn_kernel<D, 4>; break;
+        case 8: kern = dequant_gemm_tn_kernel<D, 8>; break;
+        default: return KGQ_ERR_UNSUPPORTED_BITS;
+    }
+    if (smem > 48 * 1024) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+    }
+    kern<<<grid, kGemmThreads, smem, s>>>(codes, ranges, offsets, rows, g, partial);
+    return KGQ_OK;
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+extern "C" size_t kgq_dequant_gemm_workspace_bytes(int64_t rows, int32_t d) {
+    if (d == 32 || d == 64 || d == 128) return (size_t)dq_gemm_grid(rows) * d * d * sizeof(float);
+    return 0;
+}
+
+extern "C" int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges,
+                                       const float *offsets, int64_t rows, int32_t d, int32_t bits,
+                                       const float *g, float *dtheta, void *workspace,
+                                       size_t workspace_bytes, int32_t accumulate, void *stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (rows < 0 || d < 1 || !dtheta) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (rows == 0) {
+        if (!accumulate) {
+            cudaError_t e = cudaMemsetAsync(dtheta, 0, (size_t)d * d * sizeof(float), s);
+            if (e != cudaSuccess) return kgq_set_cuda_error(e);
+        }
+        return KGQ_OK;
+    }
+    if (!codes || !ranges || !offsets || !g) return KGQ_ERR_INVALID_ARG;
+    const bool fast = (d == 32 || d == 64 || d == 128) && (((uintptr_t)g & 15u) == 0);
+    if (fast) {
+        const size_t need = kgq_dequant_gemm_workspace_bytes(rows, d);
+        if (!workspace || workspace_bytes < need) return KGQ_ERR_INVALID_ARG;
+        float *partial = reinterpret_cast<float *>(workspace);
+        int st = KGQ_OK;
+        switch (d) {
+            case 32: st = launch_dq_gemm<32>(bits, codes, ranges, offsets, rows, g, partial, s); break;
+            case 64: st = launch_dq_gemm<64>(bits, codes, ranges, offsets, rows, g, partial, s); break;
+            case 128: st = launch_dq_gemm<128>(bits, codes, ranges, offsets, rows, g, partial, s); break;
+        }
+        if (st != KGQ_OK) return st;
+        const int dd = d * d;
+        reduce_partials_kernel<<<(dd + 255) / 256, 256, 0, s>>>(partial, dq_gemm_grid(rows), dd,
+                                                                dtheta, accumulate);
+    } else {
+        dequant_gemm_generic_kernel<<<(d * d + 255) / 256, 256, 0, s>>>(
+            codes, ranges, offsets, rows, d, bits, g, dtheta, accumulate);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

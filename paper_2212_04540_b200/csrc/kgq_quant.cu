@@ -1,0 +1,538 @@
+// kgq_quant.cu -- fused per-group quantize+pack (K1) and unpack+dequantize (K2)
+// for sm_100a.  Semantics: reference quantize.py:177-247 (see include/kgq.h).
+//
+// Fast kernels (group G in {32,64,128,256}, 16-byte aligned buffers):
+//   * 4 threads per group, 8 groups per warp.  Thread j of a group owns the
+//     float4 j of every 16-element block of the group (element 16i+4j+e), so a
+//     warp-wide 128-bit load covers 8 x 64 contiguous bytes (fully used
+//     sectors), and min/max needs only two xor-shuffles.
+//   * fp32 math reproduces numpy bit-for-bit: a = x - Z, q = a / R (IEEE,
+//     hoisted reciprocal + Markstein correction, kgq_common.cuh), s = q * B,
+//     clip, then the code.  Stochastic rounding uses code = ceil(s - u),
+//     which equals floor(s) + [u < frac] exactly; ceil(s - u) is formed with
+//     round-up FP adds, and the magic constant 1.5*2^23 turns it into an
+//     integer in the low mantissa bits with no F2I conversion.
+//   * Codes are staged per warp in shared memory and leave as coalesced
+//     16-byte stores.  R, Z leave as one fp32 each per group.
+// Generic kernels (any G, any alignment, caller noise): warp per group.
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+constexpr int kWarps = 8;              // warps per CTA
+constexpr int kThreads = kWarps * 32;
+constexpr int kGroupsPerWarp = 8;      // 4 threads per group
+
+// ---------------------------------------------------------------------------
+// K1: fast fused quantize + pack.
+// ---------------------------------------------------------------------------
+template <int G, int BITS, int MODE>
+__global__ void __launch_bounds__(kThreads)
+quantize_t4_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__restrict__ codes,
+                   float *__restrict__ ranges, float *__restrict__ offsets, uint64_t seed,
+                   uint64_t tid, int64_t group_offset) {
+    constexpr int NB = G / 16;                    // float4 per thread
+    constexpr int GB = G * BITS / 8;              // packed bytes per group
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    __shared__ __align__(16) uint8_t stage[kWarps][kGroupsPerWarp * GB];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane & 3, gw = lane >> 2;
+    uint8_t *st = stage[warp];
+    const FastKey fk = make_fast_key(seed, tid);
+
+    const int64_t n_tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    for (int64_t tile = (int64_t)blockIdx.x * kWarps + warp; tile < n_tiles;
+         tile += (int64_t)gridDim.x * kWarps) {
+        const int64_t g = tile * kGroupsPerWarp + gw;
+        const bool valid = g < n_groups;
+        const float4 *src = reinterpret_cast<const float4 *>(x) + (valid ? g : 0) * (G / 4);
+        float4 v[NB];
+#pragma unroll
+        for (int i = 0; i < NB; i++) v[i] = ldg_stream(src + 4 * i + j);
+
+        float mn = fminf(fminf(v[0].x, v[0].y), fminf(v[0].z, v[0].w));
+        float mx = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
+#pragma unroll
+        for (int i = 1; i < NB; i++) {
+            mn = fminf(mn, fminf(fminf(v[i].x, v[i].y), fminf(v[i].z, v[i].w)));
+            mx = fmaxf(mx, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+        }
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float z = mn;
+        const float r = __fsub_rn(mx, mn);
+        const DivR dv = make_div(r);
+        const uint64_t gglob = (uint64_t)(group_offset + g);
+
+        uint32_t piece[NB];   // 4*BITS bits per block (elements 16i+4j .. +3)
+        if (r > 0.0f) {
+#pragma unroll
+            for (int i = 0; i < NB; i += 2) {
+                uint4 rnd = make_uint4(0, 0, 0, 0);
+                if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * (i >> 1) + j));
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int ib = i + h;
+                    if (ib >= NB) break;
+                    u64x4 r64 = {0, 0, 0, 0};
+                    if (MODE == KGQ_ROUND_SR_COMPAT)
+                        r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * ib + j) + 1ull,
+                                            0, 0, 0, seed, tid);
+                    const float xs[4] = {v[ib].x, v[ib].y, v[ib].z, v[ib].w};
+                    const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+                    const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        float s = __fmul_rn(div_a(dv, __fsub_rn(xs[e], z)), Bf);
+                        s = fminf(s, Bf);
+                        const uint32_t u16 = h ? (rw[e] >> 16) : (rw[e] & 0xFFFFu);
+                        acc += code_bits<MODE>(s, u16, cw[e] >> 11) << (BITS * e);
+                    }
+                    piece[ib] = acc - magic_sum4<BITS>();
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NB; i++) piece[i] = 0;   // R == 0 -> scaled 0 -> code 0
+        }
+
+        // stage the packed codes (LSB-first, group-contiguous)
+        uint8_t *gst = st + gw * GB;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            if (BITS == 8) {
+                *reinterpret_cast<uint32_t *>(gst + 16 * i + 4 * j) = piece[i];
+            } else if (BITS == 4) {
+                *reinterpret_cast<uint16_t *>(gst + 8 * i + 2 * j) = (uint16_t)piece[i];
+            } else if (BITS == 2) {
+                gst[4 * i + j] = (uint8_t)piece[i];
+            } else {  // BITS == 1: nibble; pair lanes j, j^1 into one byte
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, piece[i], 1);
+                if ((j & 1) == 0) gst[2 * i + (j >> 1)] = (uint8_t)(piece[i] | (other << 4));
+            }
+        }
+        __syncwarp();
+        const int64_t g0 = tile * kGroupsPerWarp;
+        const int nvalid = (int)imin64(kGroupsPerWarp, n_groups - g0);
+        uint8_t *dst = codes + g0 * GB;
+        const int nbytes = nvalid * GB;
+        if ((nbytes & 15) == 0) {
+            for (int b = lane * 16; b < nbytes; b += 32 * 16)
+                *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
+        } else {
+            for (int b = lane * 4; b < nbytes; b += 32 * 4)
+                *reinterpret_cast<uint32_t *>(dst + b) = *reinterpret_cast<const uint32_t *>(st + b);
+        }
+        if (valid && j == 0) {
+            ranges[g] = r;
+            offsets[g] = z;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 generic: one warp per group, any G / alignment / mode (incl. caller noise).
+// Each lane owns whole output bytes, so no packing races.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, int bits, int mode,
+                        uint64_t seed, uint64_t tid, int64_t group_offset,
+                        const double *__restrict__ noise, uint8_t *__restrict__ codes,
+                        float *__restrict__ ranges, float *__restrict__ offsets) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int GB = (G * bits + 7) / 8;
+    const float Bf = (float)((1u << bits) - 1u);
+    const FastKey fk = make_fast_key(seed, tid);
+    for (int64_t g = warp_id; g < n_groups; g += n_warps) {
+        const float *row = x + g * (int64_t)G;
+        float mn = INFINITY, mx = -INFINITY;
+        for (int k = lane; k < G; k += 32) {
+            mn = fminf(mn, row[k]);
+            mx = fmaxf(mx, row[k]);
+        }
+        mn = warp_min(mn, 32);
+        mx = warp_max(mx, 32);
+        const float z = mn, r = __fsub_rn(mx, mn);
+        const uint64_t gglob = (uint64_t)(group_offset + g);
+        const int per_byte = 8 / bits;
+        for (int bi = lane; bi < GB; bi += 32) {
+            uint32_t byte = 0;
+            for (int t = 0; t < per_byte; t++) {
+                const int k = bi * per_byte + t;
+                if (k >= G) break;
+                uint32_t code = 0;
+                if (r > 0.0f) {
+                    float s = __fmul_rn(__fdiv_rn(__fsub_rn(row[k], z), r), Bf);
+                    s = fminf(fmaxf(s, 0.0f), Bf);
+                    if (mode == KGQ_ROUND_NEAREST) {
+                        code = (uint32_t)rintf(s);
+                    } else {
+                        const float fl = floorf(s);
+                        const float frac = __fsub_rn(s, fl);
+                        double u;
+                        if (mode == KGQ_ROUND_SR_FAST)
+                            u = (double)fast_u16(fk, gglob, k) * (1.0 / 65536.0);
+                        else if (mode == KGQ_ROUND_SR_COMPAT)
+                            u = (double)compat_raw53(seed, tid, gglob, G, k) * 0x1p-53;
+                        else
+                            u = noise[g * (int64_t)G + k];
+                        code = (uint32_t)fl + ((u < (double)frac) ? 1u : 0u);
+                    }
+                }
+                byte |= code << (t * bits);
+            }
+            codes[g * (int64_t)GB + bi] = (uint8_t)byte;
+        }
+        if (lane == 0) {
+            ranges[g] = r;
+            offsets[g] = z;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: fast unpack + dequantize.  out = (R*c)/B + Z (fp32, IEEE), R==0 -> Z.
+// bits <= 4: per-group table of the B+1 reconstruction values in smem
+// (computed once with IEEE division), one LDS per element.
+// bits == 8: arithmetic with the hoisted-reciprocal division.
+// ---------------------------------------------------------------------------
+template <int G, int BITS>
+__global__ void __launch_bounds__(kThreads)
+dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
+                     const float *__restrict__ offsets, int64_t n_groups, float *__restrict__ out) {
+    constexpr int NB = G / 16;
+    constexpr int GB = G * BITS / 8;
+    constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;   // table entries per group
+    constexpr int LS = (NL == 16) ? 17 : NL;            // padded stride (bank spread)
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    __shared__ __align__(16) uint8_t stage[kWarps][kGroupsPerWarp * GB];
+    __shared__ float lut[kWarps][kGroupsPerWarp * LS];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane & 3, gw = lane >> 2;
+    uint8_t *st = stage[warp];
+    float *lt = lut[warp] + gw * LS;
+
+    const int64_t n_tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    for (int64_t tile = (int64_t)blockIdx.x * kWarps + warp; tile < n_tiles;
+         tile += (int64_t)gridDim.x * kWarps) {
+        const int64_t g0 = tile * kGroupsPerWarp;
+        const int nvalid = (int)imin64(kGroupsPerWarp, n_groups - g0);
+        const uint8_t *srcc = codes + g0 * GB;
+        const int nbytes = nvalid * GB;
+        if ((nbytes & 15) == 0) {
+            for (int b = lane * 16; b < nbytes; b += 32 * 16)
+                *reinterpret_cast<uint4 *>(st + b) = __ldg(reinterpret_cast<const uint4 *>(srcc + b));
+        } else {
+            for (int b = lane * 4; b < nbytes; b += 32 * 4)
+                *reinterpret_cast<uint32_t *>(st + b) = __ldg(reinterpret_cast<const uint32_t *>(srcc + b));
+        }
+        const int64_t g = g0 + gw;
+        const bool valid = gw < nvalid;
+        const float r = valid ? __ldg(ranges + g) : 0.f;
+        const float z = valid ? __ldg(offsets + g) : 0.f;
+        if (NL > 1) {
+            for (int c = j; c < NL; c += 4)
+                lt[c] = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+        }
+        __syncwarp();
+        if (valid) {
+            const uint8_t *gst = st + gw * GB;
+            float4 *dst = reinterpret_cast<float4 *>(out) + g * (G / 4);
+            DivR dB;
+            if (BITS == 8) dB = make_div(Bf);
+            const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
+#pragma unroll
+            for (int i = 0; i < NB; i++) {
+                uint32_t piece;
+                if (BITS == 8) piece = *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j);
+                else if (BITS == 4) piece = *reinterpret_cast<const uint16_t *>(gst + 8 * i + 2 * j);
+                else if (BITS == 2) piece = gst[4 * i + j];
+                else piece = (gst[2 * i + (j >> 1)] >> (4 * (j & 1))) & 0xFu;
+                float o[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t c = (piece >> (BITS * e)) & PackInfo<BITS>::B;
+                    if (NL > 1) {
+                        o[e] = lt[c];
+                    } else {
+                        if (r == 0.0f) { o[e] = z; continue; }
+                        const float cf = __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f);
+                        const float t = __fmul_rn(r, cf);
+                        float q;
+                        if (rfast) {
+                            const float q0 = __fmul_rn(t, dB.y);
+                            const float er = __fmaf_rn(-Bf, q0, t);
+                            q = __fmaf_rn(dB.y, er, q0);
+                        } else {
+                            q = __fdiv_rn(t, Bf);
+                        }
+                        o[e] = __fadd_rn(q, z);
+                    }
+                }
+                stg_stream(dst + 4 * i + j, make_float4(o[0], o[1], o[2], o[3]));
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void dequantize_generic_kernel(const uint8_t *__restrict__ codes,
+                                          const float *__restrict__ ranges,
+                                          const float *__restrict__ offsets, int64_t n_groups,
+                                          int G, int bits, float *__restrict__ out) {
+    const int GB = (G * bits + 7) / 8;
+    const float Bf = (float)((1u << bits) - 1u);
+    const uint32_t mask = (1u << bits) - 1u;
+    const int64_t n = n_groups * (int64_t)G;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = idx / G;
+        const int k = (int)(idx - g * G);
+        const int bit = k * bits;
+        const uint32_t c = (codes[g * GB + (bit >> 3)] >> (bit & 7)) & mask;
+        const float r = ranges[g], z = offsets[g];
+        out[idx] = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Noise export (parity seam) and pack/unpack of raw codes.
+// ---------------------------------------------------------------------------
+__global__ void fast_noise_kernel(uint64_t seed, uint64_t tid, int64_t group_offset,
+                                  int64_t n_groups, int G, uint16_t *__restrict__ out) {
+    const FastKey fk = make_fast_key(seed, tid);
+    const int64_t n = n_groups * (int64_t)G;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = idx / G;
+        out[idx] = (uint16_t)fast_u16(fk, (uint64_t)(group_offset + g), (int)(idx - g * G));
+    }
+}
+
+__global__ void compat_noise_kernel(uint64_t seed, uint64_t tid, int64_t group_offset,
+                                    int64_t n_groups, int G, uint64_t *__restrict__ out) {
+    const int64_t n = n_groups * (int64_t)G;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = idx / G;
+        out[idx] = compat_raw53(seed, tid, (uint64_t)(group_offset + g), G, (int)(idx - g * G));
+    }
+}
+
+__global__ void pack_codes_kernel(const uint8_t *__restrict__ codes, int64_t rows, int cols,
+                                  int bits, uint8_t *__restrict__ packed, int32_t *overflow) {
+    const int RB = (cols * bits + 7) / 8;
+    const int per_byte = 8 / bits;
+    const int64_t n = rows * (int64_t)RB;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = idx / RB;
+        const int bi = (int)(idx - row * RB);
+        uint32_t byte = 0;
+        for (int t = 0; t < per_byte; t++) {
+            const int k = bi * per_byte + t;
+            if (k >= cols) break;
+            const uint32_t c = codes[row * cols + k];
+            if (c >> bits) atomicOr(overflow, 1);
+            byte |= (c & ((1u << bits) - 1u)) << (t * bits);
+        }
+        packed[idx] = (uint8_t)byte;
+    }
+}
+
+__global__ void unpack_codes_kernel(const uint8_t *__restrict__ packed, int64_t rows, int cols,
+                                    int bits, uint8_t *__restrict__ codes) {
+    const int RB = (cols * bits + 7) / 8;
+    const int64_t n = rows * (int64_t)cols;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = idx / cols;
+        const int k = (int)(idx - row * cols);
+        const int bit = k * bits;
+        codes[idx] = (uint8_t)((packed[row * RB + (bit >> 3)] >> (bit & 7)) & ((1u << bits) - 1u));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+static inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+static inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm) {
+    int64_t b = (work_items + per_block - 1) / per_block;
+    const int64_t cap = (int64_t)kSMs * max_blocks_per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+template <int G, int BITS, int MODE>
+static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, float *ranges,
+                            float *offsets, uint64_t seed, uint64_t tid, int64_t goff,
+                            cudaStream_t s) {
+    const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    const int grid = grid_for(tiles, kWarps, 8);
+    quantize_t4_kernel<G, BITS, MODE><<<grid, kThreads, 0, s>>>(x, n_groups, codes, ranges,
+                                                               offsets, seed, tid, goff);
+}
+
+template <int G, int BITS>
+static bool dispatch_quant_mode(int mode, const float *x, int64_t n_groups, uint8_t *codes,
+                                float *ranges, float *offsets, uint64_t seed, uint64_t tid,
+                                int64_t goff, cudaStream_t s) {
+    switch (mode) {
+        case KGQ_ROUND_NEAREST:
+            launch_quant_t4<G, BITS, KGQ_ROUND_NEAREST>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            return true;
+        case KGQ_ROUND_SR_FAST:
+            launch_quant_t4<G, BITS, KGQ_ROUND_SR_FAST>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            return true;
+        case KGQ_ROUND_SR_COMPAT:
+            launch_quant_t4<G, BITS, KGQ_ROUND_SR_COMPAT>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            return true;
+        default:
+            return false;
+    }
+}
+
+template <int G>
+static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_groups,
+                                uint8_t *codes, float *ranges, float *offsets, uint64_t seed,
+                                uint64_t tid, int64_t goff, cudaStream_t s) {
+    switch (bits) {
+        case 1: return dispatch_quant_mode<G, 1>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+        case 2: return dispatch_quant_mode<G, 2>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+        case 4: return dispatch_quant_mode<G, 4>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+        case 8: return dispatch_quant_mode<G, 8>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+    }
+    return false;
+}
+
+template <int G>
+static bool dispatch_dequant_bits(int bits, const uint8_t *codes, const float *ranges,
+                                  const float *offsets, int64_t n_groups, float *out,
+                                  cudaStream_t s) {
+    const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    const int grid = grid_for(tiles, kWarps, 8);
+    switch (bits) {
+        case 1: dequantize_t4_kernel<G, 1><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 2: dequantize_t4_kernel<G, 2><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 4: dequantize_t4_kernel<G, 4><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 8: dequantize_t4_kernel<G, 8><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+    }
+    return false;
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+static inline bool bits_ok(int bits) { return bits == 1 || bits == 2 || bits == 4 || bits == 8; }
+
+extern "C" int kgq_quantize_f32(const float *x, int64_t n_groups, int32_t group, int32_t bits,
+                                int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                                int64_t group_offset, const double *noise, uint8_t *codes,
+                                float *ranges, float *offsets, void *stream) {
+    if (!bits_ok(bits)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (group < 1 || n_groups < 0 || rounding < 0 || rounding > 3 || group_offset < 0)
+        return KGQ_ERR_INVALID_ARG;
+    if (rounding == KGQ_ROUND_SR_NOISE && !noise) return KGQ_ERR_INVALID_ARG;
+    if (n_groups == 0) return KGQ_OK;
+    if (!x || !codes || !ranges || !offsets) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool fast_ok = rounding != KGQ_ROUND_SR_NOISE && aligned16(x) && aligned16(codes) &&
+                         (group == 32 || group == 64 || group == 128 || group == 256);
+    bool done = false;
+    if (fast_ok) {
+        switch (group) {
+            case 32: done = dispatch_quant_bits<32>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
+            case 64: done = dispatch_quant_bits<64>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
+            case 128: done = dispatch_quant_bits<128>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
+            case 256: done = dispatch_quant_bits<256>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
+        }
+    }
+    if (!done) {
+        const int grid = grid_for(n_groups, kWarps, 8);
+        quantize_generic_kernel<<<grid, kThreads, 0, s>>>(x, n_groups, group, bits, rounding, seed,
+                                                          tensor_id, group_offset, noise, codes,
+                                                          ranges, offsets);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_dequantize_f32(const uint8_t *codes, const float *ranges, const float *offsets,
+                                  int64_t n_groups, int32_t group, int32_t bits, float *out,
+                                  void *stream) {
+    if (!bits_ok(bits)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (group < 1 || n_groups < 0) return KGQ_ERR_INVALID_ARG;
+    if (n_groups == 0) return KGQ_OK;
+    if (!codes || !ranges || !offsets || !out) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool fast_ok = aligned16(codes) && aligned16(out) &&
+                         (group == 32 || group == 64 || group == 128 || group == 256);
+    bool done = false;
+    if (fast_ok) {
+        switch (group) {
+            case 32: done = dispatch_dequant_bits<32>(bits, codes, ranges, offsets, n_groups, out, s); break;
+            case 64: done = dispatch_dequant_bits<64>(bits, codes, ranges, offsets, n_groups, out, s); break;
+            case 128: done = dispatch_dequant_bits<128>(bits, codes, ranges, offsets, n_groups, out, s); break;
+            case 256: done = dispatch_dequant_bits<256>(bits, codes, ranges, offsets, n_groups, out, s); break;
+        }
+    }
+    if (!done) {
+        const int grid = grid_for(n_groups * (int64_t)group, 256, 8);
+        dequantize_generic_kernel<<<grid, 256, 0, s>>>(codes, ranges, offsets, n_groups, group, bits, out);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_fast_noise_u16(uint64_t seed, uint64_t tensor_id, int64_t group_offset,
+                                  int64_t n_groups, int32_t group, uint16_t *out, void *stream) {
+    if (group < 1 || n_groups < 0 || group_offset < 0 || (!out && n_groups)) return KGQ_ERR_INVALID_ARG;
+    if (n_groups == 0) return KGQ_OK;
+    const int grid = grid_for(n_groups * (int64_t)group, 256, 8);
+    fast_noise_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, tensor_id, group_offset, n_groups, group, out);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_compat_noise_raw53(uint64_t seed, uint64_t tensor_id, int64_t group_offset,
+                                      int64_t n_groups, int32_t group, uint64_t *out, void *stream) {
+    if (group < 1 || n_groups < 0 || group_offset < 0 || (!out && n_groups)) return KGQ_ERR_INVALID_ARG;
+    if (n_groups == 0) return KGQ_OK;
+    const int grid = grid_for(n_groups * (int64_t)group, 256, 8);
+    compat_noise_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, tensor_id, group_offset, n_groups, group, out);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_pack_codes(const uint8_t *codes, int64_t rows, int32_t cols, int32_t bits,
+                              uint8_t *packed, int32_t *overflow, void *stream) {
+    if (!bits_ok(bits)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (rows < 0 || cols < 0 || !overflow) return KGQ_ERR_INVALID_ARG;
+    if (rows == 0 || cols == 0) return KGQ_OK;
+    const int64_t n = rows * (int64_t)((cols * bits + 7) / 8);
+    pack_codes_kernel<<<grid_for(n, 256, 8), 256, 0, (cudaStream_t)stream>>>(codes, rows, cols, bits, packed, overflow);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_unpack_codes(const uint8_t *packed, int64_t rows, int32_t cols, int32_t bits,
+                                uint8_t *codes, void *stream) {
+    if (!bits_ok(bits)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (rows < 0 || cols < 0) return KGQ_ERR_INVALID_ARG;
+    if (rows == 0 || cols == 0) return KGQ_OK;
+    unpack_codes_kernel<<<grid_for(rows * (int64_t)cols, 256, 8), 256, 0, (cudaStream_t)stream>>>(packed, rows, cols, bits, codes);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -1,0 +1,227 @@
+"""GPU parity of the fused quantize/pack (K1) and unpack/dequantize (K2) kernels.
+
+Bit-exact against (a) golden fixtures produced by the reference itself and
+(b) the CPU oracle on larger seeded inputs, through the C ABI (libkgq.so).
+Full-size (BASELINE configs[1]) behaviour is checked through size-independent
+properties.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+RNG_OF_MODE = {0: "fast", 1: "fast", 2: "compat"}
+
+
+def _kgq():
+    import paper_2212_04540_b200 as kgq
+    return kgq
+
+
+def _cfg(kgq, group, bits, mode, per_row):
+    rounding = "nearest" if mode == 0 else "stochastic"
+    return kgq.QuantConfig(bits=bits, rounding=rounding, group=None if per_row else group,
+                           rng=RNG_OF_MODE[mode])
+
+
+def _to_dev(x, misalign=False):
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    if misalign:  # force the generic (unaligned) kernels
+        buf = torch.empty(t.numel() + 1, dtype=torch.float32, device="cuda")
+        buf[1:] = t.reshape(-1)
+        t = buf[1:].view(t.shape)
+    return t
+
+
+def _assert_q_equal(q, codes, ranges, offsets):
+    assert np.array_equal(q.codes.cpu().numpy(), codes)
+    assert np.array_equal(q.ranges.cpu().numpy().view(np.uint32), np.asarray(ranges).view(np.uint32))
+    assert np.array_equal(q.offsets.cpu().numpy().view(np.uint32), np.asarray(offsets).view(np.uint32))
+
+
+@pytest.mark.parametrize("misalign", [False, True], ids=["fast", "generic"])
+@pytest.mark.parametrize("case", list(golden_io.quant_cases()), ids=lambda c: f"c{c['idx']}")
+def test_quantize_matches_reference_golden(case, misalign):
+    kgq = _kgq()
+    per_row = case["group"] == case["x"].shape[1]
+    x = case["x"] if per_row else case["x"].reshape(-1, case["group"])
+    xt = _to_dev(x, misalign)
+    cfg = _cfg(kgq, case["group"], case["bits"], case["mode"], True)
+    q = kgq.quantize_tensor(xt, cfg, kgq.RandomStream(case["seed"]), tensor_id=case["tid"])
+    _assert_q_equal(q, case["codes"], case["ranges"], case["offsets"])
+    assert kgq.stored_bytes(q) == case["stored_bytes"]
+    deq = kgq.dequantize_tensor(q)
+    assert np.array_equal(deq.cpu().numpy().view(np.uint32),
+                          case["deq"].reshape(deq.shape).view(np.uint32))
+
+
+@pytest.mark.parametrize("case", [c for c in golden_io.quant_cases() if c["mode"] == 1],
+                         ids=lambda c: f"c{c['idx']}")
+def test_exported_noise_route(case):
+    """Fast-mode codes == reference fed the exported fast noise (the fixture),
+    and the caller-noise kernel reproduces them from the exported draws."""
+    kgq = _kgq()
+    x = case["x"].reshape(-1, case["group"])
+    u16 = kgq.fast_noise_u16(case["seed"], case["tid"], x.shape[0], x.shape[1])
+    assert np.array_equal(u16.cpu().numpy(),
+                          orc.fast_noise_u16(case["seed"], case["tid"], x.shape[0], x.shape[1]))
+    noise = u16.to(torch.float64) / 65536.0
+    q = kgq.quantize_tensor(_to_dev(x), kgq.QuantConfig(bits=case["bits"]), noise=noise)
+    _assert_q_equal(q, case["codes"], case["ranges"], case["offsets"])
+
+
+def test_compat_noise_equals_numpy_stream():
+    kgq = _kgq()
+    z = golden_io.load("philox")
+    for i in range(int(z["n_keys"])):
+        seed, tid = (int(v) for v in z[f"k{i}_key"])
+        u = kgq.RandomStream(seed).matrix_uniforms(tid, 5, 13)
+        assert np.array_equal(u.cpu().numpy(), z[f"k{i}_matrix_uniforms"])
+
+
+def _edge_big(rows, cols, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((rows, cols), dtype=np.float32)
+    x[::97] = x[::97, :1]
+    x[::89] *= np.float32(1e-30)
+    x[5::101] = np.abs(x[5::101])
+    x[5::101, ::2] = 0.0
+    x[7::103] *= np.float32(1e30)
+    return x
+
+
+@pytest.mark.parametrize("cols,group", [(64, None), (128, None), (128, 64), (256, None), (256, 128),
+                                        (64, 256), (32, None)])
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("mode", [0, 1, 2], ids=["nearest", "fast", "compat"])
+def test_quantize_matches_oracle_large(cols, group, bits, mode):
+    kgq = _kgq()
+    rows = 1 << 15 if cols <= 64 else 1 << 14
+    x = _edge_big(rows, cols, 17 + cols + bits)
+    G = cols if group is None else group
+    cfg = kgq.QuantConfig(bits=bits, rounding="nearest" if mode == 0 else "stochastic", group=group,
+                          rng=RNG_OF_MODE[mode])
+    seed, tid = 0xDEADBEEF12345678, 2 ** 33 + 7
+    q = kgq.quantize_tensor(_to_dev(x), cfg, kgq.RandomStream(seed), tensor_id=tid)
+    codes, ranges, offsets = orc.quantize(x.reshape(-1, G), G, bits, mode, seed, tid, threads=8)
+    _assert_q_equal(q, codes, ranges, offsets)
+    deq = kgq.dequantize_tensor(q).cpu().numpy().reshape(-1, G)
+    ref = orc.dequantize(codes, ranges, offsets, G, bits, threads=8)
+    assert np.array_equal(deq.view(np.uint32), ref.view(np.uint32))
+
+
+def test_group_offset_sharding_is_byte_identical():
+    """Row-partitioned quantization (multi-GPU) gives the same bytes."""
+    kgq = _kgq()
+    x = _to_dev(_edge_big(4096, 64, 3))
+    st = kgq.RandomStream(5)
+    for rng in ("fast", "compat"):
+        cfg = kgq.QuantConfig(bits=2, rng=rng)
+        full = kgq.quantize_tensor(x, cfg, st, tensor_id=9)
+        for lo, hi in [(0, 1000), (1000, 1001), (1001, 4096)]:
+            part = kgq.quantize_tensor(x[lo:hi], cfg, st, tensor_id=9, group_offset=lo)
+            assert torch.equal(part.codes, full.codes[lo:hi])
+            assert torch.equal(part.ranges, full.ranges[lo:hi])
+
+
+def test_quantize_row_matches_matrix_rows():
+    """test_quantize.py:102-110 on GPU: row stream == matrix stream."""
+    kgq = _kgq()
+    x = _to_dev(np.random.default_rng(2).standard_normal((37, 13)).astype(np.float32))
+    for rng in ("fast", "compat"):
+        cfg = kgq.QuantConfig(bits=2, rng=rng)
+        q = kgq.quantize_tensor(x, cfg, kgq.RandomStream(9), tensor_id=5)
+        unpacked = kgq.unpack_codes(q.codes, 2, 13)
+        for row in np.random.default_rng(3).permutation(37)[:10]:
+            codes, _, _ = kgq.quantize_row(x[row], cfg, kgq.RandomStream(9), tensor_id=5, row=int(row))
+            assert torch.equal(codes, unpacked[row])
+
+
+def test_pack_unpack_known_answers_and_errors():
+    kgq = _kgq()
+    assert int(kgq.pack_bits([1, 0, 1, 1, 0, 0, 0, 0], 1)[0]) == 0x0D
+    assert int(kgq.pack_bits([3, 2, 1, 0], 2)[0]) == 0x1B
+    with pytest.raises(kgq.EncodingError):
+        kgq.pack_bits([4], 2)
+    with pytest.raises(kgq.EncodingError):
+        kgq.pack_codes(torch.zeros((2, 2), dtype=torch.uint8, device="cuda"), 3)
+    rng = np.random.default_rng(6)
+    for _ in range(50):
+        bits = int(rng.choice([1, 2, 4, 8]))
+        n = int(rng.integers(1, 64))
+        c = torch.from_numpy(rng.integers(0, 1 << bits, (24, n)).astype(np.uint8)).cuda()
+        assert torch.equal(kgq.unpack_codes(kgq.pack_codes(c, bits), bits, n), c)
+
+
+def test_errors_match_reference_classes():
+    kgq = _kgq()
+    with pytest.raises(ValueError):
+        kgq.QuantConfig(bits=3)
+    with pytest.raises(ValueError):
+        kgq.QuantConfig(rounding="up")
+    x = torch.zeros((4, 8), device="cuda")
+    with pytest.raises(ValueError):   # SR without a stream, quantize.py:189-190
+        kgq.quantize_tensor(x, kgq.QuantConfig(bits=2))
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=32))
+    assert kgq.dequantize_tensor(q) is x      # pass-through is the raw tensor
+    with pytest.raises(ValueError):
+        kgq.quantize_tensor(torch.zeros((3, 8), device="cuda"), kgq.QuantConfig(bits=2, group=16),
+                            kgq.RandomStream(0))
+    with pytest.raises(ValueError):
+        kgq.quantize_tensor(torch.zeros((3, 8)), kgq.QuantConfig(bits=2), kgq.RandomStream(0))
+
+
+def test_empty_and_tiny_inputs():
+    kgq = _kgq()
+    st = kgq.RandomStream(1)
+    q = kgq.quantize_tensor(torch.zeros((0, 64), device="cuda"), kgq.QuantConfig(bits=2), st)
+    assert q.codes.shape == (0, 16) and kgq.dequantize_tensor(q).shape == (0, 64)
+    x = torch.tensor([[4.2, 4.2, 4.2]], device="cuda")
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=2), st)
+    assert q.codes.cpu().tolist() == [[0]] and float(q.ranges[0]) == 0.0
+    assert torch.equal(kgq.dequantize_tensor(q), x)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_full_size_properties(bits):
+    """BASELINE configs[1] shapes (64M x 128 is 32 GB fp32): bounds, codes
+    range, determinism, unbiasedness and a sampled oracle check."""
+    kgq = _kgq()
+    free, _ = torch.cuda.mem_get_info()
+    rows, cols = (64 << 20, 128) if free > 100e9 else (16 << 20, 128)
+    g = torch.Generator(device="cuda").manual_seed(bits)
+    x = torch.randn((rows, cols), device="cuda", generator=g)
+    cfg = kgq.QuantConfig(bits=bits, group=64)
+    st = kgq.RandomStream(11)
+    q = kgq.quantize_tensor(x, cfg, st, tensor_id=3)
+    q2 = kgq.quantize_tensor(x, cfg, st, tensor_id=3)
+    assert torch.equal(q.codes, q2.codes)
+    del q2
+    B = (1 << bits) - 1
+    # sample 4096 groups spread over the tensor and compare with the oracle
+    n_groups = rows * cols // 64
+    idx = torch.linspace(0, n_groups - 1, 4096, device="cuda").long()
+    xs = x.view(-1, 64)[idx].cpu().numpy()
+    for k, gi in enumerate(idx.cpu().numpy()[:64]):
+        c, r, o = orc.quantize(xs[k:k + 1], 64, bits, orc.MODE_SR_FAST, 11, 3, group_offset=int(gi))
+        assert np.array_equal(q.codes[gi].cpu().numpy(), c[0])
+    # chunked checks on the dequantized tensor (bounded memory)
+    chunk = 1 << 22
+    err_sum = 0.0
+    for s in range(0, n_groups, chunk):
+        sl = slice(s, min(n_groups, s + chunk))
+        sub = kgq.QuantizedTensor(sl.stop - sl.start, 64, bits, q.codes[sl], q.ranges[sl], q.offsets[sl])
+        deq = kgq.dequantize_tensor(sub)
+        xv = x.view(-1, 64)[sl]
+        r = q.ranges[sl][:, None]
+        z = q.offsets[sl][:, None]
+        assert bool((deq >= z).all()) and bool((deq <= z + r * (1 + 1e-6)).all())
+        assert bool(((deq - xv).abs() <= r / B * (1 + 1e-5) + 1e-30).all())
+        err_sum += float(((deq - xv) / torch.clamp(r, min=1e-30)).double().sum())
+    # unbiased SR: mean normalized error ~ 0 (sigma <= 1/(2B sqrt(n)))
+    n = rows * cols
+    assert abs(err_sum / n) < 6.0 / (2 * B * np.sqrt(n))
