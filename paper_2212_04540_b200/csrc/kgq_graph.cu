@@ -218,8 +218,7 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
             const int k = lane + 32 * c;
             uint32_t code = 0;
             if (r > 0.0f) {
-                float s = __fmul_rn(div_a(dv, __fsub_rn(h[c], z)), Bf);
-                s = fminf(s, Bf);
+                const float s = __fmul_rn(div_a(dv, __fsub_rn(h[c], z)), Bf);
                 uint32_t u16 = 0;
                 uint64_t raw53 = 0;
                 if (MODE == KGQ_ROUND_SR_FAST) {
@@ -238,7 +237,7 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
                 } else if (MODE == KGQ_ROUND_SR_COMPAT) {
                     raw53 = compat_raw53(seed, tid, gglob, d, k);
                 }
-                code = code_bits<MODE>(s, u16, raw53) - kMagicBits;
+                code = code_bits<MODE>(s, __uint2float_rn(u16), raw53) - kMagicBits;
             } else if (MODE == KGQ_ROUND_SR_FAST) {
                 // keep the shuffles convergent: nothing to do, code stays 0
             }

@@ -23,6 +23,42 @@ constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;
 constexpr int kGroupsPerWarp = 8;      // 4 threads per group
 
+// Codes of the NB float4 a thread owns, packed 4*BITS bits per float4.
+// GUARD=false: the group passed group_div_unguarded (no per-element check).
+template <int NB, int G, int BITS, int MODE, bool GUARD>
+__device__ __forceinline__ void quant_pieces(const float4 (&v)[NB], float z, const DivR &dv,
+                                             const FastKey &fk, uint64_t gglob, int j,
+                                             uint64_t seed, uint64_t tid, uint32_t (&piece)[NB]) {
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+#pragma unroll
+    for (int i = 0; i < NB; i += 2) {
+        uint4 rnd = make_uint4(0, 0, 0, 0);
+        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * (i >> 1) + j));
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int ib = i + h;
+            if (ib >= NB) break;
+            u64x4 r64 = {0, 0, 0, 0};
+            if (MODE == KGQ_ROUND_SR_COMPAT)
+                r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * ib + j) + 1ull,
+                                    0, 0, 0, seed, tid);
+            const float xs[4] = {v[ib].x, v[ib].y, v[ib].z, v[ib].w};
+            const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+            const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
+            uint32_t acc = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const float a = __fsub_rn(xs[e], z);
+                const float q = GUARD ? div_a(dv, a) : div_a_unguarded(dv, a);
+                const float s = __fmul_rn(q, Bf);
+                const float uf = h ? __uint2float_rn(rw[e] >> 16) : __uint2float_rn(rw[e] & 0xFFFFu);
+                acc += code_bits<MODE>(s, uf, cw[e] >> 11) << (BITS * e);
+            }
+            piece[ib] = acc - magic_sum4<BITS>();
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K1: fast fused quantize + pack.
 // ---------------------------------------------------------------------------
@@ -33,8 +69,14 @@ quantize_t4_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__res
                    uint64_t tid, int64_t group_offset) {
     constexpr int NB = G / 16;                    // float4 per thread
     constexpr int GB = G * BITS / 8;              // packed bytes per group
-    constexpr float Bf = (float)PackInfo<BITS>::B;
+    // cp.async prefetch depth: each lane streams its own float4s for the next
+    // S-1 tiles into private shared-memory slots (no cross-lane sharing, so
+    // no barriers), keeping 2-5 tiles of loads in flight per warp without
+    // holding them in registers.  48 KB static smem per CTA at most.
+    constexpr int S = (NB <= 4) ? 12 / NB : 1;
     __shared__ __align__(16) uint8_t stage[kWarps][kGroupsPerWarp * GB];
+    extern __shared__ __align__(16) float4 pf_raw[];   // [kWarps][S][NB][32], dynamic
+    auto pf = reinterpret_cast<float4 (*)[S > 1 ? S : 1][NB][32]>(pf_raw);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane & 3, gw = lane >> 2;
@@ -42,14 +84,40 @@ quantize_t4_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__res
     const FastKey fk = make_fast_key(seed, tid);
 
     const int64_t n_tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
-    for (int64_t tile = (int64_t)blockIdx.x * kWarps + warp; tile < n_tiles;
-         tile += (int64_t)gridDim.x * kWarps) {
+    const int64_t stride = (int64_t)gridDim.x * kWarps;
+    const int64_t tile0 = (int64_t)blockIdx.x * kWarps + warp;
+    auto src_of = [&](int64_t t) {
+        const int64_t g = t * kGroupsPerWarp + gw;
+        return reinterpret_cast<const float4 *>(x) + (g < n_groups ? g : 0) * (G / 4);
+    };
+    auto issue = [&](int64_t t, int s) {   // one commit group per tile (possibly empty)
+        if (S > 1 && t < n_tiles) {
+            const float4 *src = src_of(t);
+#pragma unroll
+            for (int i = 0; i < NB; i++) cp_async16(&pf[S > 1 ? warp : 0][s][i][lane], src + 4 * i + j);
+        }
+        cp_async_commit();
+    };
+    if (S > 1) {
+#pragma unroll
+        for (int k = 0; k < S - 1; k++) issue(tile0 + k * stride, k);
+    }
+    int cur = 0;
+    for (int64_t tile = tile0; tile < n_tiles; tile += stride) {
         const int64_t g = tile * kGroupsPerWarp + gw;
         const bool valid = g < n_groups;
-        const float4 *src = reinterpret_cast<const float4 *>(x) + (valid ? g : 0) * (G / 4);
         float4 v[NB];
+        if (S > 1) {
+            cp_async_wait<S - 2>();
 #pragma unroll
-        for (int i = 0; i < NB; i++) v[i] = ldg_stream(src + 4 * i + j);
+            for (int i = 0; i < NB; i++) v[i] = pf[warp][cur][i][lane];
+            issue(tile + (S - 1) * stride, cur == 0 ? S - 1 : cur - 1);
+            cur = (cur + 1 == S) ? 0 : cur + 1;
+        } else {
+            const float4 *src = src_of(tile);
+#pragma unroll
+            for (int i = 0; i < NB; i++) v[i] = ldg_stream(src + 4 * i + j);
+        }
 
         float mn = fminf(fminf(v[0].x, v[0].y), fminf(v[0].z, v[0].w));
         float mx = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
@@ -69,32 +137,10 @@ quantize_t4_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__res
 
         uint32_t piece[NB];   // 4*BITS bits per block (elements 16i+4j .. +3)
         if (r > 0.0f) {
-#pragma unroll
-            for (int i = 0; i < NB; i += 2) {
-                uint4 rnd = make_uint4(0, 0, 0, 0);
-                if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * (i >> 1) + j));
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const int ib = i + h;
-                    if (ib >= NB) break;
-                    u64x4 r64 = {0, 0, 0, 0};
-                    if (MODE == KGQ_ROUND_SR_COMPAT)
-                        r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * ib + j) + 1ull,
-                                            0, 0, 0, seed, tid);
-                    const float xs[4] = {v[ib].x, v[ib].y, v[ib].z, v[ib].w};
-                    const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
-                    const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
-                    uint32_t acc = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        float s = __fmul_rn(div_a(dv, __fsub_rn(xs[e], z)), Bf);
-                        s = fminf(s, Bf);
-                        const uint32_t u16 = h ? (rw[e] >> 16) : (rw[e] & 0xFFFFu);
-                        acc += code_bits<MODE>(s, u16, cw[e] >> 11) << (BITS * e);
-                    }
-                    piece[ib] = acc - magic_sum4<BITS>();
-                }
-            }
+            if (group_div_unguarded(dv, z))
+                quant_pieces<NB, G, BITS, MODE, false>(v, z, dv, fk, gglob, j, seed, tid, piece);
+            else
+                quant_pieces<NB, G, BITS, MODE, true>(v, z, dv, fk, gglob, j, seed, tid, piece);
         } else {
 #pragma unroll
             for (int i = 0; i < NB; i++) piece[i] = 0;   // R == 0 -> scaled 0 -> code 0
@@ -203,16 +249,78 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
 // (computed once with IEEE division), one LDS per element.
 // bits == 8: arithmetic with the hoisted-reciprocal division.
 // ---------------------------------------------------------------------------
+// (R*c)/B + Z for one code (R == 0 -> Z), IEEE: hoisted RN(1/B) + Markstein
+// correction (t = R*c is 0 or in [2^-100, 2^108] when R is in the window).
+template <int BITS>
+__device__ __forceinline__ float lut_entry(float r, float z, int c) {
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    constexpr float yB = 1.0f / Bf;            // RN(1/B), exact constant folding
+    if (r == 0.0f) return z;
+    const float t = __fmul_rn(r, (float)c);
+    float qv;
+    if (r >= 0x1p-100f && r <= 0x1p100f) {
+        const float q0 = __fmul_rn(t, yB);
+        const float er = __fmaf_rn(-Bf, q0, t);
+        qv = __fmaf_rn(yB, er, q0);
+    } else {
+        qv = __fdiv_rn(t, Bf);
+    }
+    return __fadd_rn(qv, z);
+}
+
+// Per-group outputs of one warp tile (8 groups) from staged codes + table.
+template <int G, int BITS>
+__device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const float *lt, float r, float z,
+                                                   float4 *dst, int j) {
+    constexpr int NB = G / 16;
+    constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    DivR dB;
+    if (BITS == 8) dB = make_div(Bf);
+    const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        uint32_t piece;
+        if (BITS == 8) piece = *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j);
+        else if (BITS == 4) piece = *reinterpret_cast<const uint16_t *>(gst + 8 * i + 2 * j);
+        else if (BITS == 2) piece = gst[4 * i + j];
+        else piece = (gst[2 * i + (j >> 1)] >> (4 * (j & 1))) & 0xFu;
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const uint32_t c = (piece >> (BITS * e)) & PackInfo<BITS>::B;
+            if (NL > 1) {
+                o[e] = lt[c];
+            } else {
+                if (r == 0.0f) { o[e] = z; continue; }
+                const float cf = __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f);
+                const float t = __fmul_rn(r, cf);
+                float qv;
+                if (rfast) {
+                    const float q0 = __fmul_rn(t, dB.y);
+                    const float er = __fmaf_rn(-Bf, q0, t);
+                    qv = __fmaf_rn(dB.y, er, q0);
+                } else {
+                    qv = __fdiv_rn(t, Bf);
+                }
+                o[e] = __fadd_rn(qv, z);
+            }
+        }
+        stg_stream(dst + 4 * i + j, make_float4(o[0], o[1], o[2], o[3]));
+    }
+}
+
 template <int G, int BITS>
 __global__ void __launch_bounds__(kThreads)
 dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
                      const float *__restrict__ offsets, int64_t n_groups, float *__restrict__ out) {
-    constexpr int NB = G / 16;
     constexpr int GB = G * BITS / 8;
+    constexpr int TB = kGroupsPerWarp * GB;             // code bytes per warp tile
+    constexpr int NCH = TB / 16;                        // uint4 chunks per tile
+    constexpr int CPL = (NCH + 31) / 32;                // chunks per lane
     constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;   // table entries per group
     constexpr int LS = (NL == 16) ? 17 : NL;            // padded stride (bank spread)
-    constexpr float Bf = (float)PackInfo<BITS>::B;
-    __shared__ __align__(16) uint8_t stage[kWarps][kGroupsPerWarp * GB];
+    __shared__ __align__(16) uint8_t stage[kWarps][TB];
     __shared__ float lut[kWarps][kGroupsPerWarp * LS];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -220,67 +328,56 @@ dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict_
     uint8_t *st = stage[warp];
     float *lt = lut[warp] + gw * LS;
 
-    const int64_t n_tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
-    for (int64_t tile = (int64_t)blockIdx.x * kWarps + warp; tile < n_tiles;
-         tile += (int64_t)gridDim.x * kWarps) {
-        const int64_t g0 = tile * kGroupsPerWarp;
-        const int nvalid = (int)imin64(kGroupsPerWarp, n_groups - g0);
-        const uint8_t *srcc = codes + g0 * GB;
-        const int nbytes = nvalid * GB;
-        if ((nbytes & 15) == 0) {
-            for (int b = lane * 16; b < nbytes; b += 32 * 16)
-                *reinterpret_cast<uint4 *>(st + b) = __ldg(reinterpret_cast<const uint4 *>(srcc + b));
-        } else {
-            for (int b = lane * 4; b < nbytes; b += 32 * 4)
-                *reinterpret_cast<uint32_t *>(st + b) = __ldg(reinterpret_cast<const uint32_t *>(srcc + b));
-        }
-        const int64_t g = g0 + gw;
-        const bool valid = gw < nvalid;
-        const float r = valid ? __ldg(ranges + g) : 0.f;
-        const float z = valid ? __ldg(offsets + g) : 0.f;
+    const int64_t n_full = n_groups / kGroupsPerWarp;   // full tiles (software-pipelined)
+    const int64_t stride = (int64_t)gridDim.x * kWarps;
+    int64_t tile = (int64_t)blockIdx.x * kWarps + warp;
+
+    // prefetch registers: this lane's code chunks + its group's (R, Z)
+    uint4 cw[CPL];
+    float r_n = 0.f, z_n = 0.f;
+    auto prefetch = [&](int64_t t) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(codes + t * TB);
+#pragma unroll
+        for (int k = 0; k < CPL; k++)
+            if (lane + 32 * k < NCH) cw[k] = __ldg(src + lane + 32 * k);
+        r_n = __ldg(ranges + t * kGroupsPerWarp + gw);
+        z_n = __ldg(offsets + t * kGroupsPerWarp + gw);
+    };
+    if (tile < n_full) prefetch(tile);
+    for (; tile < n_full; tile += stride) {
+#pragma unroll
+        for (int k = 0; k < CPL; k++)
+            if (lane + 32 * k < NCH) reinterpret_cast<uint4 *>(st)[lane + 32 * k] = cw[k];
+        const float r = r_n, z = z_n;
         if (NL > 1) {
-            for (int c = j; c < NL; c += 4)
-                lt[c] = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+#pragma unroll
+            for (int c = j; c < NL; c += 4) lt[c] = lut_entry<BITS>(r, z, c);
+        }
+        // prefetch after the table: a slow-path division call would otherwise
+        // force the in-flight loads to retire
+        if (tile + stride < n_full) prefetch(tile + stride);
+        __syncwarp();
+        const int64_t g = tile * kGroupsPerWarp + gw;
+        dequant_tile_store<G, BITS>(st + gw * GB, lt, r, z, reinterpret_cast<float4 *>(out) + g * (G / 4), j);
+        __syncwarp();
+    }
+    // the last partial tile (at most one in the grid)
+    if (n_groups % kGroupsPerWarp && (int64_t)blockIdx.x * kWarps + warp == n_full % stride) {
+        const int64_t g0 = n_full * kGroupsPerWarp;
+        const int nvalid = (int)(n_groups - g0);
+        const uint8_t *srcc = codes + g0 * GB;
+        for (int b = lane * 4; b < nvalid * GB; b += 32 * 4)
+            *reinterpret_cast<uint32_t *>(st + b) = __ldg(reinterpret_cast<const uint32_t *>(srcc + b));
+        const bool valid = gw < nvalid;
+        const float r = valid ? __ldg(ranges + g0 + gw) : 0.f;
+        const float z = valid ? __ldg(offsets + g0 + gw) : 0.f;
+        if (NL > 1) {
+            for (int c = j; c < NL; c += 4) lt[c] = lut_entry<BITS>(r, z, c);
         }
         __syncwarp();
-        if (valid) {
-            const uint8_t *gst = st + gw * GB;
-            float4 *dst = reinterpret_cast<float4 *>(out) + g * (G / 4);
-            DivR dB;
-            if (BITS == 8) dB = make_div(Bf);
-            const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
-#pragma unroll
-            for (int i = 0; i < NB; i++) {
-                uint32_t piece;
-                if (BITS == 8) piece = *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j);
-                else if (BITS == 4) piece = *reinterpret_cast<const uint16_t *>(gst + 8 * i + 2 * j);
-                else if (BITS == 2) piece = gst[4 * i + j];
-                else piece = (gst[2 * i + (j >> 1)] >> (4 * (j & 1))) & 0xFu;
-                float o[4];
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const uint32_t c = (piece >> (BITS * e)) & PackInfo<BITS>::B;
-                    if (NL > 1) {
-                        o[e] = lt[c];
-                    } else {
-                        if (r == 0.0f) { o[e] = z; continue; }
-                        const float cf = __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f);
-                        const float t = __fmul_rn(r, cf);
-                        float q;
-                        if (rfast) {
-                            const float q0 = __fmul_rn(t, dB.y);
-                            const float er = __fmaf_rn(-Bf, q0, t);
-                            q = __fmaf_rn(dB.y, er, q0);
-                        } else {
-                            q = __fdiv_rn(t, Bf);
-                        }
-                        o[e] = __fadd_rn(q, z);
-                    }
-                }
-                stg_stream(dst + 4 * i + j, make_float4(o[0], o[1], o[2], o[3]));
-            }
-        }
-        __syncwarp();
+        if (valid)
+            dequant_tile_store<G, BITS>(st + gw * GB, lt, r, z,
+                                        reinterpret_cast<float4 *>(out) + (g0 + gw) * (G / 4), j);
     }
 }
 
@@ -380,8 +477,21 @@ static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, fl
                             cudaStream_t s) {
     const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
     const int grid = grid_for(tiles, kWarps, 8);
-    quantize_t4_kernel<G, BITS, MODE><<<grid, kThreads, 0, s>>>(x, n_groups, codes, ranges,
-                                                               offsets, seed, tid, goff);
+    constexpr int NB = G / 16;
+    constexpr int S = (NB <= 4) ? 12 / NB : 1;
+    const size_t smem = S > 1 ? (size_t)kWarps * S * NB * 32 * sizeof(float4) : 0;
+    if (smem > 48 * 1024) {
+        static unsigned attr_set = 0;   // per template instance, bit per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set & (1u << (dev & 31)))) {
+            cudaFuncSetAttribute(quantize_t4_kernel<G, BITS, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set |= 1u << (dev & 31);
+        }
+    }
+    quantize_t4_kernel<G, BITS, MODE><<<grid, kThreads, smem, s>>>(x, n_groups, codes, ranges,
+                                                                  offsets, seed, tid, goff);
 }
 
 template <int G, int BITS>

@@ -1,0 +1,137 @@
+"""Stateless hot-path ops shared by the Tape and the autograd Functions.
+
+Each op is one (or two) libkgq launches on the current CUDA stream:
+
+* ``graph_conv_forward``: fused KGNN layer forward -- H = A_hat.E (bit-exact
+  SpMM), quantize H on chip, J = H.theta, E' = relu(J), 1-bit mask -- the
+  three nodes ``record_spmm -> record_mm -> record_relu`` of model.py:81-85 in
+  one kernel.  H and J never reach HBM.
+* ``dequant_gemm_tn``: fused decompressor -> dtheta = Hhat^T g (tape.py:220-222).
+* ``bpr_forward`` / ``bpr_backward``: the BPR + L2 head (tape.py:154-183,
+  :233-244) on torch ops in the reference's op order.
+"""
+
+import torch
+
+from . import _lib
+from .quantize import (PASSTHROUGH_BITS, QuantConfig, QuantizedTensor, RandomStream,
+                       dequantize_tensor, packed_group_bytes, quantize_tensor)
+from .tensorops import CSR, BitMask, mm, relu, spmm
+
+FUSED_DIMS = (32, 64, 128)
+
+
+def can_fuse(cfg: QuantConfig, d: int) -> bool:
+    return (not cfg.passthrough) and d in FUSED_DIMS and (cfg.group is None or cfg.group == d)
+
+
+def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
+                       stream: RandomStream | None, tensor_id: int | None = None,
+                       row_offset: int = 0, want_h: bool = False):
+    """One fused layer.  Returns (e_next, mask, q, h) where q is the quantized
+    H context (per-row groups) and h is H only if ``want_h``.
+
+    ``adj`` may be a row block of the global adjacency (rows ``row_offset``..)
+    with global column ids; ``e`` then holds all the rows it references.
+    """
+    n_rows, d = adj.shape[0], e.shape[1]
+    if not can_fuse(cfg, d):
+        raise ValueError("graph_conv_forward needs bits < 32, d in (32, 64, 128), group == d")
+    if cfg.rounding == "stochastic":
+        if stream is None:
+            raise ValueError("stochastic rounding needs a RandomStream")
+        if tensor_id is None:
+            tensor_id = stream.next_tensor_id()
+        seed = stream.seed
+    else:
+        seed, tensor_id = 0, 0
+    dev = e.device
+    e = e.contiguous()
+    theta = theta.contiguous()
+    codes = torch.empty((n_rows, packed_group_bytes(d, cfg.bits)), dtype=torch.uint8, device=dev)
+    ranges = torch.empty(n_rows, dtype=torch.float32, device=dev)
+    offsets = torch.empty(n_rows, dtype=torch.float32, device=dev)
+    e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
+    mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
+    h = torch.empty((n_rows, d), dtype=torch.float32, device=dev) if want_h else None
+    st = _lib.load().kgq_layer_forward_f32(
+        adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows, e.data_ptr(), d,
+        theta.data_ptr(), cfg.bits, cfg.mode, seed, int(tensor_id) & 0xFFFFFFFFFFFFFFFF, row_offset,
+        codes.data_ptr(), ranges.data_ptr(), offsets.data_ptr(), e_next.data_ptr(), mask.data_ptr(),
+        _lib.ptr(h), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_layer_forward_f32")
+    q = QuantizedTensor(n_rows, d, cfg.bits, codes, ranges, offsets)
+    return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, h
+
+
+def layer_forward_unfused(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
+                          stream: RandomStream | None, tensor_id: int | None = None,
+                          row_offset: int = 0):
+    """spmm -> quantize -> mm -> relu as separate launches (any d / bits)."""
+    h = spmm(adj, e)
+    q = quantize_tensor(h, cfg, stream, tensor_id, group_offset=row_offset * (
+        1 if cfg.group is None else h.shape[1] // cfg.group))
+    j = mm(h, theta)
+    e_next, mask = relu(j)
+    return e_next, mask, q, h
+
+
+def dequant_gemm_tn(q: QuantizedTensor, g: torch.Tensor, out: torch.Tensor | None = None,
+                    accumulate: bool = False) -> torch.Tensor:
+    """dtheta (+)= dequantize(q)^T @ g without materializing the dequantized H."""
+    if q.bits == PASSTHROUGH_BITS:
+        r = q.raw.t() @ g
+        if out is None:
+            return r
+        if accumulate:
+            out.add_(r)
+        else:
+            out.copy_(r)
+        return out
+    d = q.cols
+    if q.group_size != d:
+        # per-group contexts: dequantize then GEMM (rare path)
+        r = dequantize_tensor(q).t() @ g
+        if out is None:
+            return r
+        return out.add_(r) if accumulate else out.copy_(r)
+    g = g.contiguous()
+    dev = g.device
+    if out is None:
+        out = torch.empty((d, d), dtype=torch.float32, device=dev)
+        accumulate = False
+    L = _lib.load()
+    ws_bytes = int(L.kgq_dequant_gemm_workspace_bytes(q.rows, d))
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+    st = L.kgq_dequant_gemm_tn_f32(q.codes.data_ptr(), q.ranges.data_ptr(), q.offsets.data_ptr(),
+                                   q.rows, d, q.bits, g.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                   ws_bytes, 1 if accumulate else 0, _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_dequant_gemm_tn_f32")
+    return out
+
+
+def bpr_forward(u: torch.Tensor, p: torch.Tensor, n: torch.Tensor, l2: float):
+    """tape.py:166-170: margins = sum(u*(p-n)); loss = mean softplus(-m) +
+    l2*(|u|^2+|p|^2+|n|^2)/B.  Returns (loss 0-d tensor, margins)."""
+    batch = u.shape[0]
+    margins = (u * (p - n)).sum(dim=1)
+    data = torch.nn.functional.softplus(-margins).mean()
+    reg = l2 * ((u * u).sum() + (p * p).sum() + (n * n).sum()) / batch
+    return data + reg, margins
+
+
+def bpr_backward(g, margins, uh, ph, nh, l2: float, batch: int):
+    """tape.py:233-244 (against the dequantized blocks, exact margins)."""
+    coef = (torch.sigmoid(-margins) / batch)[:, None]
+    reg = 2.0 * l2 / batch
+    gu = g * (-coef * (ph - nh) + reg * uh)
+    gp = g * (-coef * uh + reg * ph)
+    gn = g * (coef * uh + reg * nh)
+    return gu, gp, gn
+
+
+def scatter_rows(src_rows: int, idx: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    """np.add.at(zeros, idx, g) (tape.py:229-231)."""
+    out = torch.zeros((src_rows, g.shape[1]), dtype=g.dtype, device=g.device)
+    out.index_add_(0, idx.to(torch.int64), g)
+    return out

@@ -204,7 +204,7 @@ def test_full_size_properties(bits):
     B = (1 << bits) - 1
     # sample 4096 groups spread over the tensor and compare with the oracle
     n_groups = rows * cols // 64
-    idx = torch.linspace(0, n_groups - 1, 4096, device="cuda").long()
+    idx = torch.from_numpy(np.linspace(0, n_groups - 1, 4096).astype(np.int64)).cuda()
     xs = x.view(-1, 64)[idx].cpu().numpy()
     for k, gi in enumerate(idx.cpu().numpy()[:64]):
         c, r, o = orc.quantize(xs[k:k + 1], 64, bits, orc.MODE_SR_FAST, 11, 3, group_offset=int(gi))
