@@ -330,15 +330,19 @@ def run_ours(args):
             "config": dict(workload_config(args), rows_per_gpu=rows,
                            parallelism=f"row shards x{world}, no data-path collective"),
             "frac_of_peak": round(value / world / peak, 4),
-            "roofline": {"bound": "hbm", "kernel": "quantize_t4_kernel (K1, fused quantize+pack)",
+            "roofline": {"bound": "hbm", "kernel": "quantize_fast_kernel (K1, fused quantize+pack)",
                          "achieved": round(q_gbs, 1), "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": round(q_gbs / peak, 4),
-                         "traffic": traffic.get("quantize"),
+                         "traffic": (round(traffic["quantize"]["dram_bytes_per_elem"] * n)
+                                     if "quantize" in traffic else None),
+                         "traffic_note": "dram__bytes_read+write per element from the committed ncu "
+                                         "capture (profiles/traffic.json), scaled to this launch",
                          "algorithmic_bytes_per_launch": int(n * bpe)},
             "kernels": {
                 "quantize": {"ms": round(q_avg, 4), "GBps": round(q_gbs, 1), "frac": round(q_gbs / peak, 4)},
                 "dequantize": {"ms": round(d_avg, 4), "GBps": round(d_gbs, 1), "frac": round(d_gbs / peak, 4),
-                               "traffic": traffic.get("dequantize")},
+                               "traffic": (round(traffic["dequantize"]["dram_bytes_per_elem"] * n)
+                                           if "dequantize" in traffic else None)},
                 "quantize_compat_rng": comp,
             },
             "clocks": clk.summary(),

@@ -21,40 +21,61 @@ namespace kgq {
 
 constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;
-constexpr int kGroupsPerWarp = 8;      // 4 threads per group
+constexpr int kGroupsPerWarp = 8;      // dequantize: 4 threads per group
 
-// Codes of the NB float4 a thread owns, packed 4*BITS bits per float4.
+// Thread geometry of the fast quantizer: a G-element group is handled by T
+// threads (T = 2 or 4); thread j owns float4 q in [j*Q, j*Q+Q) (Q = 4/T) of
+// every 16-element block, so one warp-wide 128-bit load covers 32/T groups
+// with fully used sectors and the noise calls (which pair float4 q of blocks
+// 2p and 2p+1) are never split across threads.
+template <int G, int T>
+struct Geo {
+    static constexpr int NBLK = G / 16;     // 16-element blocks per group
+    static constexpr int Q = 4 / T;         // float4 per block per thread
+    static constexpr int NF = NBLK * Q;     // float4 per thread
+    static constexpr int GPW = 32 / T;      // groups per warp tile
+    // cp.async ring depth: <= 64 KB of prefetch slots per CTA
+    static constexpr int S = (NF * 512 * kWarps * 2 <= 64 * 1024) ? (64 * 1024) / (NF * 512 * kWarps) : 1;
+};
+
+// Codes of the NF float4 a thread owns, 4*BITS bits per float4 (LSB-first).
 // GUARD=false: the group passed group_div_unguarded (no per-element check).
-template <int NB, int G, int BITS, int MODE, bool GUARD>
-__device__ __forceinline__ void quant_pieces(const float4 (&v)[NB], float z, const DivR &dv,
+template <int G, int T, int BITS, int MODE, bool GUARD>
+__device__ __forceinline__ void quant_pieces(const float4 (&v)[Geo<G, T>::NF], float z, const DivR &dv,
                                              const FastKey &fk, uint64_t gglob, int j,
-                                             uint64_t seed, uint64_t tid, uint32_t (&piece)[NB]) {
+                                             uint64_t seed, uint64_t tid,
+                                             uint32_t (&piece)[Geo<G, T>::NF]) {
+    using GE = Geo<G, T>;
     constexpr float Bf = (float)PackInfo<BITS>::B;
 #pragma unroll
-    for (int i = 0; i < NB; i += 2) {
-        uint4 rnd = make_uint4(0, 0, 0, 0);
-        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * (i >> 1) + j));
+    for (int p = 0; p < GE::NBLK / 2; p++) {
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int ib = i + h;
-            if (ib >= NB) break;
-            u64x4 r64 = {0, 0, 0, 0};
-            if (MODE == KGQ_ROUND_SR_COMPAT)
-                r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * ib + j) + 1ull,
-                                    0, 0, 0, seed, tid);
-            const float xs[4] = {v[ib].x, v[ib].y, v[ib].z, v[ib].w};
-            const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
-            const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
-            uint32_t acc = 0;
+        for (int qq = 0; qq < GE::Q; qq++) {
+            const int q = j * GE::Q + qq;
+            uint4 rnd = make_uint4(0, 0, 0, 0);
+            if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * p + q));
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const float a = __fsub_rn(xs[e], z);
-                const float q = GUARD ? div_a(dv, a) : div_a_unguarded(dv, a);
-                const float s = __fmul_rn(q, Bf);
-                const float uf = h ? __uint2float_rn(rw[e] >> 16) : __uint2float_rn(rw[e] & 0xFFFFu);
-                acc += code_bits<MODE>(s, uf, cw[e] >> 11) << (BITS * e);
+            for (int h = 0; h < 2; h++) {
+                const int i = 2 * p + h;
+                const int f = i * GE::Q + qq;
+                u64x4 r64 = {0, 0, 0, 0};
+                if (MODE == KGQ_ROUND_SR_COMPAT)
+                    r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * i + q) + 1ull,
+                                        0, 0, 0, seed, tid);
+                const float xs[4] = {v[f].x, v[f].y, v[f].z, v[f].w};
+                const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+                const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
+                uint32_t acc = 0;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const float a = __fsub_rn(xs[e], z);
+                    const float qv = GUARD ? div_a(dv, a) : div_a_unguarded(dv, a);
+                    const float s = __fmul_rn(qv, Bf);
+                    const float uf = h ? __uint2float_rn(rw[e] >> 16) : __uint2float_rn(rw[e] & 0xFFFFu);
+                    acc += code_bits<MODE>(s, uf, cw[e] >> 11) << (BITS * e);
+                }
+                piece[f] = acc - magic_sum4<BITS>();
             }
-            piece[ib] = acc - magic_sum4<BITS>();
         }
     }
 }
@@ -62,111 +83,124 @@ __device__ __forceinline__ void quant_pieces(const float4 (&v)[NB], float z, con
 // ---------------------------------------------------------------------------
 // K1: fast fused quantize + pack.
 // ---------------------------------------------------------------------------
-template <int G, int BITS, int MODE>
+template <int G, int T, int BITS, int MODE>
 __global__ void __launch_bounds__(kThreads)
-quantize_t4_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__restrict__ codes,
-                   float *__restrict__ ranges, float *__restrict__ offsets, uint64_t seed,
-                   uint64_t tid, int64_t group_offset) {
-    constexpr int NB = G / 16;                    // float4 per thread
+quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__restrict__ codes,
+                     float *__restrict__ ranges, float *__restrict__ offsets, uint64_t seed,
+                     uint64_t tid, int64_t group_offset) {
+    using GE = Geo<G, T>;
+    constexpr int NF = GE::NF, Q = GE::Q, GPW = GE::GPW, S = GE::S;
     constexpr int GB = G * BITS / 8;              // packed bytes per group
-    // cp.async prefetch depth: each lane streams its own float4s for the next
-    // S-1 tiles into private shared-memory slots (no cross-lane sharing, so
-    // no barriers), keeping 2-5 tiles of loads in flight per warp without
-    // holding them in registers.  48 KB static smem per CTA at most.
-    constexpr int S = (NB <= 4) ? 12 / NB : 1;
-    __shared__ __align__(16) uint8_t stage[kWarps][kGroupsPerWarp * GB];
-    extern __shared__ __align__(16) float4 pf_raw[];   // [kWarps][S][NB][32], dynamic
-    auto pf = reinterpret_cast<float4 (*)[S > 1 ? S : 1][NB][32]>(pf_raw);
+    constexpr int PW = 4 * BITS * Q;              // packed bits per thread per block
+    __shared__ __align__(16) uint8_t stage[kWarps][GPW * GB];
+    // cp.async ring: each lane streams its own float4s for the next S-1 tiles
+    // into private shared-memory slots (no cross-lane sharing -> no barriers).
+    extern __shared__ __align__(16) float4 pf_raw[];   // [kWarps][S][NF][32]
+    auto pf = reinterpret_cast<float4 (*)[S][NF][32]>(pf_raw);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = lane & 3, gw = lane >> 2;
+    const int j = lane % T, gw = lane / T;
     uint8_t *st = stage[warp];
     const FastKey fk = make_fast_key(seed, tid);
 
-    const int64_t n_tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    const int64_t n_tiles = (n_groups + GPW - 1) / GPW;
     const int64_t stride = (int64_t)gridDim.x * kWarps;
     const int64_t tile0 = (int64_t)blockIdx.x * kWarps + warp;
-    auto src_of = [&](int64_t t) {
-        const int64_t g = t * kGroupsPerWarp + gw;
-        return reinterpret_cast<const float4 *>(x) + (g < n_groups ? g : 0) * (G / 4);
-    };
-    auto issue = [&](int64_t t, int s) {   // one commit group per tile (possibly empty)
-        if (S > 1 && t < n_tiles) {
-            const float4 *src = src_of(t);
+    const float4 *xb = reinterpret_cast<const float4 *>(x) + j * Q;
+    const int64_t gstep = stride * GPW;
+    int64_t gnext = tile0 * GPW + gw;     // group of the next tile to prefetch
+    auto issue = [&](int s) {             // one commit group per tile (possibly empty)
+        if (gnext < n_groups) {
+            const float4 *src = xb + gnext * (G / 4);
 #pragma unroll
-            for (int i = 0; i < NB; i++) cp_async16(&pf[S > 1 ? warp : 0][s][i][lane], src + 4 * i + j);
+            for (int i = 0; i < GE::NBLK; i++)
+#pragma unroll
+                for (int qq = 0; qq < Q; qq++) cp_async16(&pf[warp][s][i * Q + qq][lane], src + 4 * i + qq);
         }
         cp_async_commit();
+        gnext += gstep;
     };
     if (S > 1) {
 #pragma unroll
-        for (int k = 0; k < S - 1; k++) issue(tile0 + k * stride, k);
+        for (int k = 0; k < S - 1; k++) issue(k);
     }
     int cur = 0;
     for (int64_t tile = tile0; tile < n_tiles; tile += stride) {
-        const int64_t g = tile * kGroupsPerWarp + gw;
-        const bool valid = g < n_groups;
-        float4 v[NB];
+        const int64_t g = tile * GPW + gw;
+        const bool valid = g < n_groups;   // invalid lanes compute on stale data, store nothing
+        float4 v[NF];
         if (S > 1) {
-            cp_async_wait<S - 2>();
+            cp_async_wait<(S > 1 ? S - 2 : 0)>();
 #pragma unroll
-            for (int i = 0; i < NB; i++) v[i] = pf[warp][cur][i][lane];
-            issue(tile + (S - 1) * stride, cur == 0 ? S - 1 : cur - 1);
+            for (int f = 0; f < NF; f++) v[f] = pf[warp][cur][f][lane];
+            issue(cur == 0 ? S - 1 : cur - 1);
             cur = (cur + 1 == S) ? 0 : cur + 1;
         } else {
-            const float4 *src = src_of(tile);
+            const float4 *src = xb + (valid ? g : 0) * (G / 4);
 #pragma unroll
-            for (int i = 0; i < NB; i++) v[i] = ldg_stream(src + 4 * i + j);
+            for (int i = 0; i < GE::NBLK; i++)
+#pragma unroll
+                for (int qq = 0; qq < Q; qq++) v[i * Q + qq] = ldg_stream(src + 4 * i + qq);
         }
 
         float mn = fminf(fminf(v[0].x, v[0].y), fminf(v[0].z, v[0].w));
         float mx = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
 #pragma unroll
-        for (int i = 1; i < NB; i++) {
-            mn = fminf(mn, fminf(fminf(v[i].x, v[i].y), fminf(v[i].z, v[i].w)));
-            mx = fmaxf(mx, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+        for (int f = 1; f < NF; f++) {
+            mn = fminf(mn, fminf(fminf(v[f].x, v[f].y), fminf(v[f].z, v[f].w)));
+            mx = fmaxf(mx, fmaxf(fmaxf(v[f].x, v[f].y), fmaxf(v[f].z, v[f].w)));
         }
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+#pragma unroll
+        for (int o = 1; o < T; o <<= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
         const float z = mn;
         const float r = __fsub_rn(mx, mn);
         const DivR dv = make_div(r);
         const uint64_t gglob = (uint64_t)(group_offset + g);
 
-        uint32_t piece[NB];   // 4*BITS bits per block (elements 16i+4j .. +3)
+        uint32_t piece[NF];
         if (r > 0.0f) {
             if (group_div_unguarded(dv, z))
-                quant_pieces<NB, G, BITS, MODE, false>(v, z, dv, fk, gglob, j, seed, tid, piece);
+                quant_pieces<G, T, BITS, MODE, false>(v, z, dv, fk, gglob, j, seed, tid, piece);
             else
-                quant_pieces<NB, G, BITS, MODE, true>(v, z, dv, fk, gglob, j, seed, tid, piece);
+                quant_pieces<G, T, BITS, MODE, true>(v, z, dv, fk, gglob, j, seed, tid, piece);
         } else {
 #pragma unroll
-            for (int i = 0; i < NB; i++) piece[i] = 0;   // R == 0 -> scaled 0 -> code 0
+            for (int f = 0; f < NF; f++) piece[f] = 0;   // R == 0 -> scaled 0 -> code 0
         }
 
-        // stage the packed codes (LSB-first, group-contiguous)
+        // stage the packed codes: the thread's Q float4 of block i are PW
+        // contiguous bits at byte (16i + 4jQ) * BITS / 8 of the group
         uint8_t *gst = st + gw * GB;
 #pragma unroll
-        for (int i = 0; i < NB; i++) {
-            if (BITS == 8) {
-                *reinterpret_cast<uint32_t *>(gst + 16 * i + 4 * j) = piece[i];
-            } else if (BITS == 4) {
-                *reinterpret_cast<uint16_t *>(gst + 8 * i + 2 * j) = (uint16_t)piece[i];
-            } else if (BITS == 2) {
-                gst[4 * i + j] = (uint8_t)piece[i];
-            } else {  // BITS == 1: nibble; pair lanes j, j^1 into one byte
-                const uint32_t other = __shfl_xor_sync(0xffffffffu, piece[i], 1);
-                if ((j & 1) == 0) gst[2 * i + (j >> 1)] = (uint8_t)(piece[i] | (other << 4));
+        for (int i = 0; i < GE::NBLK; i++) {
+            const int off = (16 * i + 4 * j * Q) * BITS / 8;
+            if (PW == 64) {
+                *reinterpret_cast<uint2 *>(gst + off) = make_uint2(piece[i * Q], piece[i * Q + 1]);
+            } else {
+                uint32_t w = piece[i * Q];
+                if constexpr (Q == 2) w |= piece[i * Q + 1] << (4 * BITS);
+                if (PW == 32) *reinterpret_cast<uint32_t *>(gst + off) = w;
+                else if (PW == 16) *reinterpret_cast<uint16_t *>(gst + off) = (uint16_t)w;
+                else if (PW == 8) gst[off] = (uint8_t)w;
+                else {  // PW == 4 (T=4, BITS=1): pair lanes j, j^1 into one byte
+                    const uint32_t other = __shfl_xor_sync(0xffffffffu, w, 1);
+                    if ((j & 1) == 0) gst[off] = (uint8_t)(w | (other << 4));
+                }
             }
         }
         __syncwarp();
-        const int64_t g0 = tile * kGroupsPerWarp;
-        const int nvalid = (int)imin64(kGroupsPerWarp, n_groups - g0);
+        const int64_t g0 = tile * GPW;
+        const int nvalid = (int)imin64(GPW, n_groups - g0);
         uint8_t *dst = codes + g0 * GB;
         const int nbytes = nvalid * GB;
-        if ((nbytes & 15) == 0) {
+        if (nvalid == GPW) {   // full tile: GPW*GB bytes, a multiple of 16
+#pragma unroll
+            for (int b = lane * 16; b < GPW * GB; b += 32 * 16)
+                *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
+        } else if ((nbytes & 15) == 0) {
             for (int b = lane * 16; b < nbytes; b += 32 * 16)
                 *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
         } else {
@@ -471,27 +505,31 @@ static inline int grid_for(int64_t work_items, int per_block, int max_blocks_per
     return (int)b;
 }
 
+// T = threads per group: 2 for G <= 64 (less per-group overhead), 4 above
+// (keeps registers and the prefetch ring small).
+template <int G> struct PickT { static constexpr int T = 4; };
+
 template <int G, int BITS, int MODE>
 static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, float *ranges,
                             float *offsets, uint64_t seed, uint64_t tid, int64_t goff,
                             cudaStream_t s) {
-    const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    constexpr int T = PickT<G>::T;
+    using GE = Geo<G, T>;
+    const int64_t tiles = (n_groups + GE::GPW - 1) / GE::GPW;
     const int grid = grid_for(tiles, kWarps, 8);
-    constexpr int NB = G / 16;
-    constexpr int S = (NB <= 4) ? 12 / NB : 1;
-    const size_t smem = S > 1 ? (size_t)kWarps * S * NB * 32 * sizeof(float4) : 0;
+    const size_t smem = GE::S > 1 ? (size_t)kWarps * GE::S * GE::NF * 32 * sizeof(float4) : 0;
     if (smem > 0) {   // dynamic + static smem may exceed the 48 KB default
         static unsigned attr_set = 0;   // per template instance, bit per device
         int dev = 0;
         cudaGetDevice(&dev);
         if (!(attr_set & (1u << (dev & 31)))) {
-            cudaFuncSetAttribute(quantize_t4_kernel<G, BITS, MODE>,
+            cudaFuncSetAttribute(quantize_fast_kernel<G, T, BITS, MODE>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr_set |= 1u << (dev & 31);
         }
     }
-    quantize_t4_kernel<G, BITS, MODE><<<grid, kThreads, smem, s>>>(x, n_groups, codes, ranges,
-                                                                  offsets, seed, tid, goff);
+    quantize_fast_kernel<G, T, BITS, MODE><<<grid, kThreads, smem, s>>>(x, n_groups, codes, ranges,
+                                                                       offsets, seed, tid, goff);
 }
 
 template <int G, int BITS>
