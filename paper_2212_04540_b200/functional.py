@@ -115,7 +115,7 @@ def bpr_forward(u: torch.Tensor, p: torch.Tensor, n: torch.Tensor, l2: float):
     l2*(|u|^2+|p|^2+|n|^2)/B.  Returns (loss 0-d tensor, margins)."""
     batch = u.shape[0]
     margins = (u * (p - n)).sum(dim=1)
-    data = torch.nn.functional.softplus(-margins).mean()
+    data = torch.logaddexp(torch.zeros_like(margins), -margins).mean()
     reg = l2 * ((u * u).sum() + (p * p).sum() + (n * n).sum()) / batch
     return data + reg, margins
 

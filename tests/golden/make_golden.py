@@ -228,7 +228,50 @@ def make_tape():
     return out
 
 
+C1_SPEC = "default,users=2000,items=3000,entities=10000,relations=20"
+
+
+def make_c1():
+    """BASELINE configs[0]: the reference's own dataset,
+    adjacency, first-epoch batches and short training runs (b=32 and b=2 fed
+    the fast-mode noise) -- the Recall@20 parity target."""
+    from kgact import train as ktrain
+    from kgact.data import sample_negatives
+    ds = synth_generate(parse_synth_spec(C1_SPEC), seed=0)
+    adj = build_adjacency(ds)
+    out = {"num_users": np.array(ds.num_users), "num_items": np.array(ds.num_items),
+           "num_entities": np.array(ds.num_entities), "num_relations": np.array(len(ds.relation_vocab)),
+           "train": ds.train, "val": ds.val, "test": ds.test, "triples": ds.triples,
+           "adj_indptr": adj.indptr.astype(np.int32), "adj_indices": adj.indices.astype(np.int32),
+           "adj_data": adj.data.astype(np.float32)}
+    rng = np.random.default_rng(0)
+    trip = sample_negatives(ds, rng)
+    order = rng.permutation(len(trip))
+    out["epoch0_triples"] = trip[order]
+    epochs = 3
+    for bits in (32, 2):
+        mcfg = ModelConfig(layers=2, dim=64, quant=kq.QuantConfig(bits=bits))
+        tcfg = ktrain.TrainConfig(epochs=epochs, batch_size=1024, seed=0,
+                                  quant=kq.QuantConfig(bits=bits))
+        saved = ktrain.RandomStream
+        ktrain.RandomStream = FastNoiseStream
+        try:
+            _, rep = ktrain.train_run(ds, mcfg, tcfg, adjacency=adj)
+        finally:
+            ktrain.RandomStream = saved
+        pre = f"run_b{bits}_"
+        out[pre + "loss_curve"] = np.array(rep["loss_curve"])
+        out[pre + "recall"] = np.array(rep["metrics"]["recall_at_20"])
+        out[pre + "ndcg"] = np.array(rep["metrics"]["ndcg_at_20"])
+        out[pre + "peak_ctx"] = np.array(rep["memory"]["activation_bytes_peak"])
+        out[pre + "peak_eq"] = np.array(rep["memory"]["fp32_equivalent_bytes"])
+        out[pre + "epoch_seconds"] = np.array(rep["timing"]["epoch_seconds"])
+    out["run_epochs"] = np.array(epochs)
+    return out
+
+
 def main():
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **make_c1())
     np.savez_compressed(os.path.join(HERE, "philox.npz"), **make_philox())
     np.savez_compressed(os.path.join(HERE, "quant.npz"), **make_quant())
     np.savez_compressed(os.path.join(HERE, "spmm.npz"), **make_spmm())

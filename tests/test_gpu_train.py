@@ -1,0 +1,201 @@
+"""GPU parity of the compressed-context engine (Tape, fused layer, autograd
+Functions, training loop) against the reference's own outputs (golden
+fixtures from tests/golden/make_golden.py) and the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+
+def _kgq():
+    import paper_2212_04540_b200 as kgq
+    return kgq
+
+
+def _tiny():
+    kgq = _kgq()
+    z = golden_io.load("tape")
+    n = int(z["n"])
+    adj = kgq.CSR.from_arrays(z["indptr"], z["indices"], z["data"], (n, n), symmetric=True)
+    return kgq, z, adj
+
+
+def _record(kgq, tape, params, adj, z, layers, d, fused):
+    from paper_2212_04540_b200.model import ModelConfig, forward_all
+    cfg = ModelConfig(layers=layers, dim=d, quant=tape.cfg)
+    readout = forward_all(tape, params, adj, cfg, fused=fused)
+    dev = "cuda"
+    u = tape.record_gather(readout, torch.from_numpy(z["users"]).to(dev))
+    p = tape.record_gather(readout, torch.from_numpy(z["pos"]).to(dev))
+    n = tape.record_gather(readout, torch.from_numpy(z["neg"]).to(dev))
+    tape.record_bpr_loss(u, p, n, 1e-5)
+    return readout
+
+
+def _params(kgq, z, d, layers):
+    from paper_2212_04540_b200.model import ModelParams
+    return ModelParams(torch.from_numpy(z[f"d{d}_E0"]).cuda(),
+                       [torch.from_numpy(z[f"d{d}_theta{i}"]).cuda() for i in range(layers)])
+
+
+@pytest.mark.parametrize("d,layers", [(64, 3), (32, 2)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_tape_b32_matches_reference(d, layers, fused):
+    kgq, z, adj = _tiny()
+    from paper_2212_04540_b200.tape import Tape
+    tape = Tape(kgq.QuantConfig(bits=32), kgq.RandomStream(21))
+    _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, fused)
+    pre = f"d{d}_b32_"
+    assert tape.peak_context_bytes == int(z[pre + "peak_ctx"])
+    assert tape.peak_fp32_equiv_bytes == int(z[pre + "peak_eq"])
+    grads = tape.backward()
+    assert tape.current_context_bytes == 0
+    assert tape.loss() == pytest.approx(float(z[pre + "loss"]), rel=1e-6)
+    for name, g in grads.items():
+        np.testing.assert_allclose(g.cpu().numpy(), z[pre + "grad_" + name], rtol=2e-4, atol=2e-7)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("fused", [True, False])
+def test_tape_quantized_matches_reference(bits, fused):
+    """Same noise (fast stream == reference fed the exported noise): layer-0
+    context codes are bit-exact; deeper contexts see H through an fp32 GEMM
+    whose summation order differs from OpenBLAS, so a few codes may flip;
+    gradients agree within a tolerance set by one code step."""
+    kgq, z, adj = _tiny()
+    from paper_2212_04540_b200.tape import Tape
+    d, layers = 64, 3
+    tape = Tape(kgq.QuantConfig(bits=bits), kgq.RandomStream(21))
+    _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, fused)
+    pre = f"d{d}_b{bits}_"
+    assert tape.peak_context_bytes == int(z[pre + "peak_ctx"])
+    assert tape.peak_fp32_equiv_bytes == int(z[pre + "peak_eq"])
+    qs = [n.context["q"] for n in tape.nodes if n.kind == "mm"]
+    bpr = [n for n in tape.nodes if n.kind == "bpr_loss"][0].context
+    qs += [bpr["qu"], bpr["qp"], bpr["qn"]]
+    assert np.array_equal(qs[0].codes.cpu().numpy(), z[pre + "q0_codes"])
+    assert np.array_equal(qs[0].ranges.cpu().numpy(), z[pre + "q0_ranges"])
+    for k, q in enumerate(qs):
+        ours = q.codes.cpu().numpy()
+        ref = z[pre + f"q{k}_codes"]
+        assert ours.shape == ref.shape
+        assert np.mean(ours != ref) < 0.02, k
+        np.testing.assert_allclose(q.ranges.cpu().numpy(), z[pre + f"q{k}_ranges"], rtol=1e-4, atol=1e-6)
+    grads = tape.backward()
+    assert tape.current_context_bytes == 0
+    assert tape.loss() == pytest.approx(float(z[pre + "loss"]), rel=1e-5)
+    for name, g in grads.items():
+        ref = z[pre + "grad_" + name]
+        scale = np.abs(ref).max()
+        err = np.abs(g.cpu().numpy() - ref).max()
+        assert err <= 0.05 * scale + 1e-7, (name, err, scale)
+
+
+def test_fused_layer_matches_unfused_and_oracle():
+    """The fused kernel's H is the bit-exact SpMM and its codes equal a
+    standalone quantize of that H; J within fp32 GEMM tolerance."""
+    kgq = _kgq()
+    import scipy.sparse as sp
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(0)
+    for d in (32, 64, 128):
+        n = 3000
+        a = sp.random(n, n, density=0.004, random_state=d, format="csr", dtype=np.float32)
+        a = (a + a.T + sp.eye(n, dtype=np.float32)).tocsr()
+        a.sum_duplicates()
+        a.sort_indices()
+        A = kgq.CSR.from_scipy(a)
+        e = rng.standard_normal((n, d), dtype=np.float32)
+        e[::7] = np.maximum(e[::7], 0)
+        th = (rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)
+        for bits in (1, 2, 4, 8):
+            for rng_mode, rounding in (("fast", "stochastic"), ("compat", "stochastic"), ("fast", "nearest")):
+                cfg = kgq.QuantConfig(bits=bits, rounding=rounding, rng=rng_mode)
+                et, tt = torch.from_numpy(e).cuda(), torch.from_numpy(th).cuda()
+                e1, m1, q1, h1 = F.graph_conv_forward(A, et, tt, cfg, kgq.RandomStream(4), 9,
+                                                      row_offset=0, want_h=True)
+                h_ref = orc.spmm_csr(a.indptr, a.indices, a.data, e)
+                assert np.array_equal(h1.cpu().numpy().view(np.uint32), h_ref.view(np.uint32))
+                q2 = kgq.quantize_tensor(h1, cfg, kgq.RandomStream(4), tensor_id=9)
+                assert torch.equal(q1.codes, q2.codes) and torch.equal(q1.ranges, q2.ranges)
+                j = h_ref.astype(np.float64) @ th.astype(np.float64)
+                np.testing.assert_allclose(e1.cpu().numpy(), np.maximum(j, 0), rtol=1e-4, atol=1e-5)
+                r_out, r_mask = orc.relu_mask(e1.cpu().numpy())
+                # mask bit == (J > 0) and e_next == relu(J): consistent with the relu kernel
+                assert np.array_equal(m1.packed.cpu().numpy(), r_mask)
+
+
+def test_dequant_gemm_matches_dequantize_then_matmul():
+    kgq = _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(1)
+    for d in (32, 64, 128, 48):
+        for rows in (1, 31, 1000, 40000):
+            x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+            g = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+            for bits in (1, 2, 4, 8):
+                q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(2), tensor_id=1)
+                hh = kgq.dequantize_tensor(q).double()
+                ref = (hh.t() @ g.double()).cpu().numpy()
+                out = F.dequant_gemm_tn(q, g).double().cpu().numpy()
+                np.testing.assert_allclose(out, ref, rtol=1e-4, atol=1e-4 * np.sqrt(rows))
+                # deterministic
+                out2 = F.dequant_gemm_tn(q, g).double().cpu().numpy()
+                assert np.array_equal(out, out2)
+
+
+def test_autograd_kgnn_equals_tape():
+    """The torch plugin surface (autograd Functions) == the Tape, same noise."""
+    kgq, z, adj = _tiny()
+    from paper_2212_04540_b200.autograd import BPRLossFn, ContextLedger, GatherFn, KGNN
+    from paper_2212_04540_b200.tape import Tape
+    d, layers = 64, 3
+    for bits in (32, 2):
+        cfg = kgq.QuantConfig(bits=bits)
+        tape = Tape(cfg, kgq.RandomStream(21))
+        _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, True)
+        tg = tape.backward()
+        p = _params(kgq, z, d, layers)
+        st = kgq.RandomStream(21)
+        model = KGNN(p.entity_embeddings.clone(), [t.clone() for t in p.layer_weights], cfg, st)
+        ledger = ContextLedger()
+        ro = model(adj, ledger)
+        ix = lambda k: torch.from_numpy(z[k]).cuda()
+        u, pp, n = GatherFn.apply(ro, ix("users"), ledger), GatherFn.apply(ro, ix("pos"), ledger), GatherFn.apply(ro, ix("neg"), ledger)
+        loss = BPRLossFn.apply(u, pp, n, 1e-5, cfg, st, ledger)
+        assert ledger.peak == tape.peak_context_bytes
+        assert ledger.peak_eq == tape.peak_fp32_equiv_bytes
+        loss.backward()
+        assert ledger.current == 0
+        assert float(loss) == pytest.approx(tape.loss(), rel=1e-6)
+        np.testing.assert_allclose(model.e0.grad.cpu().numpy(), tg["E0"].cpu().numpy(), rtol=1e-5, atol=1e-8)
+        for i, layer in enumerate(model.layers):
+            np.testing.assert_allclose(layer.weight.grad.cpu().numpy(), tg[f"theta{i}"].cpu().numpy(),
+                                       rtol=1e-5, atol=1e-8)
+
+
+@pytest.mark.parametrize("bits", [32, 2])
+def test_training_c1_matches_reference_run(bits):
+    """BASELINE configs[0] (small KG, 2 layers, d=64): same dataset, batches,
+    noise and init as the reference's train_run; loss curve and Recall@20."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig
+    from paper_2212_04540_b200.train import TrainConfig, train_run
+    z = golden_io.load("c1")
+    ds = D.KgDataset(int(z["num_users"]), int(z["num_items"]), int(z["num_entities"]), z["train"],
+                     z["val"], z["test"], z["triples"], int(z["num_relations"]))
+    epochs = int(z["run_epochs"])
+    q = kgq.QuantConfig(bits=bits)
+    _, rep = train_run(ds, ModelConfig(layers=2, dim=64, quant=q), TrainConfig(epochs=epochs, seed=0, quant=q))
+    pre = f"run_b{bits}_"
+    np.testing.assert_allclose(rep["loss_curve"], z[pre + "loss_curve"], rtol=2e-3)
+    assert abs(rep["metrics"]["recall_at_20"] - float(z[pre + "recall"])) < 0.01
+    assert abs(rep["metrics"]["ndcg_at_20"] - float(z[pre + "ndcg"])) < 0.01
+    assert rep["memory"]["activation_bytes_peak"] == int(z[pre + "peak_ctx"])
+    assert rep["memory"]["fp32_equivalent_bytes"] == int(z[pre + "peak_eq"])
+    assert rep["memory"]["retained_context_bytes"] == 0
