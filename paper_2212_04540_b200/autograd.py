@@ -66,13 +66,18 @@ def _ledger_free(ledger, nbytes, eq):
 
 
 class SpMMFn(torch.autograd.Function):
+    """Context: the shared adjacency, counted once per ledger and released by
+    the node that first registered it (tape.py:101-110, :187-191)."""
+
     @staticmethod
     def forward(ctx, x, adj: CSR, ledger=None):
-        ctx.adj = adj
+        ctx.adj, ctx.ledger = adj, ledger
+        ctx.adj_bytes = ledger.adjacency(adj) if ledger is not None else 0
         return spmm(adj, x)
 
     @staticmethod
     def backward(ctx, g):
+        _ledger_free(ctx.ledger, ctx.adj_bytes, ctx.adj_bytes)
         return spmm_t(ctx.adj, g.contiguous()), None, None
 
 
@@ -126,10 +131,10 @@ class QuantGraphConvFn(torch.autograd.Function):
                 row_offset=0):
         e_next, mask, q, _ = F.graph_conv_forward(adj, e, theta, cfg, stream, row_offset=row_offset)
         ctx.adj, ctx.q, ctx.mask, ctx.ledger = adj, q, mask, ledger
+        adj_b = ledger.adjacency(adj) if ledger is not None else 0
         ctx.bytes = (stored_bytes(q) + mask.nbytes, fp32_equivalent_bytes(q) + mask.nbytes)
-        if ledger is not None:
-            ledger.adjacency(adj)
         _ledger_push(ledger, *ctx.bytes)
+        ctx.bytes = (ctx.bytes[0] + adj_b, ctx.bytes[1] + adj_b)
         ctx.save_for_backward(theta)
         return e_next
 
@@ -197,8 +202,6 @@ class QuantGraphConv(torch.nn.Module):
     def forward(self, e, adj: CSR, ledger=None, row_offset=0):
         if F.can_fuse(self.cfg, e.shape[1]):
             return QuantGraphConvFn.apply(e, self.weight, adj, self.cfg, self.stream, ledger, row_offset)
-        if ledger is not None:
-            ledger.adjacency(adj)
         h = SpMMFn.apply(e, adj, ledger)
         j = QuantLinearFn.apply(h, self.weight, self.cfg, self.stream, ledger, row_offset)
         return MaskedReLUFn.apply(j, ledger)
