@@ -42,6 +42,7 @@ class CSR:
         self.shape = (int(shape[0]), int(shape[1]))
         self._symmetric = symmetric
         self._transpose = None
+        self._row_order = None
 
     @classmethod
     def from_scipy(cls, m, device="cuda", symmetric: bool | None = None) -> "CSR":
@@ -60,6 +61,14 @@ class CSR:
         import scipy.sparse as sp
         return sp.csr_matrix((self.data.cpu().numpy(), self.indices.cpu().numpy(),
                               self.indptr.cpu().numpy()), shape=self.shape)
+
+    def row_order_ptr(self) -> int:
+        """Rows by decreasing degree (stable), built once: the schedule the
+        row-group kernels use so the rows of a warp have similar lengths."""
+        if self._row_order is None:
+            deg = torch.diff(self.indptr.to(torch.int64))
+            self._row_order = torch.sort(deg, descending=True, stable=True).indices.to(torch.int32)
+        return self._row_order.data_ptr()
 
     @property
     def nnz(self) -> int:
@@ -115,8 +124,8 @@ def mm(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 def spmm_into(s: CSR, d: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     st = _lib.load().kgq_spmm_csr_f32(s.indptr.data_ptr(), s.indices.data_ptr(), s.data.data_ptr(),
-                                      s.shape[0], d.data_ptr(), d.shape[1], out.data_ptr(),
-                                      _lib.stream_ptr(d.device))
+                                      s.shape[0], s.row_order_ptr(), d.data_ptr(), d.shape[1],
+                                      out.data_ptr(), _lib.stream_ptr(d.device))
     _lib.check(st, "kgq_spmm_csr_f32")
     return out
 
