@@ -96,11 +96,13 @@ KGQ_API int kgq_unpack_codes(const uint8_t *packed, int64_t rows, int32_t cols, 
  * bit-identical to scipy csr_matvecs).  For the symmetric A_hat this is also
  * spmm_t (tape.py:217-218).  Row i of the output uses indptr[i]..indptr[i+1]
  * as given, so a row-partitioned CSR (global column ids) works unchanged.
- * row_order (optional, n_rows int32): the order rows are scheduled in (e.g.
- * by decreasing degree, for load balance); it never changes the result.     */
+ * row_order (optional, n_rows int32): the order rows are scheduled in, by
+ * decreasing degree; its first n_heavy rows (long rows) each get a whole CTA
+ * (features split across threads, neighbours streamed through shared memory),
+ * the rest are processed d/8 lanes per row.  Neither changes the result.    */
 KGQ_API int kgq_spmm_csr_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
-                     int64_t n_rows, const int32_t *row_order, const float *x, int32_t d,
-                     float *out, void *stream);
+                     int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
+                     const float *x, int32_t d, float *out, void *stream);
 
 /* relu + BitMask.from_bool, tensorops.py:84-92 / tape.py:122-126:
  * out = max(x, 0), mask bit i = x[i] > 0, LSB-first flat, ceil(n/8) bytes.  */
@@ -128,8 +130,8 @@ KGQ_API int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges, c
  * H and J are never written to memory.  h_out (optional, may be NULL) receives
  * H for debugging/parity.  d in {32, 64, 128}. */
 KGQ_API int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
-                          int64_t n_rows, const int32_t *row_order, const float *e, int32_t d,
-                          const float *theta,
+                          int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
+                          const float *e, int32_t d, const float *theta,
                           int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
                           int64_t row_offset, uint8_t *codes, float *ranges, float *offsets, float *e_next,
                           uint8_t *mask, float *h_out, void *stream);

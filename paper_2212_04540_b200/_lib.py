@@ -39,12 +39,12 @@ SIGNATURES = {
     "kgq_compat_noise_raw53": (ctypes.c_int, [_U64, _U64, _I64, _I64, _I32, _P, _P]),
     "kgq_pack_codes": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P, _P]),
     "kgq_unpack_codes": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P]),
-    "kgq_spmm_csr_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _I32, _P, _P]),
+    "kgq_spmm_csr_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _I32, _P, _P]),
     "kgq_relu_mask_f32": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
     "kgq_mask_apply_f32": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
     "kgq_dequant_gemm_workspace_bytes": (_SZ, [_I64, _I32]),
     "kgq_dequant_gemm_tn_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _I32, _P]),
-    "kgq_layer_forward_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _I32, _P, _I32, _I32, _U64, _U64,
+    "kgq_layer_forward_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _I32, _P, _I32, _I32, _U64, _U64,
                                              _I64, _P, _P, _P, _P, _P, _P, _P]),
 }
 

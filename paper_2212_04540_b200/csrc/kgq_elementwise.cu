@@ -1,0 +1,131 @@
+// kgq_elementwise.cu -- ReLU + 1-bit mask (K5, tensorops.py:84-92 / tape.py:122-126)
+// and its backward g * mask (tape.py:224-225) for sm_100a.
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+// spread the 8 bits of b so that bit k lands at bit 4k
+__device__ __forceinline__ uint32_t spread4(uint32_t b) {
+    b &= 0xFFu;
+    b = (b | (b << 12)) & 0x000F000Fu;
+    b = (b | (b << 6)) & 0x03030303u;
+    b = (b | (b << 3)) & 0x11111111u;
+    return b;
+}
+
+// relu + LSB-first flat bit mask.  A warp handles 128 elements per step:
+// lane l loads float4 l; ballot e collects bit (4l+e); lanes 0..3 assemble
+// the four 32-bit mask words.
+__global__ void __launch_bounds__(256)
+relu_mask_kernel(const float *__restrict__ x, int64_t n128, float *__restrict__ out,
+                 uint32_t *__restrict__ mask) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < n128; c += nw) {
+        const float4 v = ldg_stream(reinterpret_cast<const float4 *>(x) + c * 32 + lane);
+        const uint32_t b0 = __ballot_sync(0xffffffffu, v.x > 0.0f);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, v.y > 0.0f);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, v.z > 0.0f);
+        const uint32_t b3 = __ballot_sync(0xffffffffu, v.w > 0.0f);
+        const float4 o = make_float4(v.x > 0.0f ? v.x : 0.0f, v.y > 0.0f ? v.y : 0.0f,
+                                     v.z > 0.0f ? v.z : 0.0f, v.w > 0.0f ? v.w : 0.0f);
+        stg_stream(reinterpret_cast<float4 *>(out) + c * 32 + lane, o);
+        if (lane < 4) {
+            const int sh = 8 * lane;
+            const uint32_t w = spread4(b0 >> sh) | (spread4(b1 >> sh) << 1) |
+                               (spread4(b2 >> sh) << 2) | (spread4(b3 >> sh) << 3);
+            mask[c * 4 + lane] = w;
+        }
+    }
+}
+
+// tail / unaligned: thread per mask byte
+__global__ void relu_mask_bytes_kernel(const float *__restrict__ x, int64_t start, int64_t n,
+                                       float *__restrict__ out, uint8_t *__restrict__ mask) {
+    const int64_t nb = (n - start + 7) / 8;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t byte = 0;
+        for (int t = 0; t < 8; t++) {
+            const int64_t i = start + 8 * b + t;
+            if (i >= n) break;
+            const float v = x[i];
+            out[i] = v > 0.0f ? v : 0.0f;
+            byte |= (v > 0.0f ? 1u : 0u) << t;
+        }
+        mask[start / 8 + b] = (uint8_t)byte;
+    }
+}
+
+// ReLU backward: out = g * float(mask bit) (tape.py:224-225: g * mask.to_bool())
+__global__ void mask_apply_kernel(const float *__restrict__ g, const uint8_t *__restrict__ mask,
+                                  int64_t n, float *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t bit = (mask[i >> 3] >> (i & 7)) & 1u;
+        out[i] = __fmul_rn(g[i], bit ? 1.0f : 0.0f);
+    }
+}
+
+__global__ void mask_apply_vec_kernel(const float4 *__restrict__ g, const uint8_t *__restrict__ mask,
+                                      int64_t n4, float4 *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = (mask[i >> 1] >> (4 * (i & 1))) & 0xFu;
+        const float4 v = ldg_stream(g + i);
+        stg_stream(out + i, make_float4(__fmul_rn(v.x, (m & 1u) ? 1.0f : 0.0f),
+                                        __fmul_rn(v.y, (m & 2u) ? 1.0f : 0.0f),
+                                        __fmul_rn(v.z, (m & 4u) ? 1.0f : 0.0f),
+                                        __fmul_rn(v.w, (m & 8u) ? 1.0f : 0.0f)));
+    }
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+extern "C" int kgq_relu_mask_f32(const float *x, int64_t n, float *out, uint8_t *mask, void *stream) {
+    if (n < 0) return KGQ_ERR_INVALID_ARG;
+    if (n == 0) return KGQ_OK;
+    if (!x || !out || !mask) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t n128 = 0;
+    if ((((uintptr_t)x | (uintptr_t)out) & 15u) == 0 && ((uintptr_t)mask & 3u) == 0) n128 = n / 128;
+    if (n128) {
+        int64_t blocks = (n128 + 7) / 8;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        relu_mask_kernel<<<(int)blocks, 256, 0, s>>>(x, n128, out, reinterpret_cast<uint32_t *>(mask));
+    }
+    const int64_t start = n128 * 128;
+    if (start < n) {
+        const int64_t nb = (n - start + 7) / 8;
+        int64_t blocks = (nb + 255) / 256;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        relu_mask_bytes_kernel<<<(int)blocks, 256, 0, s>>>(x, start, n, out, mask);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_mask_apply_f32(const float *g, const uint8_t *mask, int64_t n, float *out,
+                                  void *stream) {
+    if (n < 0) return KGQ_ERR_INVALID_ARG;
+    if (n == 0) return KGQ_OK;
+    if (!g || !mask || !out) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((n & 3) == 0 && (((uintptr_t)g | (uintptr_t)out) & 15u) == 0) {
+        const int64_t n4 = n / 4;
+        int64_t blocks = (n4 + 255) / 256;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        mask_apply_vec_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(g), mask, n4,
+                                                          reinterpret_cast<float4 *>(out));
+    } else {
+        int64_t blocks = (n + 255) / 256;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        mask_apply_kernel<<<(int)blocks, 256, 0, s>>>(g, mask, n, out);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+

@@ -1,32 +1,49 @@
-// kgq_graph.cu -- KG neighbour aggregation (K4 CSR SpMM), ReLU + 1-bit mask
-// (K5) and the fused per-layer forward (spmm -> quantize H -> H.theta -> relu
-// -> mask) for sm_100a.
+// kgq_graph.cu -- KG neighbour aggregation (K4 CSR SpMM) and the fused
+// per-layer forward (spmm -> quantize H -> H.theta -> relu -> mask) on sm_100a.
 //
-// Row-group layout (d in {32, 64, 128}): a row is owned by LPR = d/8 lanes and
-// a warp works on RPW = 32/LPR rows at once.  Lane gl of a row group owns the
-// two float4 at feature offsets 32p+4q and 32p+16+4q (p = gl>>2, q = gl&3):
-// one neighbour row is gathered with one 128-bit load per lane (fully used
-// sectors), and those 8 features are exactly the 8 elements of fast-noise
-// call 4p+q, so the fused quantizer needs one Philox call per lane.
-// Every output element is accumulated in ascending column order as
-// acc = acc + a*x with separate mul and add -- the order scipy's csr_matvecs
-// uses (tensorops.py:8-12, 37-50) -- so results are bit-identical; only the
-// loads are reordered (4 neighbours x 2 float4 in flight per lane).
-// Rows are visited in an optional degree-sorted order (row_order) so the RPW
-// rows of a warp have similar lengths.
+// Exactness: every output element is accumulated in ascending column order
+// as acc = acc + a*x with separate mul and add -- the order scipy's
+// csr_matvecs uses (tensorops.py:8-12, 37-50) -- so results are bit-identical
+// to the reference.  Only the LOADS are reordered/prefetched; the per-element
+// add chain is never split, so rows cannot be divided across threads along
+// the nonzero axis.  What we parallelise instead is (a) rows, (b) features.
+//
+// Schedule (row_order = rows by decreasing degree, n_heavy = #rows above
+// kHeavy nonzeros; both built once per graph by the host):
+//  * heavy rows (the first n_heavy of row_order): one CTA per row.  Thread t
+//    owns feature t and runs that feature's sequential chain; all 256
+//    threads stream the row's neighbour rows into a P-stage shared-memory
+//    ring with cp.async (32 neighbours per stage), with the next stage's
+//    column ids prefetched into registers one iteration ahead, so a 6k-nonzero
+//    hub row costs ~nnz/(P*32) memory latencies instead of ~nnz/8.
+//  * light rows: row groups.  A row is owned by LPR = d/8 lanes and a warp
+//    works on RPW = 32/LPR rows of similar degree at once.  Lane gl owns the
+//    two float4 at features 32p+4q and 32p+16+4q (p = gl>>2, q = gl&3): one
+//    neighbour row is one 128-bit load per lane, and those 8 features are
+//    the 8 elements of fast-noise call 4p+q (one Philox call per lane in the
+//    fused quantizer).  The next column ids are prefetched while the current
+//    neighbour rows are gathered.
 #include "kgq_common.cuh"
 
 namespace kgq {
 
+constexpr int kCH = 32;             // neighbours per ring stage (heavy path)
+
 template <int D>
 struct RG {
-    static constexpr int LPR = D / 8;      // lanes per row
+    static constexpr int LPR = D / 8;      // lanes per row (light path)
     static constexpr int RPW = 32 / LPR;   // rows per warp
+    // heavy-path ring: P stages of kCH neighbour rows (<= 32 KB) + values
+    static constexpr int P = (32 * 1024) / (kCH * D * 4) > 4 ? 4 : (32 * 1024) / (kCH * D * 4);
+    static constexpr int NI = kCH * D / 4 / 256;           // cp.async per thread per stage
+    static constexpr size_t ring_bytes = (size_t)P * kCH * (D + 1) * 4;
 };
 
-// Sequential ascending-column accumulation of one row (bit-exact with scipy).
-// All lanes of the warp must call this together: the nonzero loop runs to the
-// warp's longest row with per-row predicates so shuffles stay convergent.
+// ---------------------------------------------------------------------------
+// Light path: one row per LPR-lane group (all lanes of the warp call this
+// together; the nonzero loop runs to the warp's longest row with per-row
+// predicates so shuffles stay convergent).
+// ---------------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
                                             const int32_t *__restrict__ indices,
@@ -40,18 +57,24 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
         beg = __ldg(indptr + row);
         end = __ldg(indptr + row + 1);
     }
-    int len = end - beg;
+    const int len = end - beg;
     int maxlen = len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     const int f0 = 8 * (gl >> 2) + (gl & 3);
+    int32_t nx_col = 0;
+    float nx_val = 0.0f;
+    if (gl < len) {
+        nx_col = __ldg(indices + beg + gl);
+        nx_val = __ldg(vals + beg + gl);
+    }
     for (int base = 0; base < maxlen; base += LPR) {
         const int cnt = min(LPR, len - base);         // may be <= 0 for short rows
-        int32_t my_col = 0;
-        float my_val = 0.0f;
-        if (gl < cnt) {
-            my_col = __ldg(indices + beg + base + gl);
-            my_val = __ldg(vals + beg + base + gl);
+        const int32_t my_col = nx_col;
+        const float my_val = nx_val;
+        if (gl < len - base - LPR) {                  // prefetch the next LPR column ids
+            nx_col = __ldg(indices + beg + base + LPR + gl);
+            nx_val = __ldg(vals + beg + base + LPR + gl);
         }
 #pragma unroll
         for (int t = 0; t < LPR; t += 4) {
@@ -85,21 +108,96 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Heavy path: one row per CTA (256 threads).  Thread t < D ends with H[row][t].
+// ring: P stages x kCH rows x D floats, then P x kCH values.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indptr,
+                                                const int32_t *__restrict__ indices,
+                                                const float *__restrict__ vals,
+                                                const float *__restrict__ x, int64_t row,
+                                                float *ring) {
+    constexpr int P = RG<D>::P, NI = RG<D>::NI;
+    float *xs = ring;                               // [P][kCH][D]
+    float *vs = ring + P * kCH * D;                 // [P][kCH]
+    const int t = threadIdx.x;
+    const int32_t beg = __ldg(indptr + row), end = __ldg(indptr + row + 1);
+    const int n = end - beg;
+    const int nch = (n + kCH - 1) / kCH;
+    int32_t pcol[NI];
+    float pval = 0.0f;
+    auto load_idx = [&](int c) {
+#pragma unroll
+        for (int m = 0; m < NI; m++) {
+            const int i = t + 256 * m, r = i / (D / 4);
+            const int k = c * kCH + r;
+            pcol[m] = (k < n) ? __ldg(indices + beg + k) : -1;
+        }
+        if (t < kCH) pval = (c * kCH + t < n) ? __ldg(vals + beg + c * kCH + t) : 0.0f;
+    };
+    auto issue = [&](int c) {
+        const int st = c % P;
+#pragma unroll
+        for (int m = 0; m < NI; m++) {
+            const int i = t + 256 * m, r = i / (D / 4), f4 = i % (D / 4);
+            if (pcol[m] >= 0)
+                cp_async16(xs + (st * kCH + r) * D + f4 * 4, x + (int64_t)pcol[m] * D + f4 * 4);
+        }
+        if (t < kCH) vs[st * kCH + t] = pval;
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int c = 0; c < P - 1; c++) {
+        load_idx(c);
+        issue(c);
+    }
+    load_idx(P - 1);
+    float acc = 0.0f;
+    for (int c = 0; c < nch; c++) {
+        cp_async_wait<P - 2>();
+        __syncthreads();
+        const int st = c % P;
+        if (t < D) {
+            const int cnt = min(kCH, n - c * kCH);
+            const float *xr = xs + st * kCH * D + t;
+            const float *vr = vs + st * kCH;
+            for (int r = 0; r < cnt; r++) acc = __fadd_rn(acc, __fmul_rn(vr[r], xr[r * D]));
+        }
+        __syncthreads();
+        issue(c + P - 1);
+        load_idx(c + P);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    return acc;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256)
-spmm_rg_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-               const float *__restrict__ vals, int64_t n_rows, const int32_t *__restrict__ row_order,
-               const float *__restrict__ x, float *__restrict__ out) {
+spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+            const float *__restrict__ vals, int64_t n_rows, const int32_t *__restrict__ row_order,
+            int64_t n_heavy, const float *__restrict__ x, float *__restrict__ out) {
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
+    extern __shared__ __align__(16) float dyn[];
+    if ((int64_t)blockIdx.x < n_heavy) {
+        const int64_t row = __ldg(row_order + blockIdx.x);
+        const float h = heavy_spmm_row<D>(indptr, indices, vals, x, row, dyn);
+        if (threadIdx.x < D) out[row * D + threadIdx.x] = h;
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int gl = lane % LPR, grp = lane / LPR;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t lb = (int64_t)blockIdx.x - n_heavy;
+    const int64_t nlb = (int64_t)gridDim.x - n_heavy;
+    const int64_t warp = lb * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nw = nlb * (blockDim.x >> 5);
+    const int64_t n_light = n_rows - n_heavy;
     const int f0 = 8 * (gl >> 2) + (gl & 3);
-    for (int64_t base = warp * RPW; base < n_rows; base += nw * RPW) {
+    for (int64_t base = warp * RPW; base < n_light; base += nw * RPW) {
         const int64_t slot = base + grp;
-        const bool active = slot < n_rows;
-        const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + slot) : slot) : 0;
+        const bool active = slot < n_light;
+        const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
         float4 acc[2];
         rg_spmm_row<D>(indptr, indices, vals, x, row, active, gl, acc);
         if (active) {
@@ -127,120 +225,105 @@ spmm_generic_kernel(const int32_t *__restrict__ indptr, const int32_t *__restric
     }
 }
 
-// spread the 8 bits of b so that bit k lands at bit 4k
-__device__ __forceinline__ uint32_t spread4(uint32_t b) {
-    b &= 0xFFu;
-    b = (b | (b << 12)) & 0x000F000Fu;
-    b = (b | (b << 6)) & 0x03030303u;
-    b = (b | (b << 3)) & 0x11111111u;
-    return b;
-}
-
-// relu + LSB-first flat bit mask.  A warp handles 128 elements per step:
-// lane l loads float4 l; ballot e collects bit (4l+e); lanes 0..3 assemble
-// the four 32-bit mask words.
-__global__ void __launch_bounds__(256)
-relu_mask_kernel(const float *__restrict__ x, int64_t n128, float *__restrict__ out,
-                 uint32_t *__restrict__ mask) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c = warp; c < n128; c += nw) {
-        const float4 v = ldg_stream(reinterpret_cast<const float4 *>(x) + c * 32 + lane);
-        const uint32_t b0 = __ballot_sync(0xffffffffu, v.x > 0.0f);
-        const uint32_t b1 = __ballot_sync(0xffffffffu, v.y > 0.0f);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, v.z > 0.0f);
-        const uint32_t b3 = __ballot_sync(0xffffffffu, v.w > 0.0f);
-        const float4 o = make_float4(v.x > 0.0f ? v.x : 0.0f, v.y > 0.0f ? v.y : 0.0f,
-                                     v.z > 0.0f ? v.z : 0.0f, v.w > 0.0f ? v.w : 0.0f);
-        stg_stream(reinterpret_cast<float4 *>(out) + c * 32 + lane, o);
-        if (lane < 4) {
-            const int sh = 8 * lane;
-            const uint32_t w = spread4(b0 >> sh) | (spread4(b1 >> sh) << 1) |
-                               (spread4(b2 >> sh) << 2) | (spread4(b3 >> sh) << 3);
-            mask[c * 4 + lane] = w;
-        }
-    }
-}
-
-// tail / unaligned: thread per mask byte
-__global__ void relu_mask_bytes_kernel(const float *__restrict__ x, int64_t start, int64_t n,
-                                       float *__restrict__ out, uint8_t *__restrict__ mask) {
-    const int64_t nb = (n - start + 7) / 8;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t byte = 0;
-        for (int t = 0; t < 8; t++) {
-            const int64_t i = start + 8 * b + t;
-            if (i >= n) break;
-            const float v = x[i];
-            out[i] = v > 0.0f ? v : 0.0f;
-            byte |= (v > 0.0f ? 1u : 0u) << t;
-        }
-        mask[start / 8 + b] = (uint8_t)byte;
-    }
-}
-
-// ReLU backward: out = g * float(mask bit) (tape.py:224-225: g * mask.to_bool())
-__global__ void mask_apply_kernel(const float *__restrict__ g, const uint8_t *__restrict__ mask,
-                                  int64_t n, float *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t bit = (mask[i >> 3] >> (i & 7)) & 1u;
-        out[i] = __fmul_rn(g[i], bit ? 1.0f : 0.0f);
-    }
-}
-
-__global__ void mask_apply_vec_kernel(const float4 *__restrict__ g, const uint8_t *__restrict__ mask,
-                                      int64_t n4, float4 *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t m = (mask[i >> 1] >> (4 * (i & 1))) & 0xFu;
-        const float4 v = ldg_stream(g + i);
-        stg_stream(out + i, make_float4(__fmul_rn(v.x, (m & 1u) ? 1.0f : 0.0f),
-                                        __fmul_rn(v.y, (m & 2u) ? 1.0f : 0.0f),
-                                        __fmul_rn(v.z, (m & 4u) ? 1.0f : 0.0f),
-                                        __fmul_rn(v.w, (m & 8u) ? 1.0f : 0.0f)));
-    }
-}
-
 // ---------------------------------------------------------------------------
-// Fused layer forward (row-group layout):
-//   H = A_hat.E (bit-exact spmm), quantize H on chip (group = d; same
-//   arithmetic and noise as kgq_quantize_f32: lane gl's 8 features are the 8
-//   elements of call 4p+q), J = H.theta (theta in smem, FFMA, ascending k),
-//   E' = relu(J), mask = J > 0.  H and J never reach HBM.
+// Fused layer forward: H = A_hat.E (bit-exact), quantize H on chip (group =
+// d; the same arithmetic and noise as kgq_quantize_f32), J = H.theta (theta
+// in smem, FFMA over ascending k), E' = relu(J), mask = J > 0.  H and J never
+// reach HBM.  Dynamic smem: theta (D*D fp32) then the heavy-path ring.
 // ---------------------------------------------------------------------------
 template <int D, int BITS, int MODE>
 __global__ void __launch_bounds__(256)
 layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
                      const float *__restrict__ vals, int64_t n_rows,
-                     const int32_t *__restrict__ row_order, const float *__restrict__ e,
-                     const float *__restrict__ theta, uint64_t seed, uint64_t tid,
-                     int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
-                     float *__restrict__ offsets, float *__restrict__ e_next,
-                     uint32_t *__restrict__ mask, float *__restrict__ h_out) {
+                     const int32_t *__restrict__ row_order, int64_t n_heavy,
+                     const float *__restrict__ e, const float *__restrict__ theta, uint64_t seed,
+                     uint64_t tid, int64_t row_offset, uint8_t *__restrict__ codes,
+                     float *__restrict__ ranges, float *__restrict__ offsets,
+                     float *__restrict__ e_next, uint32_t *__restrict__ mask,
+                     float *__restrict__ h_out) {
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
     constexpr float Bf = (float)((1u << BITS) - 1u);
     constexpr int RB = D * BITS / 8;                // packed bytes per row
-    extern __shared__ __align__(16) float th[];     // theta, D*D fp32 (64 KB at D=128)
+    constexpr int LPW = 32 / BITS;                  // codes per 32-bit word
+    extern __shared__ __align__(16) float dyn[];
+    float *th = dyn;                                // [D][D]
+    float *ring = dyn + D * D;                      // heavy-path staging
+    __shared__ float red[2][8];
+    __shared__ float hrow[D];
     for (int i = threadIdx.x; i < D * D / 4; i += blockDim.x)
         reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
     __syncthreads();
+    const FastKey fk = make_fast_key(seed, tid);
 
+    if ((int64_t)blockIdx.x < n_heavy) {
+        // ------------------------- heavy row: CTA -------------------------
+        const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+        const int64_t row = __ldg(row_order + blockIdx.x);
+        const float h = heavy_spmm_row<D>(indptr, indices, vals, e, row, ring);
+        const bool own = t < D;                     // warps 0 .. D/32-1 hold the row
+        if (own && h_out) h_out[row * D + t] = h;
+        float mn = own ? h : INFINITY, mx = own ? h : -INFINITY;
+        mn = warp_min(mn, 32);
+        mx = warp_max(mx, 32);
+        if (lane == 0) { red[0][wid] = mn; red[1][wid] = mx; }
+        if (own) hrow[t] = h;
+        __syncthreads();
+        mn = red[0][0];
+        mx = red[1][0];
+#pragma unroll
+        for (int w = 1; w < D / 32; w++) { mn = fminf(mn, red[0][w]); mx = fmaxf(mx, red[1][w]); }
+        const float z = mn, r = __fsub_rn(mx, mn);
+        const uint64_t gglob = (uint64_t)(row_offset + row);
+        if (own) {
+            uint32_t code = 0;
+            if (r > 0.0f) {
+                const DivR dv = make_div(r);
+                const float s = __fmul_rn(div_a(dv, __fsub_rn(h, z)), Bf);
+                float uf = 0.0f;
+                uint64_t raw53 = 0;
+                if (MODE == KGQ_ROUND_SR_FAST) uf = __uint2float_rn(fast_u16(fk, gglob, t));
+                if (MODE == KGQ_ROUND_SR_COMPAT) raw53 = compat_raw53(seed, tid, gglob, D, t);
+                code = code_bits<MODE>(s, uf, raw53) - kMagicBits;
+            }
+            // feature t = 32*wid + lane: word (t*BITS)/32 collects LPW lanes
+            const uint32_t mine = code << ((lane % LPW) * BITS);
+            const int wib = lane / LPW;
+#pragma unroll
+            for (int w = 0; w < 32 / LPW; w++) {
+                const uint32_t word = __reduce_or_sync(0xffffffffu, wib == w ? mine : 0u);
+                if (lane == w)
+                    reinterpret_cast<uint32_t *>(codes + row * RB)[wid * (32 / LPW) + w] = word;
+            }
+            if (t == 0) {
+                ranges[row] = r;
+                offsets[row] = z;
+            }
+            float j = 0.0f;
+#pragma unroll 8
+            for (int k = 0; k < D; k++) j = __fmaf_rn(hrow[k], th[k * D + t], j);
+            const bool pos = j > 0.0f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, pos);
+            e_next[row * D + t] = pos ? j : 0.0f;
+            if (lane == 0) mask[row * (D / 32) + wid] = bal;
+        }
+        return;
+    }
+
+    // ------------------------- light rows: row groups -----------------------
     const int lane = threadIdx.x & 31;
     const int gl = lane % LPR, grp = lane / LPR;
     const int p = gl >> 2, q = gl & 3;
     const int f0 = 8 * p + q;                       // float4 index of my first four features
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const FastKey fk = make_fast_key(seed, tid);
-    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+    const int64_t lb = (int64_t)blockIdx.x - n_heavy;
+    const int64_t nlb = (int64_t)gridDim.x - n_heavy;
+    const int64_t warp = lb * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nw = nlb * (blockDim.x >> 5);
+    const int64_t n_light = n_rows - n_heavy;
 
-    for (int64_t base = warp * RPW; base < n_rows; base += nw * RPW) {
+    for (int64_t base = warp * RPW; base < n_light; base += nw * RPW) {
         const int64_t slot = base + grp;
-        const bool active = slot < n_rows;
-        const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + slot) : slot) : 0;
+        const bool active = slot < n_light;
+        const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
         float4 h[2];
         rg_spmm_row<D>(indptr, indices, vals, e, row, active, gl, h);
         if (active && h_out) {
@@ -343,7 +426,6 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
                                     j1.z > 0.f ? j1.z : 0.f, j1.w > 0.f ? j1.w : 0.f);
             if (q == 0) mask[row * (D / 32) + p] = w;
         }
-        (void)gmask;
     }
 }
 
@@ -351,88 +433,63 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
 
 using namespace kgq;
 
-static inline int persistent_blocks(int64_t warps_needed, int per_sm) {
-    int64_t b = (warps_needed + 7) / 8;
+static inline int light_blocks(int64_t n_light, int rpw, int per_sm) {
+    int64_t warps = (n_light + rpw - 1) / rpw;
+    int64_t b = (warps + 7) / 8;
     const int64_t cap = (int64_t)kSMs * per_sm;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
 }
 
+template <typename K>
+static cudaError_t ensure_smem(K kern, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int D>
+static int launch_spmm(const int32_t *indptr, const int32_t *indices, const float *vals,
+                       int64_t n_rows, const int32_t *row_order, int64_t n_heavy, const float *x,
+                       float *out, cudaStream_t s) {
+    const size_t smem = n_heavy ? RG<D>::ring_bytes : 0;
+    cudaError_t ea = ensure_smem(spmm_kernel<D>, smem);
+    if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 16);
+    spmm_kernel<D><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out);
+    return KGQ_OK;
+}
+
 extern "C" int kgq_spmm_csr_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
-                                int64_t n_rows, const int32_t *row_order, const float *x, int32_t d,
-                                float *out, void *stream) {
-    if (n_rows < 0 || d < 1) return KGQ_ERR_INVALID_ARG;
+                                int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
+                                const float *x, int32_t d, float *out, void *stream) {
+    if (n_rows < 0 || d < 1 || n_heavy < 0 || n_heavy > n_rows) return KGQ_ERR_INVALID_ARG;
+    if (n_heavy && !row_order) return KGQ_ERR_INVALID_ARG;
     if (n_rows == 0) return KGQ_OK;
     if (!indptr || !out || !x) return KGQ_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const bool vec = ((((uintptr_t)x) | ((uintptr_t)out)) & 15u) == 0;
-    if (vec && d == 32) {
-        spmm_rg_kernel<32><<<persistent_blocks((n_rows + 7) / 8, 16), 256, 0, s>>>(indptr, indices, vals, n_rows, row_order, x, out);
-    } else if (vec && d == 64) {
-        spmm_rg_kernel<64><<<persistent_blocks((n_rows + 3) / 4, 16), 256, 0, s>>>(indptr, indices, vals, n_rows, row_order, x, out);
-    } else if (vec && d == 128) {
-        spmm_rg_kernel<128><<<persistent_blocks((n_rows + 1) / 2, 16), 256, 0, s>>>(indptr, indices, vals, n_rows, row_order, x, out);
-    } else {
+    int st = KGQ_OK;
+    if (vec && d == 32) st = launch_spmm<32>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out, s);
+    else if (vec && d == 64) st = launch_spmm<64>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out, s);
+    else if (vec && d == 128) st = launch_spmm<128>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out, s);
+    else {
         int64_t b = (n_rows + 7) / 8;
         spmm_generic_kernel<<<(int)(b < 0x7fffffff ? b : 0x7fffffff), 256, 0, s>>>(indptr, indices, vals, n_rows, x, d, out);
     }
-    KGQ_LAUNCH_CHECK();
-    return KGQ_OK;
-}
-extern "C" int kgq_relu_mask_f32(const float *x, int64_t n, float *out, uint8_t *mask, void *stream) {
-    if (n < 0) return KGQ_ERR_INVALID_ARG;
-    if (n == 0) return KGQ_OK;
-    if (!x || !out || !mask) return KGQ_ERR_INVALID_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
-    int64_t n128 = 0;
-    if ((((uintptr_t)x | (uintptr_t)out) & 15u) == 0 && ((uintptr_t)mask & 3u) == 0) n128 = n / 128;
-    if (n128) {
-        int64_t blocks = (n128 + 7) / 8;
-        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
-        relu_mask_kernel<<<(int)blocks, 256, 0, s>>>(x, n128, out, reinterpret_cast<uint32_t *>(mask));
-    }
-    const int64_t start = n128 * 128;
-    if (start < n) {
-        const int64_t nb = (n - start + 7) / 8;
-        int64_t blocks = (nb + 255) / 256;
-        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
-        relu_mask_bytes_kernel<<<(int)blocks, 256, 0, s>>>(x, start, n, out, mask);
-    }
-    KGQ_LAUNCH_CHECK();
-    return KGQ_OK;
-}
-
-extern "C" int kgq_mask_apply_f32(const float *g, const uint8_t *mask, int64_t n, float *out,
-                                  void *stream) {
-    if (n < 0) return KGQ_ERR_INVALID_ARG;
-    if (n == 0) return KGQ_OK;
-    if (!g || !mask || !out) return KGQ_ERR_INVALID_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
-    if ((n & 3) == 0 && (((uintptr_t)g | (uintptr_t)out) & 15u) == 0) {
-        const int64_t n4 = n / 4;
-        int64_t blocks = (n4 + 255) / 256;
-        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
-        mask_apply_vec_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(g), mask, n4,
-                                                          reinterpret_cast<float4 *>(out));
-    } else {
-        int64_t blocks = (n + 255) / 256;
-        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
-        mask_apply_kernel<<<(int)blocks, 256, 0, s>>>(g, mask, n, out);
-    }
+    if (st != KGQ_OK) return st;
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
 
 template <int D, int BITS>
 static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indices, const float *vals,
-                        int64_t n_rows, const int32_t *row_order, const float *e, const float *theta,
-                        uint64_t seed, uint64_t tid, int64_t row_offset, uint8_t *codes, float *ranges,
-                        float *offsets, float *e_next, uint32_t *mask, float *h_out,
-                        cudaStream_t s) {
-    const size_t smem = (size_t)D * D * sizeof(float);
-    const int blocks = persistent_blocks((n_rows + RG<D>::RPW - 1) / RG<D>::RPW, 8);
-    void (*kern)(const int32_t *, const int32_t *, const float *, int64_t, const int32_t *,
+                        int64_t n_rows, const int32_t *row_order, int64_t n_heavy, const float *e,
+                        const float *theta, uint64_t seed, uint64_t tid, int64_t row_offset,
+                        uint8_t *codes, float *ranges, float *offsets, float *e_next,
+                        uint32_t *mask, float *h_out, cudaStream_t s) {
+    const size_t smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
+    void (*kern)(const int32_t *, const int32_t *, const float *, int64_t, const int32_t *, int64_t,
                  const float *, const float *, uint64_t, uint64_t, int64_t, uint8_t *, float *,
                  float *, float *, uint32_t *, float *);
     switch (rounding) {
@@ -441,12 +498,11 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
         case KGQ_ROUND_SR_COMPAT: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
         default: return KGQ_ERR_INVALID_ARG;
     }
-    if (smem > 48 * 1024) {
-        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
-    }
-    kern<<<blocks, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, e, theta, seed, tid,
-                                   row_offset, codes, ranges, offsets, e_next, mask, h_out);
+    cudaError_t ea = ensure_smem(kern, smem);
+    if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 8);
+    kern<<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed,
+                                 tid, row_offset, codes, ranges, offsets, e_next, mask, h_out);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
@@ -454,28 +510,34 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
 template <int D>
 static int launch_layer_bits(int bits, int rounding, const int32_t *indptr, const int32_t *indices,
                              const float *vals, int64_t n_rows, const int32_t *row_order,
-                             const float *e, const float *theta,
-                             uint64_t seed, uint64_t tid, int64_t row_offset, uint8_t *codes,
-                             float *ranges, float *offsets, float *e_next, uint32_t *mask,
-                             float *h_out, cudaStream_t s) {
+                             int64_t n_heavy, const float *e, const float *theta, uint64_t seed,
+                             uint64_t tid, int64_t row_offset, uint8_t *codes, float *ranges,
+                             float *offsets, float *e_next, uint32_t *mask, float *h_out,
+                             cudaStream_t s) {
+#define KGQ_LAYER(B) launch_layer<D, B>(rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, \
+                                        theta, seed, tid, row_offset, codes, ranges, offsets, e_next, \
+                                        mask, h_out, s)
     switch (bits) {
-        case 1: return launch_layer<D, 1>(rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tid, row_offset, codes, ranges, offsets, e_next, mask, h_out, s);
-        case 2: return launch_layer<D, 2>(rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tid, row_offset, codes, ranges, offsets, e_next, mask, h_out, s);
-        case 4: return launch_layer<D, 4>(rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tid, row_offset, codes, ranges, offsets, e_next, mask, h_out, s);
-        case 8: return launch_layer<D, 8>(rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tid, row_offset, codes, ranges, offsets, e_next, mask, h_out, s);
+        case 1: return KGQ_LAYER(1);
+        case 2: return KGQ_LAYER(2);
+        case 4: return KGQ_LAYER(4);
+        case 8: return KGQ_LAYER(8);
     }
+#undef KGQ_LAYER
     return KGQ_ERR_UNSUPPORTED_BITS;
 }
 
 extern "C" int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
-                                     int64_t n_rows, const int32_t *row_order, const float *e,
-                                     int32_t d, const float *theta,
-                                     int32_t bits, int32_t rounding, uint64_t seed,
-                                     uint64_t tensor_id, int64_t row_offset, uint8_t *codes,
-                                     float *ranges, float *offsets, float *e_next, uint8_t *mask,
-                                     float *h_out, void *stream) {
+                                     int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
+                                     const float *e, int32_t d, const float *theta, int32_t bits,
+                                     int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                                     int64_t row_offset, uint8_t *codes, float *ranges,
+                                     float *offsets, float *e_next, uint8_t *mask, float *h_out,
+                                     void *stream) {
     if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
-    if (n_rows < 0 || row_offset < 0 || rounding < 0 || rounding > 2) return KGQ_ERR_INVALID_ARG;
+    if (n_rows < 0 || row_offset < 0 || rounding < 0 || rounding > 2 || n_heavy < 0 || n_heavy > n_rows)
+        return KGQ_ERR_INVALID_ARG;
+    if (n_heavy && !row_order) return KGQ_ERR_INVALID_ARG;
     if (n_rows == 0) return KGQ_OK;
     if (!indptr || !e || !theta || !codes || !ranges || !offsets || !e_next || !mask)
         return KGQ_ERR_INVALID_ARG;
@@ -485,9 +547,9 @@ extern "C" int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indic
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *m32 = reinterpret_cast<uint32_t *>(mask);
     switch (d) {
-        case 32: return launch_layer_bits<32>(bits, rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
-        case 64: return launch_layer_bits<64>(bits, rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
-        case 128: return launch_layer_bits<128>(bits, rounding, indptr, indices, vals, n_rows, row_order, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 32: return launch_layer_bits<32>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 64: return launch_layer_bits<64>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 128: return launch_layer_bits<128>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
     }
     return KGQ_ERR_INVALID_ARG;
 }

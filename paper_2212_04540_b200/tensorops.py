@@ -43,6 +43,7 @@ class CSR:
         self._symmetric = symmetric
         self._transpose = None
         self._row_order = None
+        self._n_heavy = 0
 
     @classmethod
     def from_scipy(cls, m, device="cuda", symmetric: bool | None = None) -> "CSR":
@@ -62,13 +63,18 @@ class CSR:
         return sp.csr_matrix((self.data.cpu().numpy(), self.indices.cpu().numpy(),
                               self.indptr.cpu().numpy()), shape=self.shape)
 
-    def row_order_ptr(self) -> int:
-        """Rows by decreasing degree (stable), built once: the schedule the
-        row-group kernels use so the rows of a warp have similar lengths."""
+    HEAVY_NNZ = 256     # rows above this many nonzeros get a whole CTA in the kernels
+
+    def schedule(self):
+        """(row_order pointer, n_heavy): rows by decreasing degree (stable),
+        built once.  The kernels give each of the first n_heavy (long) rows a
+        CTA and pack the rest d/8 lanes per row, so the rows sharing a warp
+        have similar lengths.  The schedule never changes results."""
         if self._row_order is None:
             deg = torch.diff(self.indptr.to(torch.int64))
             self._row_order = torch.sort(deg, descending=True, stable=True).indices.to(torch.int32)
-        return self._row_order.data_ptr()
+            self._n_heavy = int((deg > self.HEAVY_NNZ).sum())
+        return self._row_order.data_ptr(), self._n_heavy
 
     @property
     def nnz(self) -> int:
@@ -124,7 +130,7 @@ def mm(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 def spmm_into(s: CSR, d: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     st = _lib.load().kgq_spmm_csr_f32(s.indptr.data_ptr(), s.indices.data_ptr(), s.data.data_ptr(),
-                                      s.shape[0], s.row_order_ptr(), d.data_ptr(), d.shape[1],
+                                      s.shape[0], *s.schedule(), d.data_ptr(), d.shape[1],
                                       out.data_ptr(), _lib.stream_ptr(d.device))
     _lib.check(st, "kgq_spmm_csr_f32")
     return out

@@ -95,6 +95,34 @@ def test_tape_quantized_matches_reference(bits, fused):
         assert err <= 0.05 * scale + 1e-7, (name, err, scale)
 
 
+def _hub_graph(n, seed):
+    """Random symmetric graph plus hub rows far above the CTA-per-row
+    threshold (so both kernel paths run)."""
+    import scipy.sparse as sp
+    a = sp.random(n, n, density=0.004, random_state=seed, format="lil", dtype=np.float32)
+    rng = np.random.default_rng(seed)
+    for hub, deg in ((5, n - 1), (17, 1500), (400, 700), (999, 300)):
+        cols = rng.choice(n, size=deg, replace=False)
+        a[hub, cols] = rng.random(deg).astype(np.float32) + 0.1
+    a = a.tocsr()
+    a = (a + a.T + sp.eye(n, dtype=np.float32)).tocsr()
+    a.sum_duplicates()
+    a.sort_indices()
+    return a
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 48])
+def test_spmm_hub_rows_bit_exact(d):
+    kgq = _kgq()
+    a = _hub_graph(4000, d)
+    A = kgq.CSR.from_scipy(a)
+    assert A.schedule()[1] >= 4
+    x = np.random.default_rng(d).standard_normal((4000, d), dtype=np.float32)
+    out = kgq.spmm(A, torch.from_numpy(x).cuda()).cpu().numpy()
+    ref = orc.spmm_csr(a.indptr, a.indices, a.data, x)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
 def test_fused_layer_matches_unfused_and_oracle():
     """The fused kernel's H is the bit-exact SpMM and its codes equal a
     standalone quantize of that H; J within fp32 GEMM tolerance."""
@@ -104,8 +132,7 @@ def test_fused_layer_matches_unfused_and_oracle():
     rng = np.random.default_rng(0)
     for d in (32, 64, 128):
         n = 3000
-        a = sp.random(n, n, density=0.004, random_state=d, format="csr", dtype=np.float32)
-        a = (a + a.T + sp.eye(n, dtype=np.float32)).tocsr()
+        a = _hub_graph(n, d)
         a.sum_duplicates()
         a.sort_indices()
         A = kgq.CSR.from_scipy(a)
