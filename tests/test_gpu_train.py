@@ -226,3 +226,50 @@ def test_training_c1_matches_reference_run(bits):
     assert rep["memory"]["activation_bytes_peak"] == int(z[pre + "peak_ctx"])
     assert rep["memory"]["fp32_equivalent_bytes"] == int(z[pre + "peak_eq"])
     assert rep["memory"]["retained_context_bytes"] == 0
+
+
+def test_row_block_fused_layer_is_bit_identical_to_full():
+    """Multi-GPU row partitioning: a rank's row block (global column ids,
+    row_offset = its first global row) reproduces the full run's rows exactly."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import functional as F
+    a = _hub_graph(5000, 7)
+    A = kgq.CSR.from_scipy(a)
+    rng = np.random.default_rng(3)
+    e = torch.from_numpy(rng.standard_normal((5000, 64), dtype=np.float32)).cuda()
+    th = torch.from_numpy((rng.standard_normal((64, 64)) / 8).astype(np.float32)).cuda()
+    cfg = kgq.QuantConfig(bits=2)
+    full = F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(1), 4)
+    for w in (2, 4, 8):
+        cuts = D.partition_rows(a.indptr, w)
+        for r in range(w):
+            lo, hi = int(cuts[r]), int(cuts[r + 1])
+            ip, ix, vv = D.row_block(a.indptr, a.indices, a.data, lo, hi)
+            blk = kgq.CSR.from_arrays(ip, ix, vv, (hi - lo, 5000), symmetric=False)
+            en, m, q, _ = F.graph_conv_forward(blk, e, th, cfg, kgq.RandomStream(1), 4, row_offset=lo)
+            assert torch.equal(en, full[0][lo:hi])
+            assert torch.equal(q.codes, full[2].codes[lo:hi])
+            assert torch.equal(q.ranges, full[2].ranges[lo:hi])
+
+
+def test_partitioned_step_gpu_world1_matches_tape():
+    kgq, z, adj = _tiny()
+    from paper_2212_04540_b200.parallel import GpuOps, RowPartition, SoloComm, partitioned_step
+    from paper_2212_04540_b200.tape import Tape
+    n = int(z["n"])
+    cfg = kgq.QuantConfig(bits=2)
+    p = _params(kgq, z, 64, 3)
+    tape = Tape(cfg, kgq.RandomStream(21))
+    _record(kgq, tape, p, adj, z, 3, 64, True)
+    tg = tape.backward()
+    part = RowPartition.build(z["indptr"], 1, 0)
+    a_local = GpuOps.local_adjacency(z["indptr"], z["indices"], z["data"], 0, n, n, "cuda")
+    ix = lambda k: torch.from_numpy(z[k].astype(np.int64)).cuda()
+    loss, de0, dth = partitioned_step(part, a_local, p.entity_embeddings, p.layer_weights,
+                                      ix("users"), ix("pos"), ix("neg"), 1e-5, cfg,
+                                      kgq.RandomStream(21), SoloComm())
+    assert float(loss) == tape.loss()
+    np.testing.assert_allclose(de0.cpu().numpy(), tg["E0"].cpu().numpy(), rtol=1e-5, atol=1e-8)
+    for i, t in enumerate(dth):
+        np.testing.assert_allclose(t.cpu().numpy(), tg[f"theta{i}"].cpu().numpy(), rtol=1e-5, atol=1e-8)

@@ -1,0 +1,145 @@
+"""Row-partitioned training at world size 2 over gloo on CPU.
+
+The exchange logic of ``parallel.partitioned_step`` runs with the CPU oracle
+as its compute ops; the forward pass must be bit-identical to world size 1
+(noise keyed by global row), and so must the local E0 gradient rows; the
+theta gradients differ only by the all-reduce summation order."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+from paper_2212_04540_b200 import data as D
+from paper_2212_04540_b200.parallel import RowPartition, SoloComm, partitioned_step
+from paper_2212_04540_b200.quantize import QuantConfig, RandomStream
+from tests import golden_io
+
+
+class _Q:
+    def __init__(self, codes, ranges, offsets, rows, cols, bits):
+        self.codes, self.ranges, self.offsets = codes, ranges, offsets
+        self.rows, self.cols, self.bits = rows, cols, bits
+
+
+class _Mask:
+    def __init__(self, bits):
+        self.bits = bits
+
+
+class OracleOps:
+    """CPU stand-ins for the libkgq ops (the oracle is the checker)."""
+
+    @staticmethod
+    def local_adjacency(indptr, indices, vals, lo, hi, n, device=None):
+        return D.row_block(indptr, indices, vals, lo, hi)
+
+    @staticmethod
+    def _quant(x, cfg, stream, row_offset=0, tensor_id=None):
+        tid = stream.next_tensor_id() if tensor_id is None else tensor_id
+        x = np.ascontiguousarray(x.numpy(), dtype=np.float32)
+        mode = orc.MODE_SR_FAST if cfg.rng == "fast" else orc.MODE_SR_COMPAT
+        c, r, o = orc.quantize(x, x.shape[1], cfg.bits, mode, stream.seed, tid, group_offset=row_offset)
+        return _Q(c, r, o, x.shape[0], x.shape[1], cfg.bits)
+
+    @staticmethod
+    def graph_conv(a_local, e_full, theta, cfg, stream, row_offset=0):
+        ip, ix, vv = a_local
+        h = orc.spmm_csr(ip, ix, vv, e_full.numpy())
+        q = OracleOps._quant(torch.from_numpy(h), cfg, stream, row_offset)
+        j = h @ theta.numpy()
+        out, mask = orc.relu_mask(j)
+        return torch.from_numpy(out), _Mask(j > 0), q, None
+
+    @staticmethod
+    def quantize(t, cfg, stream):
+        return OracleOps._quant(t, cfg, stream)
+
+    @staticmethod
+    def dequantize(q):
+        return torch.from_numpy(orc.dequantize(q.codes, q.ranges, q.offsets, q.cols, q.bits))
+
+    @staticmethod
+    def dequant_gemm(q, g):
+        return OracleOps.dequantize(q).t() @ g
+
+    @staticmethod
+    def mask_apply(g, mask):
+        return g * torch.from_numpy(mask.bits.astype(np.float32))
+
+    @staticmethod
+    def spmm(a_local, x):
+        ip, ix, vv = a_local
+        return torch.from_numpy(orc.spmm_csr(ip, ix, vv, x.numpy()))
+
+    @staticmethod
+    def scatter_rows(rows, idx, g):
+        out = np.zeros((rows, g.shape[1]), dtype=np.float32)
+        np.add.at(out, idx.numpy().astype(np.int64), g.numpy())
+        return torch.from_numpy(out)
+
+
+def _problem():
+    z = golden_io.load("tape")
+    n = int(z["n"])
+    thetas = [torch.from_numpy(z[f"d64_theta{i}"]) for i in range(3)]
+    e0 = torch.from_numpy(z["d64_E0"])
+    idx = [torch.from_numpy(z[k].astype(np.int64)) for k in ("users", "pos", "neg")]
+    return z, n, e0, thetas, idx
+
+
+def _run(world, rank, comm):
+    z, n, e0, thetas, (users, pos, neg) = _problem()
+    part = RowPartition.build(z["indptr"], world, rank)
+    a_local = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
+    cfg = QuantConfig(bits=2)
+    loss, de0, dth = partitioned_step(part, a_local, e0[part.lo:part.hi], thetas, users, pos, neg,
+                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps)
+    return part, loss, de0, dth
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2212_04540_b200.parallel import Comm
+        part, loss, de0, dth = _run(world, rank, Comm())
+        out_q.put((rank, part.lo, part.hi, float(loss), de0.numpy(), [t.numpy() for t in dth]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partitioned_step_world2_gloo_matches_world1():
+    part1, loss1, de1, dth1 = _run(1, 0, SoloComm())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    de_full = np.zeros_like(de1.numpy())
+    for rank, lo, hi, loss, de, dth in res:
+        assert loss == float(loss1)                       # forward bit-identical
+        de_full[lo:hi] = de
+        for a, b in zip(dth, dth1):
+            np.testing.assert_allclose(a, b.numpy(), rtol=1e-5, atol=1e-8)
+    assert np.array_equal(de_full, de1.numpy())           # local E0 rows bit-identical
+
+
+def test_partitioned_world1_matches_reference_tape():
+    """W=1 partitioned step vs the reference Tape fed the same (fast) noise
+    (golden tape.npz, b=2): same loss, gradients within one code step."""
+    z, n, e0, thetas, (users, pos, neg) = _problem()
+    part, loss, de0, dth = _run(1, 0, SoloComm())
+    assert float(loss) == pytest.approx(float(z["d64_b2_loss"]), rel=1e-5)
+    for name, g in [("E0", de0)] + [(f"theta{i}", t) for i, t in enumerate(dth)]:
+        ref = z["d64_b2_grad_" + name]
+        assert np.abs(g.numpy() - ref).max() <= 0.05 * np.abs(ref).max() + 1e-7, name
