@@ -200,6 +200,126 @@ def workload_config(args):
                   % (args.rows * args.cols * 4 / 1e9)}
 
 
+def train_bench(args, world, rank):
+    """KGNN training on the Amazon-book-shaped synthetic KG (BASELINE configs[3];
+    159,251 nodes, 3 layers, d=64, B=1024) at INT2: ms/step, epochs/s and the
+    activation ledger.  world > 1: row-partitioned step (parallel.py, NCCL)."""
+    import torch
+    import paper_2212_04540_b200 as kgq
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig, init_params
+    from paper_2212_04540_b200.train import AdamState, TrainConfig, adam_step, memory_report, train_epoch
+
+    ds = D.synth_kg(D.SHAPES[args.train_shape], seed=0)
+    steps_per_epoch = (len(ds.train) + 1023) // 1024
+    out = {"workload": f"{args.train_shape}-shaped synthetic KG ({ds.num_users} users, {ds.num_items} items, "
+                       f"{ds.num_entities} entities, {len(ds.triples)} triples, {len(ds.train)} train pairs), "
+                       "KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
+           "steps_per_epoch": steps_per_epoch, "n_gpus": world}
+    res = {}
+    for bits in (2, 32):
+        q = kgq.QuantConfig(bits=bits)
+        mcfg = ModelConfig(layers=3, dim=64, quant=q)
+        cfg = TrainConfig(quant=q)
+        rng = np.random.default_rng(0)
+        stream = kgq.RandomStream(0)
+        cur = torch.cuda.current_stream()
+        if world == 1:
+            adj = D.build_adjacency(ds)
+            params = init_params(ds.num_nodes, mcfg, 0)
+            state = AdamState(params.as_dict())
+            train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.warmup + 2)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            st = train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.train_steps)
+            b.record(cur)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / st["steps"]
+            mem = memory_report(st["peak_context_bytes"], st["peak_fp32_equivalent_bytes"], st["adjacency_bytes"])
+            res[bits] = (ms, mem, st["mean_loss"])
+        else:
+            ms = _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args)
+            res[bits] = (ms, None, None)
+    ms2, mem2, loss2 = res[2]
+    ms32 = res[32][0]
+    out.update({"ms_per_step": round(ms2, 3), "epoch_s": round(ms2 * steps_per_epoch / 1e3, 3),
+                "epochs_per_s": round(1e3 / (ms2 * steps_per_epoch), 4),
+                "fp32_ms_per_step": round(ms32, 3),
+                "int2_time_overhead_vs_fp32": round(ms2 / ms32 - 1.0, 4),
+                "timed_steps": args.train_steps})
+    if world == 1 and rank == 0 and not args.skip_cpu:
+        # CPU port of the reference step (oracle/oracle.py dense engine: scipy
+        # CSR spmm + numpy GEMMs, the reference's op structure), 2 steps
+        from oracle import oracle as orc
+        indptr, indices, vals = D.adjacency_arrays(ds)
+        p0 = init_params(ds.num_nodes, ModelConfig(layers=3, dim=64), 0, device="cpu")
+        e0 = p0.entity_embeddings.numpy()
+        ths = [t.numpy() for t in p0.layer_weights]
+        trip = D.sample_negatives(ds, np.random.default_rng(0))[:1024]
+        t0 = time.perf_counter()
+        for _ in range(2):
+            orc.dense_step(e0, ths, indptr, indices, vals, trip[:, 0], ds.num_users + trip[:, 1],
+                           ds.num_users + trip[:, 2], 1e-5, dtype=np.float32)
+        cs = (time.perf_counter() - t0) / 2
+        out["cpu_baseline"] = {"value": round(cs * 1e3, 1), "unit": "ms/step", "cores": os.cpu_count(),
+                               "kind": "port",
+                               "sample": "2 fp32 steps of oracle.dense_step (numpy/scipy restatement of "
+                                         "the reference Tape step, no quantization) on the same graph"}
+    if mem2 is not None:
+        mb = lambda v: round(v / 1e6, 3)
+        out["activation_MB"] = {
+            "int2_incl_adjacency": mb(mem2["activation_bytes_peak"]),
+            "fp32_incl_adjacency": mb(mem2["fp32_equivalent_bytes"]),
+            "ratio_incl_adjacency": round(mem2["compression_ratio"], 3),
+            "int2_excl_adjacency": mb(mem2["activation_bytes_excl_adjacency"]),
+            "fp32_excl_adjacency": mb(mem2["fp32_equivalent_excl_adjacency"]),
+            "ratio_excl_adjacency": round(mem2["compression_ratio_excl_adjacency"], 3),
+            "definition": "reference ledger (tape.py:86-93): quantized contexts + masks + indices + "
+                          "margins; 'incl' also counts the shared CSR adjacency once (reference definition)"}
+        out["mean_loss_timed_steps"] = round(loss2, 5)
+    return out
+
+
+def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
+    """Row-partitioned step timing (parallel.partitioned_step over NCCL)."""
+    import torch
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import init_params
+    from paper_2212_04540_b200.parallel import Comm, GpuOps, RowPartition, partitioned_step
+    indptr, indices, vals = D.adjacency_arrays(ds)
+    part = RowPartition.build(indptr, world, rank)
+    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda")
+    params = init_params(ds.num_nodes, mcfg, 0)
+    e0 = params.entity_embeddings[part.lo:part.hi].clone()
+    thetas = params.layer_weights
+    comm = Comm()
+    trip = torch.from_numpy(D.sample_negatives(ds, rng)).cuda().long()
+    n_users = ds.num_users
+
+    def one(i):
+        b = trip[(i * 1024) % len(trip):][:1024]
+        loss, de0, dth = partitioned_step(part, a_local, e0, thetas, b[:, 0], n_users + b[:, 1],
+                                          n_users + b[:, 2], 1e-5, cfg.quant, stream, comm)
+        with torch.no_grad():
+            e0.sub_(1e-3 * de0)
+            for t, g in zip(thetas, dth):
+                t.sub_(1e-3 * g)
+
+    for i in range(args.warmup + 2):
+        one(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    cur = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(cur)
+    for i in range(args.train_steps):
+        one(100 + i)
+    b.record(cur)
+    torch.cuda.synchronize()
+    return max_over_ranks(a.elapsed_time(b) / args.train_steps, world)
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args)
@@ -312,6 +432,11 @@ def run_ours(args):
                "d2h_bytes_per_step": e_rows * cols * 4,
                "sample": f"{e_rows}x{cols} fp32 per GPU per step (pinned host buffers)"}
 
+    train = None
+    if not args.skip_train:
+        torch.cuda.empty_cache()
+        train = train_bench(args, world, rank)
+
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         threads = os.cpu_count() or 1
@@ -349,6 +474,7 @@ def run_ours(args):
             "gpu_launches": 2 * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "train": train,
             "native_lib": os.path.relpath(_lib.LIB_PATH, ROOT),
         }
         print(json.dumps(line), flush=True)
@@ -375,6 +501,9 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-compat", action="store_true")
+    ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--train-shape", default="amazon", choices=["small", "lastfm", "amazon"])
+    ap.add_argument("--train-steps", type=int, default=100)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("KGQ_ALLOW_SHORT_WARMUP"):
         args.warmup = 3
