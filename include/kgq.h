@@ -124,6 +124,14 @@ KGQ_API int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges, c
                             float *dtheta, void *workspace, size_t workspace_bytes,
                             int32_t accumulate, void *stream);
 
+/* Adam step, train.py:42-59, fused into one pass with the reference's numpy
+ * float32 op order (scalars rounded to float32, true divisions, separate
+ * roundings) -- bit-identical to the numpy update.  step >= 1 is the
+ * post-increment step count t. */
+KGQ_API int kgq_adam_step_f32(float *param, const float *grad, float *m, float *v, int64_t n,
+                      double lr, double beta1, double beta2, double eps, int64_t step,
+                      void *stream);
+
 /* Fused KGNN layer forward (model.py:81-85 + tape.py:101-126), one pass:
  *   H = spmm(A, E); ctx = quantize(H) (group = d); J = H @ theta;
  *   E_next = relu(J); mask = J > 0.

@@ -237,3 +237,17 @@ def dense_step(e0, thetas, indptr, indices, vals, users, pos, neg, l2, aggregati
         g_e = A.T @ g_h
     grads["E0"] = g_e
     return loss, grads
+
+
+def adam_step(params: dict, grads: dict, m: dict, v: dict, t: int, lr: float,
+              b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8) -> None:
+    """The reference's numpy Adam update (train.py:42-59), in place, float32."""
+    for name, g in grads.items():
+        mm, vv = m[name], v[name]
+        mm *= b1
+        mm += (1 - b1) * g
+        vv *= b2
+        vv += (1 - b2) * (g * g)
+        m_hat = mm / (1 - b1 ** t)
+        v_hat = vv / (1 - b2 ** t)
+        params[name] -= lr * m_hat / (np.sqrt(v_hat) + eps)

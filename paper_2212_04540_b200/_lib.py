@@ -44,6 +44,8 @@ SIGNATURES = {
     "kgq_mask_apply_f32": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
     "kgq_dequant_gemm_workspace_bytes": (_SZ, [_I64, _I32]),
     "kgq_dequant_gemm_tn_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _I32, _P]),
+    "kgq_adam_step_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, _I64, _P]),
     "kgq_layer_forward_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _I32, _P, _I32, _I32, _U64, _U64,
                                              _I64, _P, _P, _P, _P, _P, _P, _P]),
 }

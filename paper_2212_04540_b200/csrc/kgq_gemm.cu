@@ -13,14 +13,18 @@
 namespace kgq {
 
 constexpr int kGemmThreads = 256;
-constexpr int kChunkRows = 32;
+constexpr int kChunkRows = 64;
 
 static inline int dq_gemm_grid(int64_t rows) {
     int64_t chunks = (rows + kChunkRows - 1) / kChunkRows;
-    int64_t g = chunks < (int64_t)kSMs * 2 ? chunks : (int64_t)kSMs * 2;
+    int64_t g = chunks < (int64_t)kSMs ? chunks : (int64_t)kSMs;   // 1 CTA per SM (135 regs)
     return g < 1 ? 1 : (int)g;
 }
 
+// Each CTA walks a fixed set of 64-row chunks.  The next chunk's g rows
+// (float4), packed code bytes and (R, Z) are prefetched into registers while
+// the current chunk is dequantized into shared memory (bit-exact with
+// dequantize_tensor) and accumulated into 8x8 FFMA register tiles.
 template <int D, int BITS>
 __global__ void __launch_bounds__(kGemmThreads)
 dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
@@ -30,11 +34,15 @@ dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restric
     constexpr int TT = T8 * T8;             // threads per full d x d tile
     constexpr int S = kGemmThreads / TT;    // row slices
     constexpr int RB = D * BITS / 8;        // packed bytes per row
-    constexpr float Bf = (float)((1u << BITS) - 1u);
+    constexpr int GV = kChunkRows * D / 4 / kGemmThreads;   // g float4 per thread per chunk
+    constexpr int CW = (kChunkRows * RB / 4 + kGemmThreads - 1) / kGemmThreads;  // code words per thread
+    constexpr int EPT = kChunkRows * D / kGemmThreads;      // dequantized elements per thread
     constexpr uint32_t MASK = (1u << BITS) - 1u;
     extern __shared__ __align__(16) float sm[];
-    float *hs = sm;                          // [kChunkRows][D]
-    float *gs = sm + kChunkRows * D;         // [kChunkRows][D]
+    float *hs = sm;                                          // [kChunkRows][D]
+    float *gs = sm + kChunkRows * D;                         // [kChunkRows][D]
+    uint32_t *cs = reinterpret_cast<uint32_t *>(gs + kChunkRows * D);   // [kChunkRows*RB/4]
+    float *rz = reinterpret_cast<float *>(cs + kChunkRows * RB / 4);    // [2][kChunkRows]
 
     const int t = threadIdx.x;
     const int slice = t / TT, tt = t % TT;
@@ -46,30 +54,55 @@ dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restric
         for (int b = 0; b < 8; b++) acc[a][b] = 0.0f;
 
     const int64_t n_chunks = (rows + kChunkRows - 1) / kChunkRows;
-    for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    float4 pg[GV];
+    uint32_t pc[CW];
+    float pr = 0.f, pz = 0.f;
+    auto prefetch = [&](int64_t ch) {
         const int64_t r0 = ch * kChunkRows;
         const int nr = (int)imin64(kChunkRows, rows - r0);
-        // g rows -> smem (float4)
-        for (int i = t; i < kChunkRows * D / 4; i += kGemmThreads) {
-            const int rr = (i * 4) / D;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (rr < nr) v = __ldg(reinterpret_cast<const float4 *>(g + r0 * D) + i);
-            reinterpret_cast<float4 *>(gs)[i] = v;
+#pragma unroll
+        for (int m = 0; m < GV; m++) {
+            const int i = t + kGemmThreads * m, rr = (i * 4) / D;
+            pg[m] = rr < nr ? __ldg(reinterpret_cast<const float4 *>(g + r0 * D) + i)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        // dequantize H rows -> smem: (R*c)/B + Z, R == 0 -> Z (quantize.py:206-209)
-        for (int i = t; i < kChunkRows * D; i += kGemmThreads) {
-            const int rr = i / D, k = i % D;
-            float v = 0.0f;
-            if (rr < nr) {
-                const int64_t row = r0 + rr;
-                const int bit = k * BITS;
-                const uint32_t c = (__ldg(codes + row * RB + (bit >> 3)) >> (bit & 7)) & MASK;
-                const float r = __ldg(ranges + row), z = __ldg(offsets + row);
-                v = (r == 0.0f) ? z : __fadd_rn(__fdiv_rn(__fmul_rn(r, (float)c), Bf), z);
+#pragma unroll
+        for (int m = 0; m < CW; m++) {
+            const int i = t + kGemmThreads * m;
+            pc[m] = (i < kChunkRows * RB / 4 && i * 4 < nr * RB)
+                        ? __ldg(reinterpret_cast<const uint32_t *>(codes + r0 * RB) + i) : 0u;
+        }
+        if (t < kChunkRows) {
+            pr = t < nr ? __ldg(ranges + r0 + t) : 0.f;
+            pz = t < nr ? __ldg(offsets + r0 + t) : 0.f;
+        }
+    };
+    int64_t ch = blockIdx.x;
+    if (ch < n_chunks) prefetch(ch);
+    for (; ch < n_chunks; ch += gridDim.x) {
+        const int nr = (int)imin64(kChunkRows, rows - ch * kChunkRows);
+#pragma unroll
+        for (int m = 0; m < GV; m++) reinterpret_cast<float4 *>(gs)[t + kGemmThreads * m] = pg[m];
+#pragma unroll
+        for (int m = 0; m < CW; m++)
+            if (t + kGemmThreads * m < kChunkRows * RB / 4) cs[t + kGemmThreads * m] = pc[m];
+        if (t < kChunkRows) { rz[t] = pr; rz[kChunkRows + t] = pz; }
+        __syncthreads();
+        if (ch + gridDim.x < n_chunks) prefetch(ch + gridDim.x);
+        // dequantize: (R*c)/B + Z, R == 0 -> Z (quantize.py:206-209); rows past the end -> 0
+        {
+            const int rr = (t * EPT) / D, k0 = (t * EPT) % D;
+            const float r = rz[rr], z = rz[kChunkRows + rr];
+            const uint8_t *cb = reinterpret_cast<const uint8_t *>(cs) + rr * RB;
+#pragma unroll
+            for (int e = 0; e < EPT; e++) {
+                const int bit = (k0 + e) * BITS;
+                const uint32_t c = (cb[bit >> 3] >> (bit & 7)) & MASK;
+                hs[rr * D + k0 + e] = rr < nr ? lut_entry<BITS>(r, z, (int)c) : 0.0f;
             }
-            hs[i] = v;
         }
         __syncthreads();
+#pragma unroll 4
         for (int rr = slice; rr < kChunkRows; rr += S) {
             const float4 a0 = *reinterpret_cast<const float4 *>(hs + rr * D + ti * 8);
             const float4 a1 = *reinterpret_cast<const float4 *>(hs + rr * D + ti * 8 + 4);
@@ -102,11 +135,19 @@ dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restric
     for (int i = t; i < D * D; i += kGemmThreads) dst[i] = red[i];
 }
 
+// Fixed-order reduction of the per-CTA partials: 8 interleaved running sums
+// (independent loads in flight) combined in a fixed order -> deterministic.
 __global__ void reduce_partials_kernel(const float *__restrict__ partial, int nparts, int dd,
                                        float *__restrict__ out, int accumulate) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dd; i += gridDim.x * blockDim.x) {
-        float s = 0.0f;
-        for (int p = 0; p < nparts; p++) s = __fadd_rn(s, partial[(int64_t)p * dd + i]);
+        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int p = 0;
+        for (; p + 8 <= nparts; p += 8)
+#pragma unroll
+            for (int u = 0; u < 8; u++) s8[u] = __fadd_rn(s8[u], __ldg(partial + (int64_t)(p + u) * dd + i));
+        for (; p < nparts; p++) s8[p & 7] = __fadd_rn(s8[p & 7], __ldg(partial + (int64_t)p * dd + i));
+        const float s = __fadd_rn(__fadd_rn(__fadd_rn(s8[0], s8[1]), __fadd_rn(s8[2], s8[3])),
+                                  __fadd_rn(__fadd_rn(s8[4], s8[5]), __fadd_rn(s8[6], s8[7])));
         out[i] = accumulate ? __fadd_rn(out[i], s) : s;
     }
 }
@@ -138,7 +179,8 @@ template <int D>
 static int launch_dq_gemm(int bits, const uint8_t *codes, const float *ranges, const float *offsets,
                           int64_t rows, const float *g, float *partial, cudaStream_t s) {
     const int grid = dq_gemm_grid(rows);
-    size_t smem = (size_t)2 * kChunkRows * D * sizeof(float);
+    size_t smem = (size_t)2 * kChunkRows * D * sizeof(float) + (size_t)kChunkRows * D * bits / 8 +
+                  2 * kChunkRows * sizeof(float);
     if (smem < (size_t)D * D * sizeof(float)) smem = (size_t)D * D * sizeof(float);
     void (*kern)(const uint8_t *, const float *, const float *, int64_t, const float *, float *);
     switch (bits) {
@@ -193,7 +235,7 @@ extern "C" int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges
         }
         if (st != KGQ_OK) return st;
         const int dd = d * d;
-        reduce_partials_kernel<<<(dd + 255) / 256, 256, 0, s>>>(partial, dq_gemm_grid(rows), dd,
+        reduce_partials_kernel<<<(dd + 127) / 128, 128, 0, s>>>(partial, dq_gemm_grid(rows), dd,
                                                                 dtheta, accumulate);
     } else {
         dequant_gemm_generic_kernel<<<(d * d + 255) / 256, 256, 0, s>>>(

@@ -1,0 +1,89 @@
+// kgq_optim.cu -- fused Adam step (train.py:42-59) for sm_100a.
+// One pass over (param, grad, m, v) with the reference's numpy float32 op
+// order: every product, quotient, sqrt and sum is separately rounded, the
+// Python scalars enter as float32 (NEP 50 weak scalars), and m/c1, v/c2 are
+// true divisions -- bit-identical to the numpy update.
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+struct AdamScalars { float b1, omb1, b2, omb2, c1, c2, lr, eps; };
+
+__device__ __forceinline__ void adam_elem(float &p, float g, float &m, float &v, const AdamScalars &a) {
+    m = __fadd_rn(__fmul_rn(m, a.b1), __fmul_rn(a.omb1, g));
+    v = __fadd_rn(__fmul_rn(v, a.b2), __fmul_rn(a.omb2, __fmul_rn(g, g)));
+    const float mh = __fdiv_rn(m, a.c1);
+    const float vh = __fdiv_rn(v, a.c2);
+    p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mh), __fadd_rn(__fsqrt_rn(vh), a.eps)));
+}
+
+__global__ void __launch_bounds__(256)
+adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
+                float4 *__restrict__ v, int64_t n4, AdamScalars a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 pp = p[i], mm = m[i], vv = v[i];
+        const float4 gg = ldg_stream(g + i);
+        adam_elem(pp.x, gg.x, mm.x, vv.x, a);
+        adam_elem(pp.y, gg.y, mm.y, vv.y, a);
+        adam_elem(pp.z, gg.z, mm.z, vv.z, a);
+        adam_elem(pp.w, gg.w, mm.w, vv.w, a);
+        p[i] = pp;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
+__global__ void adam_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
+                            float *__restrict__ v, int64_t n, AdamScalars a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float pp = p[i], mm = m[i], vv = v[i];
+        adam_elem(pp, g[i], mm, vv, a);
+        p[i] = pp;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+extern "C" int kgq_adam_step_f32(float *param, const float *grad, float *m, float *v, int64_t n,
+                                 double lr, double beta1, double beta2, double eps, int64_t step,
+                                 void *stream) {
+    if (n < 0 || step < 1) return KGQ_ERR_INVALID_ARG;
+    if (n == 0) return KGQ_OK;
+    if (!param || !grad || !m || !v) return KGQ_ERR_INVALID_ARG;
+    AdamScalars a;
+    a.b1 = (float)beta1;
+    a.omb1 = (float)(1.0 - beta1);
+    a.b2 = (float)beta2;
+    a.omb2 = (float)(1.0 - beta2);
+    double p1 = 1.0, p2 = 1.0;            // beta ** t, as Python's float pow
+    p1 = pow(beta1, (double)step);
+    p2 = pow(beta2, (double)step);
+    a.c1 = (float)(1.0 - p1);
+    a.c2 = (float)(1.0 - p2);
+    a.lr = (float)lr;
+    a.eps = (float)eps;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool vec = (n & 3) == 0 &&
+                     ((((uintptr_t)param) | ((uintptr_t)grad) | ((uintptr_t)m) | ((uintptr_t)v)) & 15u) == 0;
+    if (vec) {
+        const int64_t n4 = n / 4;
+        int64_t blocks = (n4 + 255) / 256;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        adam_vec_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<float4 *>(param),
+                                                    reinterpret_cast<const float4 *>(grad),
+                                                    reinterpret_cast<float4 *>(m),
+                                                    reinterpret_cast<float4 *>(v), n4, a);
+    } else {
+        int64_t blocks = (n + 255) / 256;
+        if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+        adam_kernel<<<(int)blocks, 256, 0, s>>>(param, grad, m, v, n, a);
+    }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -283,25 +283,6 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
 // (computed once with IEEE division), one LDS per element.
 // bits == 8: arithmetic with the hoisted-reciprocal division.
 // ---------------------------------------------------------------------------
-// (R*c)/B + Z for one code (R == 0 -> Z), IEEE: hoisted RN(1/B) + Markstein
-// correction (t = R*c is 0 or in [2^-100, 2^108] when R is in the window).
-template <int BITS>
-__device__ __forceinline__ float lut_entry(float r, float z, int c) {
-    constexpr float Bf = (float)PackInfo<BITS>::B;
-    constexpr float yB = 1.0f / Bf;            // RN(1/B), exact constant folding
-    if (r == 0.0f) return z;
-    const float t = __fmul_rn(r, (float)c);
-    float qv;
-    if (r >= 0x1p-100f && r <= 0x1p100f) {
-        const float q0 = __fmul_rn(t, yB);
-        const float er = __fmaf_rn(-Bf, q0, t);
-        qv = __fmaf_rn(yB, er, q0);
-    } else {
-        qv = __fdiv_rn(t, Bf);
-    }
-    return __fadd_rn(qv, z);
-}
-
 // Per-group outputs of one warp tile (8 groups) from staged codes + table.
 template <int G, int BITS>
 __device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const float *lt, float r, float z,

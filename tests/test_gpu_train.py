@@ -273,3 +273,23 @@ def test_partitioned_step_gpu_world1_matches_tape():
     np.testing.assert_allclose(de0.cpu().numpy(), tg["E0"].cpu().numpy(), rtol=1e-5, atol=1e-8)
     for i, t in enumerate(dth):
         np.testing.assert_allclose(t.cpu().numpy(), tg[f"theta{i}"].cpu().numpy(), rtol=1e-5, atol=1e-8)
+
+
+def test_fused_adam_bit_identical_to_numpy_reference():
+    from paper_2212_04540_b200.train import AdamState, adam_step
+    rng = np.random.default_rng(11)
+    shapes = {"E0": (1001, 64), "theta0": (64, 64), "odd": (37, 3)}
+    p_np = {k: rng.standard_normal(s).astype(np.float32) for k, s in shapes.items()}
+    m_np = {k: np.zeros_like(v) for k, v in p_np.items()}
+    v_np = {k: np.zeros_like(v) for k, v in p_np.items()}
+    p_t = {k: torch.from_numpy(v.copy()).cuda() for k, v in p_np.items()}
+    state = AdamState(p_t)
+    for t in range(1, 6):
+        g_np = {k: (rng.standard_normal(s) * 10.0 ** rng.integers(-6, 2)).astype(np.float32)
+                for k, s in shapes.items()}
+        orc.adam_step(p_np, g_np, m_np, v_np, t, 1e-3)
+        adam_step(p_t, {k: torch.from_numpy(v).cuda() for k, v in g_np.items()}, state, 1e-3)
+        for k in shapes:
+            assert np.array_equal(p_t[k].cpu().numpy().view(np.uint32), p_np[k].view(np.uint32)), (t, k)
+            assert np.array_equal(state.m[k].cpu().numpy(), m_np[k])
+            assert np.array_equal(state.v[k].cpu().numpy(), v_np[k])
