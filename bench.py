@@ -232,7 +232,8 @@ def train_bench(args, world, rank):
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(cur)
-            st = train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.train_steps)
+            st = train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.train_steps,
+                             graphs=not args.no_graphs)
             b.record(cur)
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / st["steps"]
@@ -502,6 +503,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-compat", action="store_true")
     ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="train step without CUDA graphs")
     ap.add_argument("--train-shape", default="amazon", choices=["small", "lastfm", "amazon"])
     ap.add_argument("--train-steps", type=int, default=100)
     args = ap.parse_args()

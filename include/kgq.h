@@ -62,10 +62,13 @@ KGQ_API int kgq_last_cuda_error(void);
  * pack_codes :213-233, RandomStream :61-102).
  * bits in {1,2,4,8}; noise (n_groups*group float64) only for KGQ_ROUND_SR_NOISE.
  * group_offset: global index of group 0 (row-partitioned tensors key their
- * noise by global row, so any partitioning gives byte-identical codes).   */
+ * noise by global row, so any partitioning gives byte-identical codes).
+ * tid_base (optional device pointer): the key's tensor id is
+ * tensor_id + *tid_base, read on the device -- a captured CUDA graph advances
+ * the base between replays so every replay draws fresh noise.             */
 KGQ_API int kgq_quantize_f32(const float *x, int64_t n_groups, int32_t group, int32_t bits,
                      int32_t rounding, uint64_t seed, uint64_t tensor_id,
-                     int64_t group_offset, const double *noise, uint8_t *codes, float *ranges, float *offsets,
+                     const uint64_t *tid_base, int64_t group_offset, const double *noise, uint8_t *codes, float *ranges, float *offsets,
                      void *stream);
 
 /* dequantize_tensor(q, float32), quantize.py:199-210 (+ unpack_codes :236-247). */
@@ -132,6 +135,13 @@ KGQ_API int kgq_adam_step_f32(float *param, const float *grad, float *m, float *
                       double lr, double beta1, double beta2, double eps, int64_t step,
                       void *stream);
 
+/* Same update for CUDA-graph replay: t = *step_ptr (device int64, >= 1) and
+ * the bias corrections are read from c12[2t], c12[2t+1] (host-built float32
+ * table of 1 - beta1^t, 1 - beta2^t).  n % 4 == 0 and 16-byte alignment. */
+KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, float *v, int64_t n,
+                          double lr, double beta1, double beta2, double eps,
+                          const float *c12, const int64_t *step_ptr, void *stream);
+
 /* Fused KGNN layer forward (model.py:81-85 + tape.py:101-126), one pass:
  *   H = spmm(A, E); ctx = quantize(H) (group = d); J = H @ theta;
  *   E_next = relu(J); mask = J > 0.
@@ -141,7 +151,7 @@ KGQ_API int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices,
                           int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
                           const float *e, int32_t d, const float *theta,
                           int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
-                          int64_t row_offset, uint8_t *codes, float *ranges, float *offsets, float *e_next,
+                          const uint64_t *tid_base, int64_t row_offset, uint8_t *codes, float *ranges, float *offsets, float *e_next,
                           uint8_t *mask, float *h_out, void *stream);
 
 #ifdef __cplusplus

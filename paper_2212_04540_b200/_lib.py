@@ -33,7 +33,7 @@ SIGNATURES = {
     "kgq_version": (ctypes.c_int, []),
     "kgq_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "kgq_last_cuda_error": (ctypes.c_int, []),
-    "kgq_quantize_f32": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _U64, _U64, _I64, _P, _P, _P, _P, _P]),
+    "kgq_quantize_f32": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _U64, _U64, _P, _I64, _P, _P, _P, _P, _P]),
     "kgq_dequantize_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
     "kgq_fast_noise_u16": (ctypes.c_int, [_U64, _U64, _I64, _I64, _I32, _P, _P]),
     "kgq_compat_noise_raw53": (ctypes.c_int, [_U64, _U64, _I64, _I64, _I32, _P, _P]),
@@ -46,8 +46,10 @@ SIGNATURES = {
     "kgq_dequant_gemm_tn_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _I32, _P]),
     "kgq_adam_step_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.c_double, _I64, _P]),
+    "kgq_adam_step_dev_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_double, _P, _P, _P]),
     "kgq_layer_forward_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _I32, _P, _I32, _I32, _U64, _U64,
-                                             _I64, _P, _P, _P, _P, _P, _P, _P]),
+                                             _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -237,7 +237,8 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
                      const float *__restrict__ vals, int64_t n_rows,
                      const int32_t *__restrict__ row_order, int64_t n_heavy,
                      const float *__restrict__ e, const float *__restrict__ theta, uint64_t seed,
-                     uint64_t tid, int64_t row_offset, uint8_t *__restrict__ codes,
+                     uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t row_offset,
+                     uint8_t *__restrict__ codes,
                      float *__restrict__ ranges, float *__restrict__ offsets,
                      float *__restrict__ e_next, uint32_t *__restrict__ mask,
                      float *__restrict__ h_out) {
@@ -253,6 +254,7 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
     for (int i = threadIdx.x; i < D * D / 4; i += blockDim.x)
         reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
     __syncthreads();
+    if (tid_base) tid += __ldg(tid_base);          // graph replays advance the key on device
     const FastKey fk = make_fast_key(seed, tid);
 
     if ((int64_t)blockIdx.x < n_heavy) {
@@ -453,8 +455,12 @@ static int launch_spmm(const int32_t *indptr, const int32_t *indices, const floa
                        int64_t n_rows, const int32_t *row_order, int64_t n_heavy, const float *x,
                        float *out, cudaStream_t s) {
     const size_t smem = n_heavy ? RG<D>::ring_bytes : 0;
-    cudaError_t ea = ensure_smem(spmm_kernel<D>, smem);
-    if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        cudaError_t ea = ensure_smem(spmm_kernel<D>, smem);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set = smem;
+    }
     const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 16);
     spmm_kernel<D><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out);
     return KGQ_OK;
@@ -485,24 +491,28 @@ extern "C" int kgq_spmm_csr_f32(const int32_t *indptr, const int32_t *indices, c
 template <int D, int BITS>
 static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indices, const float *vals,
                         int64_t n_rows, const int32_t *row_order, int64_t n_heavy, const float *e,
-                        const float *theta, uint64_t seed, uint64_t tid, int64_t row_offset,
-                        uint8_t *codes, float *ranges, float *offsets, float *e_next,
-                        uint32_t *mask, float *h_out, cudaStream_t s) {
+                        const float *theta, uint64_t seed, uint64_t tid, const uint64_t *tid_base,
+                        int64_t row_offset, uint8_t *codes, float *ranges, float *offsets,
+                        float *e_next, uint32_t *mask, float *h_out, cudaStream_t s) {
     const size_t smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
     void (*kern)(const int32_t *, const int32_t *, const float *, int64_t, const int32_t *, int64_t,
-                 const float *, const float *, uint64_t, uint64_t, int64_t, uint8_t *, float *,
-                 float *, float *, uint32_t *, float *);
+                 const float *, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
+                 uint8_t *, float *, float *, float *, uint32_t *, float *);
     switch (rounding) {
         case KGQ_ROUND_NEAREST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
         case KGQ_ROUND_SR_FAST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
         case KGQ_ROUND_SR_COMPAT: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
         default: return KGQ_ERR_INVALID_ARG;
     }
-    cudaError_t ea = ensure_smem(kern, smem);
-    if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+    static size_t smem_set[3] = {0, 0, 0};   // per instance: largest attribute already set
+    if (smem > smem_set[rounding]) {
+        cudaError_t ea = ensure_smem(kern, smem);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set[rounding] = smem;
+    }
     const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 8);
     kern<<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed,
-                                 tid, row_offset, codes, ranges, offsets, e_next, mask, h_out);
+                                 tid, tid_base, row_offset, codes, ranges, offsets, e_next, mask, h_out);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
@@ -511,12 +521,13 @@ template <int D>
 static int launch_layer_bits(int bits, int rounding, const int32_t *indptr, const int32_t *indices,
                              const float *vals, int64_t n_rows, const int32_t *row_order,
                              int64_t n_heavy, const float *e, const float *theta, uint64_t seed,
-                             uint64_t tid, int64_t row_offset, uint8_t *codes, float *ranges,
+                             uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
+                             uint8_t *codes, float *ranges,
                              float *offsets, float *e_next, uint32_t *mask, float *h_out,
                              cudaStream_t s) {
 #define KGQ_LAYER(B) launch_layer<D, B>(rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, \
-                                        theta, seed, tid, row_offset, codes, ranges, offsets, e_next, \
-                                        mask, h_out, s)
+                                        theta, seed, tid, tid_base, row_offset, codes, ranges, offsets, \
+                                        e_next, mask, h_out, s)
     switch (bits) {
         case 1: return KGQ_LAYER(1);
         case 2: return KGQ_LAYER(2);
@@ -531,7 +542,8 @@ extern "C" int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indic
                                      int64_t n_rows, const int32_t *row_order, int64_t n_heavy,
                                      const float *e, int32_t d, const float *theta, int32_t bits,
                                      int32_t rounding, uint64_t seed, uint64_t tensor_id,
-                                     int64_t row_offset, uint8_t *codes, float *ranges,
+                                     const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
+                                     float *ranges,
                                      float *offsets, float *e_next, uint8_t *mask, float *h_out,
                                      void *stream) {
     if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
@@ -547,9 +559,9 @@ extern "C" int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indic
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *m32 = reinterpret_cast<uint32_t *>(mask);
     switch (d) {
-        case 32: return launch_layer_bits<32>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
-        case 64: return launch_layer_bits<64>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
-        case 128: return launch_layer_bits<128>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 32: return launch_layer_bits<32>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, tid_base, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 64: return launch_layer_bits<64>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, tid_base, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
+        case 128: return launch_layer_bits<128>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, tid_base, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
     }
     return KGQ_ERR_INVALID_ARG;
 }

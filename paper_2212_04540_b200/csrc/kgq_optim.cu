@@ -34,6 +34,30 @@ adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__
     }
 }
 
+// Graph-capturable variant: the step t is read on the device (*step_ptr) and
+// the bias corrections come from a host-built table c12[2t], c12[2t+1] =
+// float32(1 - beta^t) (Python's float pow, exactly as the reference).
+__global__ void __launch_bounds__(256)
+adam_vec_dev_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
+                    float4 *__restrict__ v, int64_t n4, AdamScalars a, const float *__restrict__ c12,
+                    const int64_t *__restrict__ step_ptr) {
+    const int64_t t = __ldg(step_ptr);
+    a.c1 = __ldg(c12 + 2 * t);
+    a.c2 = __ldg(c12 + 2 * t + 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 pp = p[i], mm = m[i], vv = v[i];
+        const float4 gg = ldg_stream(g + i);
+        adam_elem(pp.x, gg.x, mm.x, vv.x, a);
+        adam_elem(pp.y, gg.y, mm.y, vv.y, a);
+        adam_elem(pp.z, gg.z, mm.z, vv.z, a);
+        adam_elem(pp.w, gg.w, mm.w, vv.w, a);
+        p[i] = pp;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
 __global__ void adam_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
                             float *__restrict__ v, int64_t n, AdamScalars a) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -84,6 +108,32 @@ extern "C" int kgq_adam_step_f32(float *param, const float *grad, float *m, floa
         if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
         adam_kernel<<<(int)blocks, 256, 0, s>>>(param, grad, m, v, n, a);
     }
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, float *v, int64_t n,
+                                     double lr, double beta1, double beta2, double eps,
+                                     const float *c12, const int64_t *step_ptr, void *stream) {
+    if (n < 0 || !c12 || !step_ptr) return KGQ_ERR_INVALID_ARG;
+    if (n == 0) return KGQ_OK;
+    if (!param || !grad || !m || !v) return KGQ_ERR_INVALID_ARG;
+    if ((n & 3) || ((((uintptr_t)param) | ((uintptr_t)grad) | ((uintptr_t)m) | ((uintptr_t)v)) & 15u))
+        return KGQ_ERR_MISALIGNED;
+    AdamScalars a;
+    a.b1 = (float)beta1;
+    a.omb1 = (float)(1.0 - beta1);
+    a.b2 = (float)beta2;
+    a.omb2 = (float)(1.0 - beta2);
+    a.c1 = a.c2 = 1.0f;
+    a.lr = (float)lr;
+    a.eps = (float)eps;
+    const int64_t n4 = n / 4;
+    int64_t blocks = (n4 + 255) / 256;
+    if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
+    adam_vec_dev_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4 *>(param), reinterpret_cast<const float4 *>(grad),
+        reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, a, c12, step_ptr);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

@@ -87,7 +87,8 @@ template <int G, int T, int BITS, int MODE>
 __global__ void __launch_bounds__(kThreads)
 quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__restrict__ codes,
                      float *__restrict__ ranges, float *__restrict__ offsets, uint64_t seed,
-                     uint64_t tid, int64_t group_offset) {
+                     uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t group_offset) {
+    if (tid_base) tid += __ldg(tid_base);          // graph replays advance the key on device
     using GE = Geo<G, T>;
     constexpr int NF = GE::NF, Q = GE::Q, GPW = GE::GPW, S = GE::S;
     constexpr int GB = G * BITS / 8;              // packed bytes per group
@@ -221,7 +222,8 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
 quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, int bits, int mode,
-                        uint64_t seed, uint64_t tid, int64_t group_offset,
+                        uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
+                        int64_t group_offset,
                         const double *__restrict__ noise, uint8_t *__restrict__ codes,
                         float *__restrict__ ranges, float *__restrict__ offsets) {
     const int lane = threadIdx.x & 31;
@@ -229,6 +231,7 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
     const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int GB = (G * bits + 7) / 8;
     const float Bf = (float)((1u << bits) - 1u);
+    if (tid_base) tid += __ldg(tid_base);
     const FastKey fk = make_fast_key(seed, tid);
     for (int64_t g = warp_id; g < n_groups; g += n_warps) {
         const float *row = x + g * (int64_t)G;
@@ -492,8 +495,8 @@ template <int G> struct PickT { static constexpr int T = 4; };
 
 template <int G, int BITS, int MODE>
 static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, float *ranges,
-                            float *offsets, uint64_t seed, uint64_t tid, int64_t goff,
-                            cudaStream_t s) {
+                            float *offsets, uint64_t seed, uint64_t tid, const uint64_t *tid_base,
+                            int64_t goff, cudaStream_t s) {
     constexpr int T = PickT<G>::T;
     using GE = Geo<G, T>;
     const int64_t tiles = (n_groups + GE::GPW - 1) / GE::GPW;
@@ -510,22 +513,22 @@ static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, fl
         }
     }
     quantize_fast_kernel<G, T, BITS, MODE><<<grid, kThreads, smem, s>>>(x, n_groups, codes, ranges,
-                                                                       offsets, seed, tid, goff);
+                                                                       offsets, seed, tid, tid_base, goff);
 }
 
 template <int G, int BITS>
 static bool dispatch_quant_mode(int mode, const float *x, int64_t n_groups, uint8_t *codes,
                                 float *ranges, float *offsets, uint64_t seed, uint64_t tid,
-                                int64_t goff, cudaStream_t s) {
+                                const uint64_t *tb, int64_t goff, cudaStream_t s) {
     switch (mode) {
         case KGQ_ROUND_NEAREST:
-            launch_quant_t4<G, BITS, KGQ_ROUND_NEAREST>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            launch_quant_t4<G, BITS, KGQ_ROUND_NEAREST>(x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
             return true;
         case KGQ_ROUND_SR_FAST:
-            launch_quant_t4<G, BITS, KGQ_ROUND_SR_FAST>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            launch_quant_t4<G, BITS, KGQ_ROUND_SR_FAST>(x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
             return true;
         case KGQ_ROUND_SR_COMPAT:
-            launch_quant_t4<G, BITS, KGQ_ROUND_SR_COMPAT>(x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+            launch_quant_t4<G, BITS, KGQ_ROUND_SR_COMPAT>(x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
             return true;
         default:
             return false;
@@ -535,12 +538,12 @@ static bool dispatch_quant_mode(int mode, const float *x, int64_t n_groups, uint
 template <int G>
 static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_groups,
                                 uint8_t *codes, float *ranges, float *offsets, uint64_t seed,
-                                uint64_t tid, int64_t goff, cudaStream_t s) {
+                                uint64_t tid, const uint64_t *tb, int64_t goff, cudaStream_t s) {
     switch (bits) {
-        case 1: return dispatch_quant_mode<G, 1>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
-        case 2: return dispatch_quant_mode<G, 2>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
-        case 4: return dispatch_quant_mode<G, 4>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
-        case 8: return dispatch_quant_mode<G, 8>(mode, x, n_groups, codes, ranges, offsets, seed, tid, goff, s);
+        case 1: return dispatch_quant_mode<G, 1>(mode, x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
+        case 2: return dispatch_quant_mode<G, 2>(mode, x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
+        case 4: return dispatch_quant_mode<G, 4>(mode, x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
+        case 8: return dispatch_quant_mode<G, 8>(mode, x, n_groups, codes, ranges, offsets, seed, tid, tb, goff, s);
     }
     return false;
 }
@@ -568,7 +571,8 @@ static inline bool bits_ok(int bits) { return bits == 1 || bits == 2 || bits == 
 
 extern "C" int kgq_quantize_f32(const float *x, int64_t n_groups, int32_t group, int32_t bits,
                                 int32_t rounding, uint64_t seed, uint64_t tensor_id,
-                                int64_t group_offset, const double *noise, uint8_t *codes,
+                                const uint64_t *tid_base, int64_t group_offset,
+                                const double *noise, uint8_t *codes,
                                 float *ranges, float *offsets, void *stream) {
     if (!bits_ok(bits)) return KGQ_ERR_UNSUPPORTED_BITS;
     if (group < 1 || n_groups < 0 || rounding < 0 || rounding > 3 || group_offset < 0)
@@ -582,17 +586,17 @@ extern "C" int kgq_quantize_f32(const float *x, int64_t n_groups, int32_t group,
     bool done = false;
     if (fast_ok) {
         switch (group) {
-            case 32: done = dispatch_quant_bits<32>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
-            case 64: done = dispatch_quant_bits<64>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
-            case 128: done = dispatch_quant_bits<128>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
-            case 256: done = dispatch_quant_bits<256>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, group_offset, s); break;
+            case 32: done = dispatch_quant_bits<32>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, tid_base, group_offset, s); break;
+            case 64: done = dispatch_quant_bits<64>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, tid_base, group_offset, s); break;
+            case 128: done = dispatch_quant_bits<128>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, tid_base, group_offset, s); break;
+            case 256: done = dispatch_quant_bits<256>(bits, rounding, x, n_groups, codes, ranges, offsets, seed, tensor_id, tid_base, group_offset, s); break;
         }
     }
     if (!done) {
         const int grid = grid_for(n_groups, kWarps, 8);
         quantize_generic_kernel<<<grid, kThreads, 0, s>>>(x, n_groups, group, bits, rounding, seed,
-                                                          tensor_id, group_offset, noise, codes,
-                                                          ranges, offsets);
+                                                          tensor_id, tid_base, group_offset, noise,
+                                                          codes, ranges, offsets);
     }
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;

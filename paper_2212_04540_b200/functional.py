@@ -57,7 +57,8 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     st = _lib.load().kgq_layer_forward_f32(
         adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows,
         *adj.schedule(), e.data_ptr(), d,
-        theta.data_ptr(), cfg.bits, cfg.mode, seed, int(tensor_id) & 0xFFFFFFFFFFFFFFFF, row_offset,
+        theta.data_ptr(), cfg.bits, cfg.mode, seed, int(tensor_id) & 0xFFFFFFFFFFFFFFFF,
+        stream.tid_base_ptr() if stream is not None else None, row_offset,
         codes.data_ptr(), ranges.data_ptr(), offsets.data_ptr(), e_next.data_ptr(), mask.data_ptr(),
         _lib.ptr(h), _lib.stream_ptr(dev))
     _lib.check(st, "kgq_layer_forward_f32")

@@ -87,11 +87,22 @@ class RandomStream:
     def __init__(self, seed: int):
         self.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
         self._next_tensor_id = 0
+        self._device_base = None    # uint64 device counter while capturing CUDA graphs
 
     def next_tensor_id(self) -> int:
         tid = self._next_tensor_id
         self._next_tensor_id += 1
         return tid
+
+    def tid_base_ptr(self):
+        """Device pointer the kernels add to tensor ids (None = host ids only)."""
+        return None if self._device_base is None else self._device_base.data_ptr()
+
+    def bind_device_base(self, base: "torch.Tensor | None") -> None:
+        """Key subsequent draws by (host id + *base): a captured CUDA graph
+        increments ``base`` between replays so each replay gets fresh tensor
+        ids -- the same ids the eager path would have used."""
+        self._device_base = base
 
     def matrix_uniforms(self, tensor_id: int, rows: int, cols: int, dtype=torch.float64,
                         rng: str = RNG_COMPAT, device=None) -> torch.Tensor:
@@ -201,7 +212,8 @@ def quantize_tensor(x: torch.Tensor, cfg: QuantConfig, stream: RandomStream | No
     codes = torch.empty((n_groups, packed_group_bytes(group, cfg.bits)), dtype=torch.uint8, device=dev)
     ranges = torch.empty(n_groups, dtype=torch.float32, device=dev)
     offsets = torch.empty(n_groups, dtype=torch.float32, device=dev)
-    st = _lib.load().kgq_quantize_f32(x.data_ptr(), n_groups, group, cfg.bits, mode, seed, tid,
+    tb = stream.tid_base_ptr() if (stream is not None and mode != _lib.ROUND_SR_NOISE) else None
+    st = _lib.load().kgq_quantize_f32(x.data_ptr(), n_groups, group, cfg.bits, mode, seed, tid, tb,
                                       int(group_offset), _lib.ptr(noise), codes.data_ptr(),
                                       ranges.data_ptr(), offsets.data_ptr(), _lib.stream_ptr(dev))
     _lib.check(st, "kgq_quantize_f32")

@@ -205,8 +205,9 @@ def test_autograd_kgnn_equals_tape():
                                        rtol=1e-5, atol=1e-8)
 
 
+@pytest.mark.parametrize("graphs", [False, True], ids=["eager", "cudagraph"])
 @pytest.mark.parametrize("bits", [32, 2])
-def test_training_c1_matches_reference_run(bits):
+def test_training_c1_matches_reference_run(bits, graphs):
     """BASELINE configs[0] (small KG, 2 layers, d=64): same dataset, batches,
     noise and init as the reference's train_run; loss curve and Recall@20."""
     kgq = _kgq()
@@ -218,7 +219,8 @@ def test_training_c1_matches_reference_run(bits):
                      z["val"], z["test"], z["triples"], int(z["num_relations"]))
     epochs = int(z["run_epochs"])
     q = kgq.QuantConfig(bits=bits)
-    _, rep = train_run(ds, ModelConfig(layers=2, dim=64, quant=q), TrainConfig(epochs=epochs, seed=0, quant=q))
+    _, rep = train_run(ds, ModelConfig(layers=2, dim=64, quant=q), TrainConfig(epochs=epochs, seed=0, quant=q),
+                       graphs=graphs)
     pre = f"run_b{bits}_"
     np.testing.assert_allclose(rep["loss_curve"], z[pre + "loss_curve"], rtol=2e-3)
     assert abs(rep["metrics"]["recall_at_20"] - float(z[pre + "recall"])) < 0.01
@@ -293,3 +295,32 @@ def test_fused_adam_bit_identical_to_numpy_reference():
             assert np.array_equal(p_t[k].cpu().numpy().view(np.uint32), p_np[k].view(np.uint32)), (t, k)
             assert np.array_equal(state.m[k].cpu().numpy(), m_np[k])
             assert np.array_equal(state.v[k].cpu().numpy(), v_np[k])
+
+
+def test_cuda_graph_epoch_equals_eager_epoch():
+    """Graph replays draw the same tensor ids and Adam bias corrections as the
+    eager loop: identical dataset/batches give the same trajectory (up to the
+    atomic scatter order of the gather backward)."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig, init_params
+    from paper_2212_04540_b200.train import AdamState, TrainConfig, train_epoch
+    ds = D.synth_kg(D.SynthShape(600, 400, 1500, relations=5, interactions_per_user=20.0), seed=3)
+    adj = D.build_adjacency(ds)
+    q = kgq.QuantConfig(bits=2)
+    mcfg = ModelConfig(layers=3, dim=64, quant=q)
+    cfg = TrainConfig(batch_size=256, quant=q)
+    outs = []
+    for graphs in (False, True):
+        params = init_params(ds.num_nodes, mcfg, 0)
+        state = AdamState(params.as_dict())
+        st = kgq.RandomStream(0)
+        rng = np.random.default_rng(0)
+        stats = [train_epoch(ds, adj, params, mcfg, cfg, state, st, rng, graphs=graphs) for _ in range(2)]
+        outs.append((stats, params, st._next_tensor_id, state.step))
+    (s0, p0, t0, k0), (s1, p1, t1, k1) = outs
+    assert t0 == t1 and k0 == k1 and s0[0]["steps"] == s1[0]["steps"]
+    np.testing.assert_allclose(s0[1]["losses"], s1[1]["losses"], rtol=1e-4)
+    assert s0[0]["peak_context_bytes"] == s1[0]["peak_context_bytes"]
+    np.testing.assert_allclose(p0.entity_embeddings.cpu().numpy(), p1.entity_embeddings.cpu().numpy(),
+                               rtol=1e-3, atol=1e-5)

@@ -25,7 +25,7 @@ st = kgq.RandomStream(0)
 train_epoch(ds, adj, params, mcfg, cfg, state, st, rng, max_steps=5)
 torch.cuda.synchronize()
 t = time.time()
-s = train_epoch(ds, adj, params, mcfg, cfg, state, st, rng, max_steps=steps)
+s = train_epoch(ds, adj, params, mcfg, cfg, state, st, rng, max_steps=steps, graphs=len(sys.argv) > 4)
 torch.cuda.synchronize()
 dt = time.time() - t
 print(json.dumps({"ms_per_step": 1e3 * dt / s["steps"], "steps": s["steps"], "loss": s["mean_loss"],
