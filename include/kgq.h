@@ -142,6 +142,13 @@ KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, flo
                           double lr, double beta1, double beta2, double eps,
                           const float *c12, const int64_t *step_ptr, void *stream);
 
+/* out[rows][d] = a[rows][d] . theta (transpose_theta = 0) or . theta^T (1) on
+ * the tcgen05 tensor cores (kind::tf32, 3xTF32 split: fp32-level accuracy),
+ * accumulator in TMEM.  d in {32, 64}; other d -> KGQ_ERR_INVALID_ARG (the
+ * host falls back to cuBLAS).  The d x d layer GEMM of tape.py:223. */
+KGQ_API int kgq_rowmm_f32(const float *a, int64_t rows, int32_t d, const float *theta,
+                  int32_t transpose_theta, float *out, void *stream);
+
 /* Fused KGNN layer forward (model.py:81-85 + tape.py:101-126), one pass:
  *   H = spmm(A, E); ctx = quantize(H) (group = d); J = H @ theta;
  *   E_next = relu(J); mask = J > 0.

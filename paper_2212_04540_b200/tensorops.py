@@ -128,6 +128,23 @@ def mm(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return a @ b
 
 
+def mm_theta(a: torch.Tensor, theta: torch.Tensor, transpose: bool = False) -> torch.Tensor:
+    """a @ theta (or a @ theta.T) for the d x d layer weights: tcgen05 tensor
+    cores (3xTF32, kgq_rowmm_f32) for d in (32, 64), cuBLAS otherwise."""
+    _require_2d("a", a)
+    d = theta.shape[0]
+    if a.shape[1] != d or theta.shape[1] != d:
+        raise ShapeMismatchError(f"mm: a is {tuple(a.shape)}, theta is {tuple(theta.shape)}")
+    if d not in (32, 64) or a.dtype != torch.float32 or not a.is_cuda:
+        return a @ (theta.t() if transpose else theta)
+    a = a.contiguous()
+    out = torch.empty_like(a)
+    st = _lib.load().kgq_rowmm_f32(a.data_ptr(), a.shape[0], d, theta.contiguous().data_ptr(),
+                                   1 if transpose else 0, out.data_ptr(), _lib.stream_ptr(a.device))
+    _lib.check(st, "kgq_rowmm_f32")
+    return out
+
+
 def spmm_into(s: CSR, d: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     st = _lib.load().kgq_spmm_csr_f32(s.indptr.data_ptr(), s.indices.data_ptr(), s.data.data_ptr(),
                                       s.shape[0], *s.schedule(), d.data_ptr(), d.shape[1],
