@@ -21,7 +21,7 @@ import torch
 from . import functional as F
 from .quantize import (QuantConfig, RandomStream, dequantize_tensor, fp32_equivalent_bytes,
                        quantize_tensor, stored_bytes)
-from .tensorops import CSR, mask_apply, relu, spmm, spmm_t
+from .tensorops import CSR, mask_apply, mm_theta, relu, spmm, spmm_t
 
 
 class ContextLedger:
@@ -99,7 +99,7 @@ class QuantLinearFn(torch.autograd.Function):
         (theta,) = ctx.saved_tensors
         g = g.contiguous()
         dtheta = F.dequant_gemm_tn(ctx.q, g)
-        dh = g @ theta.t()
+        dh = mm_theta(g, theta, transpose=True)
         ctx.q = None
         _ledger_free(ctx.ledger, *ctx.bytes)
         return dh, dtheta, None, None, None, None
@@ -143,7 +143,7 @@ class QuantGraphConvFn(torch.autograd.Function):
         (theta,) = ctx.saved_tensors
         gj = mask_apply(g.contiguous(), ctx.mask)
         dtheta = F.dequant_gemm_tn(ctx.q, gj)
-        dh = gj @ theta.t()
+        dh = mm_theta(gj, theta, transpose=True)
         de = spmm_t(ctx.adj, dh)
         _ledger_free(ctx.ledger, *ctx.bytes)
         ctx.q = ctx.mask = None

@@ -23,7 +23,7 @@
 //    the 8 elements of fast-noise call 4p+q (one Philox call per lane in the
 //    fused quantizer).  The next column ids are prefetched while the current
 //    neighbour rows are gathered.
-#include "kgq_common.cuh"
+#include "kgq_tc.cuh"
 
 namespace kgq {
 
@@ -225,6 +225,155 @@ spmm_generic_kernel(const int32_t *__restrict__ indptr, const int32_t *__restric
     }
 }
 
+// Quantize one light row held by its LPR-lane group (group = the row; the
+// same arithmetic and noise as kgq_quantize_f32) and store codes, R, Z.
+template <int D, int BITS, int MODE>
+__device__ __forceinline__ void light_row_quantize(const float4 (&h)[2], bool active, int64_t row,
+                                                   int gl, const FastKey &fk, uint64_t seed,
+                                                   uint64_t tid, int64_t row_offset,
+                                                   uint8_t *__restrict__ codes,
+                                                   float *__restrict__ ranges,
+                                                   float *__restrict__ offsets) {
+    constexpr int LPR = RG<D>::LPR;
+    constexpr float Bf = (float)((1u << BITS) - 1u);
+    constexpr int RB = D * BITS / 8;
+    const int p = gl >> 2, q = gl & 3;
+    const int f0 = 8 * p + q;
+        // ---- quantize H (group = this row) ----
+    float mn = fminf(fminf(fminf(h[0].x, h[0].y), fminf(h[0].z, h[0].w)),
+                     fminf(fminf(h[1].x, h[1].y), fminf(h[1].z, h[1].w)));
+    float mx = fmaxf(fmaxf(fmaxf(h[0].x, h[0].y), fmaxf(h[0].z, h[0].w)),
+                     fmaxf(fmaxf(h[1].x, h[1].y), fmaxf(h[1].z, h[1].w)));
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const float z = mn, r = __fsub_rn(mx, mn);
+    const DivR dv = make_div(r);
+    const uint64_t gglob = (uint64_t)(row_offset + row);
+    uint32_t piece[2] = {0u, 0u};
+    if (r > 0.0f) {
+        uint4 rnd = make_uint4(0, 0, 0, 0);
+        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * p + q));
+        const bool unguarded = group_div_unguarded(dv, z);
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            u64x4 r64 = {0, 0, 0, 0};
+            if (MODE == KGQ_ROUND_SR_COMPAT)
+                r64 = philox4x64_10(gglob * (uint64_t)(D / 4) + (uint64_t)(f0 + 4 * hh) + 1ull,
+                                    0, 0, 0, seed, tid);
+            const float xs[4] = {h[hh].x, h[hh].y, h[hh].z, h[hh].w};
+            const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+            const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
+            uint32_t acc = 0;
+#pragma unroll
+            for (int el = 0; el < 4; el++) {
+                const float a = __fsub_rn(xs[el], z);
+                const float qv = unguarded ? div_a_unguarded(dv, a) : div_a(dv, a);
+                const float s = __fmul_rn(qv, Bf);
+                const float uf = hh ? __uint2float_rn(rw[el] >> 16) : __uint2float_rn(rw[el] & 0xFFFFu);
+                acc += code_bits<MODE>(s, uf, cw[el] >> 11) << (BITS * el);
+            }
+            piece[hh] = acc - magic_sum4<BITS>();
+        }
+    }
+    // pieces: 4*BITS bits at element offsets 4*f0 and 4*(f0+4) of the row
+    {
+        uint8_t *rc = codes + row * RB;
+        if (BITS == 1) {   // nibbles: pair lanes q, q^1 into bytes
+            const uint32_t o0 = __shfl_xor_sync(0xffffffffu, piece[0], 1);
+            const uint32_t o1 = __shfl_xor_sync(0xffffffffu, piece[1], 1);
+            if (active && (q & 1) == 0) {
+                rc[(4 * f0) / 8] = (uint8_t)(piece[0] | (o0 << 4));
+                rc[(4 * (f0 + 4)) / 8] = (uint8_t)(piece[1] | (o1 << 4));
+            }
+        } else if (active) {
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const int off = (4 * (f0 + 4 * hh)) * BITS / 8;
+                if (BITS == 2) rc[off] = (uint8_t)piece[hh];
+                else if (BITS == 4) *reinterpret_cast<uint16_t *>(rc + off) = (uint16_t)piece[hh];
+                else *reinterpret_cast<uint32_t *>(rc + off) = piece[hh];
+            }
+        }
+    }
+    if (active && gl == 0) {
+        ranges[row] = r;
+        offsets[row] = z;
+    }
+}
+
+// Heavy row (one CTA): bit-exact SpMM streamed through the smem ring, then
+// quantize / J = H.theta (FFMA, theta in smem) / relu / mask for that row.
+template <int D, int BITS, int MODE>
+__device__ __forceinline__ void heavy_layer_row(const int32_t *__restrict__ indptr,
+                                                const int32_t *__restrict__ indices,
+                                                const float *__restrict__ vals,
+                                                const float *__restrict__ e, int64_t row,
+                                                const float *th, float *ring, float (*red)[8],
+                                                float *hrow, const FastKey &fk, uint64_t seed,
+                                                uint64_t tid, int64_t row_offset,
+                                                uint8_t *__restrict__ codes,
+                                                float *__restrict__ ranges,
+                                                float *__restrict__ offsets,
+                                                float *__restrict__ e_next,
+                                                uint32_t *__restrict__ mask,
+                                                float *__restrict__ h_out) {
+    constexpr float Bf = (float)((1u << BITS) - 1u);
+    constexpr int RB = D * BITS / 8;
+    constexpr int LPW = 32 / BITS;
+        // ------------------------- heavy row: CTA -------------------------
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const float h = heavy_spmm_row<D>(indptr, indices, vals, e, row, ring);
+    const bool own = t < D;                     // warps 0 .. D/32-1 hold the row
+    if (own && h_out) h_out[row * D + t] = h;
+    float mn = own ? h : INFINITY, mx = own ? h : -INFINITY;
+    mn = warp_min(mn, 32);
+    mx = warp_max(mx, 32);
+    if (lane == 0) { red[0][wid] = mn; red[1][wid] = mx; }
+    if (own) hrow[t] = h;
+    __syncthreads();
+    mn = red[0][0];
+    mx = red[1][0];
+#pragma unroll
+    for (int w = 1; w < D / 32; w++) { mn = fminf(mn, red[0][w]); mx = fmaxf(mx, red[1][w]); }
+    const float z = mn, r = __fsub_rn(mx, mn);
+    const uint64_t gglob = (uint64_t)(row_offset + row);
+    if (own) {
+        uint32_t code = 0;
+        if (r > 0.0f) {
+            const DivR dv = make_div(r);
+            const float s = __fmul_rn(div_a(dv, __fsub_rn(h, z)), Bf);
+            float uf = 0.0f;
+            uint64_t raw53 = 0;
+            if (MODE == KGQ_ROUND_SR_FAST) uf = __uint2float_rn(fast_u16(fk, gglob, t));
+            if (MODE == KGQ_ROUND_SR_COMPAT) raw53 = compat_raw53(seed, tid, gglob, D, t);
+            code = code_bits<MODE>(s, uf, raw53) - kMagicBits;
+        }
+        // feature t = 32*wid + lane: word (t*BITS)/32 collects LPW lanes
+        const uint32_t mine = code << ((lane % LPW) * BITS);
+        const int wib = lane / LPW;
+#pragma unroll
+        for (int w = 0; w < 32 / LPW; w++) {
+            const uint32_t word = __reduce_or_sync(0xffffffffu, wib == w ? mine : 0u);
+            if (lane == w)
+                reinterpret_cast<uint32_t *>(codes + row * RB)[wid * (32 / LPW) + w] = word;
+        }
+        if (t == 0) {
+            ranges[row] = r;
+            offsets[row] = z;
+        }
+        float j = 0.0f;
+#pragma unroll 8
+        for (int k = 0; k < D; k++) j = __fmaf_rn(hrow[k], th[k * D + t], j);
+        const bool pos = j > 0.0f;
+        const uint32_t bal = __ballot_sync(0xffffffffu, pos);
+        e_next[row * D + t] = pos ? j : 0.0f;
+        if (lane == 0) mask[row * (D / 32) + wid] = bal;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Fused layer forward: H = A_hat.E (bit-exact), quantize H on chip (group =
 // d; the same arithmetic and noise as kgq_quantize_f32), J = H.theta (theta
@@ -258,56 +407,9 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
     const FastKey fk = make_fast_key(seed, tid);
 
     if ((int64_t)blockIdx.x < n_heavy) {
-        // ------------------------- heavy row: CTA -------------------------
-        const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-        const int64_t row = __ldg(row_order + blockIdx.x);
-        const float h = heavy_spmm_row<D>(indptr, indices, vals, e, row, ring);
-        const bool own = t < D;                     // warps 0 .. D/32-1 hold the row
-        if (own && h_out) h_out[row * D + t] = h;
-        float mn = own ? h : INFINITY, mx = own ? h : -INFINITY;
-        mn = warp_min(mn, 32);
-        mx = warp_max(mx, 32);
-        if (lane == 0) { red[0][wid] = mn; red[1][wid] = mx; }
-        if (own) hrow[t] = h;
-        __syncthreads();
-        mn = red[0][0];
-        mx = red[1][0];
-#pragma unroll
-        for (int w = 1; w < D / 32; w++) { mn = fminf(mn, red[0][w]); mx = fmaxf(mx, red[1][w]); }
-        const float z = mn, r = __fsub_rn(mx, mn);
-        const uint64_t gglob = (uint64_t)(row_offset + row);
-        if (own) {
-            uint32_t code = 0;
-            if (r > 0.0f) {
-                const DivR dv = make_div(r);
-                const float s = __fmul_rn(div_a(dv, __fsub_rn(h, z)), Bf);
-                float uf = 0.0f;
-                uint64_t raw53 = 0;
-                if (MODE == KGQ_ROUND_SR_FAST) uf = __uint2float_rn(fast_u16(fk, gglob, t));
-                if (MODE == KGQ_ROUND_SR_COMPAT) raw53 = compat_raw53(seed, tid, gglob, D, t);
-                code = code_bits<MODE>(s, uf, raw53) - kMagicBits;
-            }
-            // feature t = 32*wid + lane: word (t*BITS)/32 collects LPW lanes
-            const uint32_t mine = code << ((lane % LPW) * BITS);
-            const int wib = lane / LPW;
-#pragma unroll
-            for (int w = 0; w < 32 / LPW; w++) {
-                const uint32_t word = __reduce_or_sync(0xffffffffu, wib == w ? mine : 0u);
-                if (lane == w)
-                    reinterpret_cast<uint32_t *>(codes + row * RB)[wid * (32 / LPW) + w] = word;
-            }
-            if (t == 0) {
-                ranges[row] = r;
-                offsets[row] = z;
-            }
-            float j = 0.0f;
-#pragma unroll 8
-            for (int k = 0; k < D; k++) j = __fmaf_rn(hrow[k], th[k * D + t], j);
-            const bool pos = j > 0.0f;
-            const uint32_t bal = __ballot_sync(0xffffffffu, pos);
-            e_next[row * D + t] = pos ? j : 0.0f;
-            if (lane == 0) mask[row * (D / 32) + wid] = bal;
-        }
+        heavy_layer_row<D, BITS, MODE>(indptr, indices, vals, e, __ldg(row_order + blockIdx.x), th,
+                                       ring, red, hrow, fk, seed, tid, row_offset, codes, ranges,
+                                       offsets, e_next, mask, h_out);
         return;
     }
 
@@ -333,69 +435,8 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
             o[f0] = h[0];
             o[f0 + 4] = h[1];
         }
-        // ---- quantize H (group = this row) ----
-        float mn = fminf(fminf(fminf(h[0].x, h[0].y), fminf(h[0].z, h[0].w)),
-                         fminf(fminf(h[1].x, h[1].y), fminf(h[1].z, h[1].w)));
-        float mx = fmaxf(fmaxf(fmaxf(h[0].x, h[0].y), fmaxf(h[0].z, h[0].w)),
-                         fmaxf(fmaxf(h[1].x, h[1].y), fmaxf(h[1].z, h[1].w)));
-#pragma unroll
-        for (int o = 1; o < LPR; o <<= 1) {
-            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        const float z = mn, r = __fsub_rn(mx, mn);
-        const DivR dv = make_div(r);
-        const uint64_t gglob = (uint64_t)(row_offset + row);
-        uint32_t piece[2] = {0u, 0u};
-        if (r > 0.0f) {
-            uint4 rnd = make_uint4(0, 0, 0, 0);
-            if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * p + q));
-            const bool unguarded = group_div_unguarded(dv, z);
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                u64x4 r64 = {0, 0, 0, 0};
-                if (MODE == KGQ_ROUND_SR_COMPAT)
-                    r64 = philox4x64_10(gglob * (uint64_t)(D / 4) + (uint64_t)(f0 + 4 * hh) + 1ull,
-                                        0, 0, 0, seed, tid);
-                const float xs[4] = {h[hh].x, h[hh].y, h[hh].z, h[hh].w};
-                const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
-                const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
-                uint32_t acc = 0;
-#pragma unroll
-                for (int el = 0; el < 4; el++) {
-                    const float a = __fsub_rn(xs[el], z);
-                    const float qv = unguarded ? div_a_unguarded(dv, a) : div_a(dv, a);
-                    const float s = __fmul_rn(qv, Bf);
-                    const float uf = hh ? __uint2float_rn(rw[el] >> 16) : __uint2float_rn(rw[el] & 0xFFFFu);
-                    acc += code_bits<MODE>(s, uf, cw[el] >> 11) << (BITS * el);
-                }
-                piece[hh] = acc - magic_sum4<BITS>();
-            }
-        }
-        // pieces: 4*BITS bits at element offsets 4*f0 and 4*(f0+4) of the row
-        {
-            uint8_t *rc = codes + row * RB;
-            if (BITS == 1) {   // nibbles: pair lanes q, q^1 into bytes
-                const uint32_t o0 = __shfl_xor_sync(0xffffffffu, piece[0], 1);
-                const uint32_t o1 = __shfl_xor_sync(0xffffffffu, piece[1], 1);
-                if (active && (q & 1) == 0) {
-                    rc[(4 * f0) / 8] = (uint8_t)(piece[0] | (o0 << 4));
-                    rc[(4 * (f0 + 4)) / 8] = (uint8_t)(piece[1] | (o1 << 4));
-                }
-            } else if (active) {
-#pragma unroll
-                for (int hh = 0; hh < 2; hh++) {
-                    const int off = (4 * (f0 + 4 * hh)) * BITS / 8;
-                    if (BITS == 2) rc[off] = (uint8_t)piece[hh];
-                    else if (BITS == 4) *reinterpret_cast<uint16_t *>(rc + off) = (uint16_t)piece[hh];
-                    else *reinterpret_cast<uint32_t *>(rc + off) = piece[hh];
-                }
-            }
-        }
-        if (active && gl == 0) {
-            ranges[row] = r;
-            offsets[row] = z;
-        }
+        light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
+                                          ranges, offsets);
         // ---- J = H . theta (ascending k, FFMA) ----
         float4 j0 = make_float4(0.f, 0.f, 0.f, 0.f), j1 = j0;
 #pragma unroll 4
@@ -429,6 +470,138 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
             if (q == 0) mask[row * (D / 32) + p] = w;
         }
     }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused layer forward with J = H.theta on the 5th-gen tensor cores (d = 32/64).
+// Light CTAs work on tiles of 128 consecutive (degree-sorted) rows: each
+// row group gathers + quantizes its row exactly as above and stages H (split
+// hi/lo for 3xTF32) into the shared-memory A tile; one thread then issues
+// 3*d/8 tcgen05.mma (M=128, N=d, K=d) into a TMEM accumulator and commits to
+// an mbarrier; all warps drain TMEM (tcgen05.ld), apply relu, and write E'
+// and the mask words.  Heavy rows keep the CTA-per-row FFMA path.
+// ---------------------------------------------------------------------------
+template <int D, int BITS, int MODE>
+__global__ void __launch_bounds__(256)
+layer_forward_tc_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+                        const float *__restrict__ vals, int64_t n_rows,
+                        const int32_t *__restrict__ row_order, int64_t n_heavy,
+                        const float *__restrict__ e, const float *__restrict__ theta, uint64_t seed,
+                        uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t row_offset,
+                        uint8_t *__restrict__ codes, float *__restrict__ ranges,
+                        float *__restrict__ offsets, float *__restrict__ e_next,
+                        uint32_t *__restrict__ mask, float *__restrict__ h_out) {
+    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
+    constexpr int M = 128;
+    constexpr int SPW = M / 8;                      // row slots per warp per tile
+    constexpr int ITERS = SPW / RPW;
+    extern __shared__ __align__(128) float dyn[];
+    __shared__ float red[2][8];
+    __shared__ float hrow[D];
+    __shared__ int64_t rowid[M];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    if (tid_base) tid += __ldg(tid_base);
+    const FastKey fk = make_fast_key(seed, tid);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+
+    if ((int64_t)blockIdx.x < n_heavy) {
+        float *th = dyn;
+        float *ring = dyn + D * D;
+        for (int i = t; i < D * D / 4; i += blockDim.x)
+            reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
+        __syncthreads();
+        heavy_layer_row<D, BITS, MODE>(indptr, indices, vals, e, __ldg(row_order + blockIdx.x), th,
+                                       ring, red, hrow, fk, seed, tid, row_offset, codes, ranges,
+                                       offsets, e_next, mask, h_out);
+        return;
+    }
+
+    float *ah = dyn, *al = dyn + M * D;             // A tile [M x D] hi / lo
+    float *bh = dyn + 2 * M * D, *bl = bh + D * D;  // B(n, k) = theta[k][n], hi / lo
+    for (int i = t; i < D * D; i += 256) {
+        const int n = i / D, k = i % D;
+        float hi, lo;
+        tc::split_tf32(__ldg(theta + k * D + n), hi, lo);
+        bh[tc::tile_off(n, k, D) / 4] = hi;
+        bl[tc::tile_off(n, k, D) / 4] = lo;
+    }
+    if (t == 0) tc::mbar_init(&mbar, 1);
+    if (warp == 0) tc::tmem_alloc(&tmem_base, D < 32 ? 32 : D);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    const int gl = lane % LPR, grp = lane / LPR;
+    const int f0 = 8 * (gl >> 2) + (gl & 3);
+    const int64_t lb = (int64_t)blockIdx.x - n_heavy;
+    const int64_t nlb = (int64_t)gridDim.x - n_heavy;
+    const int64_t n_light = n_rows - n_heavy;
+    uint32_t phase = 0;
+    for (int64_t tbase = lb * M; tbase < n_light; tbase += nlb * M) {
+#pragma unroll 1
+        for (int it = 0; it < ITERS; it++) {
+            const int sl = warp * SPW + it * RPW + grp;          // slot within the tile
+            const int64_t slot = tbase + sl;
+            const bool active = slot < n_light;
+            const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
+            float4 h[2];
+            rg_spmm_row<D>(indptr, indices, vals, e, row, active, gl, h);
+            if (active && h_out) {
+                float4 *o = reinterpret_cast<float4 *>(h_out + row * D);
+                o[f0] = h[0];
+                o[f0 + 4] = h[1];
+            }
+            light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
+                                              ranges, offsets);
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const float xs[4] = {h[hh].x, h[hh].y, h[hh].z, h[hh].w};
+                float hi[4], lo[4];
+#pragma unroll
+                for (int el = 0; el < 4; el++) {
+                    tc::split_tf32(active ? xs[el] : 0.0f, hi[el], lo[el]);
+                }
+                const uint32_t off = tc::tile_off(sl, 4 * (f0 + 4 * hh), M) / 4;
+                *reinterpret_cast<float4 *>(ah + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<float4 *>(al + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
+            if (gl == 0) rowid[sl] = active ? row : -1;
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
+            tc::fence_after();
+            tc::mma_3xtf32<M, D, D>(tmem, ah, al, bh, bl);
+            tc::commit(&mbar);
+        }
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        if (D >= 64 || warp < 4) {
+            const int qd = warp & 3, half = warp >> 2;
+            const int cb = (D >= 64) ? half * 32 : 0;
+            float v[32];
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)cb, v);
+            const int64_t row = rowid[32 * qd + lane];
+            if (row >= 0) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int j = 0; j < 32; j++) w |= (v[j] > 0.0f ? 1u : 0u) << j;
+                float4 *dst = reinterpret_cast<float4 *>(e_next + row * D + cb);
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    dst[j] = make_float4(v[4 * j] > 0.f ? v[4 * j] : 0.f, v[4 * j + 1] > 0.f ? v[4 * j + 1] : 0.f,
+                                         v[4 * j + 2] > 0.f ? v[4 * j + 2] : 0.f, v[4 * j + 3] > 0.f ? v[4 * j + 3] : 0.f);
+                mask[row * (D / 32) + cb / 32] = w;
+            }
+        }
+        tc::fence_before();
+        __syncthreads();
+    }
+    if (warp == 0) tc::tmem_free(tmem, D < 32 ? 32 : D);
 }
 
 }  // namespace kgq
@@ -494,14 +667,23 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
                         const float *theta, uint64_t seed, uint64_t tid, const uint64_t *tid_base,
                         int64_t row_offset, uint8_t *codes, float *ranges, float *offsets,
                         float *e_next, uint32_t *mask, float *h_out, cudaStream_t s) {
-    const size_t smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
+    constexpr bool TC = (D <= 64);   // tcgen05 J for d = 32/64; FFMA J for d = 128
+    const size_t heavy_smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
+    const size_t tc_smem = (size_t)(2 * 128 * D + 2 * D * D) * sizeof(float);
+    const size_t smem = TC ? (tc_smem > heavy_smem ? tc_smem : heavy_smem) : heavy_smem;
     void (*kern)(const int32_t *, const int32_t *, const float *, int64_t, const int32_t *, int64_t,
                  const float *, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
                  uint8_t *, float *, float *, float *, uint32_t *, float *);
     switch (rounding) {
-        case KGQ_ROUND_NEAREST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
-        case KGQ_ROUND_SR_FAST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
-        case KGQ_ROUND_SR_COMPAT: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
+        case KGQ_ROUND_NEAREST:
+            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_NEAREST> : layer_forward_kernel<D, BITS, KGQ_ROUND_NEAREST>;
+            break;
+        case KGQ_ROUND_SR_FAST:
+            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_SR_FAST> : layer_forward_kernel<D, BITS, KGQ_ROUND_SR_FAST>;
+            break;
+        case KGQ_ROUND_SR_COMPAT:
+            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_SR_COMPAT> : layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>;
+            break;
         default: return KGQ_ERR_INVALID_ARG;
     }
     static size_t smem_set[3] = {0, 0, 0};   // per instance: largest attribute already set
@@ -510,7 +692,15 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set[rounding] = smem;
     }
-    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 8);
+    const int64_t n_light = n_rows - n_heavy;
+    int light;
+    if (TC) {
+        int64_t tiles = (n_light + 127) / 128;
+        light = (int)(tiles < (int64_t)kSMs * 2 ? (tiles < 1 ? 1 : tiles) : (int64_t)kSMs * 2);
+    } else {
+        light = light_blocks(n_light, RG<D>::RPW, 8);
+    }
+    const int grid = (int)n_heavy + light;
     kern<<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed,
                                  tid, tid_base, row_offset, codes, ranges, offsets, e_next, mask, h_out);
     KGQ_LAUNCH_CHECK();

@@ -76,6 +76,10 @@ class OracleOps:
         return torch.from_numpy(orc.spmm_csr(ip, ix, vv, x.numpy()))
 
     @staticmethod
+    def mm_t(g, theta):
+        return g @ theta.t()
+
+    @staticmethod
     def scatter_rows(rows, idx, g):
         out = np.zeros((rows, g.shape[1]), dtype=np.float32)
         np.add.at(out, idx.numpy().astype(np.int64), g.numpy())
