@@ -23,7 +23,7 @@
 //    the 8 elements of fast-noise call 4p+q (one Philox call per lane in the
 //    fused quantizer).  The next column ids are prefetched while the current
 //    neighbour rows are gathered.
-#include "kgq_tc.cuh"
+#include "kgq_common.cuh"
 
 namespace kgq {
 
@@ -392,14 +392,12 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
                      float *__restrict__ e_next, uint32_t *__restrict__ mask,
                      float *__restrict__ h_out) {
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
-    constexpr float Bf = (float)((1u << BITS) - 1u);
-    constexpr int RB = D * BITS / 8;                // packed bytes per row
-    constexpr int LPW = 32 / BITS;                  // codes per 32-bit word
     extern __shared__ __align__(16) float dyn[];
     float *th = dyn;                                // [D][D]
     float *ring = dyn + D * D;                      // heavy-path staging
     __shared__ float red[2][8];
     __shared__ float hrow[D];
+    __shared__ __align__(16) float hst[8 * 256];   // per-warp k-major H staging (D * RPW = 256)
     for (int i = threadIdx.x; i < D * D / 4; i += blockDim.x)
         reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
     __syncthreads();
@@ -438,171 +436,65 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
         light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
                                           ranges, offsets);
         // ---- J = H . theta (ascending k, FFMA) ----
-        float4 j0 = make_float4(0.f, 0.f, 0.f, 0.f), j1 = j0;
-#pragma unroll 4
-        for (int k = 0; k < D; k++) {
-            const int src = 4 * (k >> 5) + ((k >> 2) & 3);      // lane owning H[k]
-            const int hh = (k >> 4) & 1, el = k & 3;
-            const float mine = hh ? (el == 0 ? h[1].x : el == 1 ? h[1].y : el == 2 ? h[1].z : h[1].w)
-                                  : (el == 0 ? h[0].x : el == 1 ? h[0].y : el == 2 ? h[0].z : h[0].w);
-            const float hk = __shfl_sync(0xffffffffu, mine, src, LPR);
-            const float4 ta = reinterpret_cast<const float4 *>(th + k * D)[f0];
-            const float4 tb = reinterpret_cast<const float4 *>(th + k * D)[f0 + 4];
-            j0.x = __fmaf_rn(hk, ta.x, j0.x); j0.y = __fmaf_rn(hk, ta.y, j0.y);
-            j0.z = __fmaf_rn(hk, ta.z, j0.z); j0.w = __fmaf_rn(hk, ta.w, j0.w);
-            j1.x = __fmaf_rn(hk, tb.x, j1.x); j1.y = __fmaf_rn(hk, tb.y, j1.y);
-            j1.z = __fmaf_rn(hk, tb.z, j1.z); j1.w = __fmaf_rn(hk, tb.w, j1.w);
-        }
-        // ---- relu + mask (word p of the row: nibble 4q and 16+4q) ----
-        uint32_t w = (j0.x > 0.f ? 1u : 0u) | (j0.y > 0.f ? 2u : 0u) | (j0.z > 0.f ? 4u : 0u) |
-                     (j0.w > 0.f ? 8u : 0u);
-        w <<= 4 * q;
-        w |= ((j1.x > 0.f ? 1u : 0u) | (j1.y > 0.f ? 2u : 0u) | (j1.z > 0.f ? 4u : 0u) |
-              (j1.w > 0.f ? 8u : 0u)) << (16 + 4 * q);
-        w |= __shfl_xor_sync(0xffffffffu, w, 1);
-        w |= __shfl_xor_sync(0xffffffffu, w, 2);
-        if (active) {
-            float4 *o = reinterpret_cast<float4 *>(e_next + row * D);
-            o[f0] = make_float4(j0.x > 0.f ? j0.x : 0.f, j0.y > 0.f ? j0.y : 0.f,
-                                j0.z > 0.f ? j0.z : 0.f, j0.w > 0.f ? j0.w : 0.f);
-            o[f0 + 4] = make_float4(j1.x > 0.f ? j1.x : 0.f, j1.y > 0.f ? j1.y : 0.f,
-                                    j1.z > 0.f ? j1.z : 0.f, j1.w > 0.f ? j1.w : 0.f);
-            if (q == 0) mask[row * (D / 32) + p] = w;
-        }
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// Fused layer forward with J = H.theta on the 5th-gen tensor cores (d = 32/64).
-// Light CTAs work on tiles of 128 consecutive (degree-sorted) rows: each
-// row group gathers + quantizes its row exactly as above and stages H (split
-// hi/lo for 3xTF32) into the shared-memory A tile; one thread then issues
-// 3*d/8 tcgen05.mma (M=128, N=d, K=d) into a TMEM accumulator and commits to
-// an mbarrier; all warps drain TMEM (tcgen05.ld), apply relu, and write E'
-// and the mask words.  Heavy rows keep the CTA-per-row FFMA path.
-// ---------------------------------------------------------------------------
-template <int D, int BITS, int MODE>
-__global__ void __launch_bounds__(256)
-layer_forward_tc_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-                        const float *__restrict__ vals, int64_t n_rows,
-                        const int32_t *__restrict__ row_order, int64_t n_heavy,
-                        const float *__restrict__ e, const float *__restrict__ theta, uint64_t seed,
-                        uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t row_offset,
-                        uint8_t *__restrict__ codes, float *__restrict__ ranges,
-                        float *__restrict__ offsets, float *__restrict__ e_next,
-                        uint32_t *__restrict__ mask, float *__restrict__ h_out) {
-    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
-    constexpr int M = 128;
-    constexpr int SPW = M / 8;                      // row slots per warp per tile
-    constexpr int ITERS = SPW / RPW;
-    extern __shared__ __align__(128) float dyn[];
-    __shared__ float red[2][8];
-    __shared__ float hrow[D];
-    __shared__ int64_t rowid[M];
-    __shared__ __align__(8) uint64_t mbar;
-    __shared__ uint32_t tmem_base;
-    if (tid_base) tid += __ldg(tid_base);
-    const FastKey fk = make_fast_key(seed, tid);
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-
-    if ((int64_t)blockIdx.x < n_heavy) {
-        float *th = dyn;
-        float *ring = dyn + D * D;
-        for (int i = t; i < D * D / 4; i += blockDim.x)
-            reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
-        __syncthreads();
-        heavy_layer_row<D, BITS, MODE>(indptr, indices, vals, e, __ldg(row_order + blockIdx.x), th,
-                                       ring, red, hrow, fk, seed, tid, row_offset, codes, ranges,
-                                       offsets, e_next, mask, h_out);
-        return;
-    }
-
-    float *ah = dyn, *al = dyn + M * D;             // A tile [M x D] hi / lo
-    float *bh = dyn + 2 * M * D, *bl = bh + D * D;  // B(n, k) = theta[k][n], hi / lo
-    for (int i = t; i < D * D; i += 256) {
-        const int n = i / D, k = i % D;
-        float hi, lo;
-        tc::split_tf32(__ldg(theta + k * D + n), hi, lo);
-        bh[tc::tile_off(n, k, D) / 4] = hi;
-        bl[tc::tile_off(n, k, D) / 4] = lo;
-    }
-    if (t == 0) tc::mbar_init(&mbar, 1);
-    if (warp == 0) tc::tmem_alloc(&tmem_base, D < 32 ? 32 : D);
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tmem = tmem_base;
-
-    const int gl = lane % LPR, grp = lane / LPR;
-    const int f0 = 8 * (gl >> 2) + (gl & 3);
-    const int64_t lb = (int64_t)blockIdx.x - n_heavy;
-    const int64_t nlb = (int64_t)gridDim.x - n_heavy;
-    const int64_t n_light = n_rows - n_heavy;
-    uint32_t phase = 0;
-    for (int64_t tbase = lb * M; tbase < n_light; tbase += nlb * M) {
-#pragma unroll 1
-        for (int it = 0; it < ITERS; it++) {
-            const int sl = warp * SPW + it * RPW + grp;          // slot within the tile
-            const int64_t slot = tbase + sl;
-            const bool active = slot < n_light;
-            const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
-            float4 h[2];
-            rg_spmm_row<D>(indptr, indices, vals, e, row, active, gl, h);
-            if (active && h_out) {
-                float4 *o = reinterpret_cast<float4 *>(h_out + row * D);
-                o[f0] = h[0];
-                o[f0 + 4] = h[1];
-            }
-            light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
-                                              ranges, offsets);
+        // The warp's RPW rows are staged k-major in smem (hs[k][RPW]); lane l
+        // then computes columns l + 32c of all RPW rows: per k one broadcast
+        // LDS of H[.][k], D/32 conflict-free LDS of theta[k][.], 8 FFMA.
+        {
+            float *hs = hst + (threadIdx.x >> 5) * (D * RPW);
 #pragma unroll
             for (int hh = 0; hh < 2; hh++) {
-                const float xs[4] = {h[hh].x, h[hh].y, h[hh].z, h[hh].w};
-                float hi[4], lo[4];
+                const int k0 = 4 * (f0 + 4 * hh);
+                hs[(k0 + 0) * RPW + grp] = hh ? h[1].x : h[0].x;
+                hs[(k0 + 1) * RPW + grp] = hh ? h[1].y : h[0].y;
+                hs[(k0 + 2) * RPW + grp] = hh ? h[1].z : h[0].z;
+                hs[(k0 + 3) * RPW + grp] = hh ? h[1].w : h[0].w;
+            }
+            __syncwarp();
+            constexpr int NCB = D / 32;
+            float jacc[RPW][NCB];
 #pragma unroll
-                for (int el = 0; el < 4; el++) {
-                    tc::split_tf32(active ? xs[el] : 0.0f, hi[el], lo[el]);
+            for (int rr = 0; rr < RPW; rr++)
+#pragma unroll
+                for (int c = 0; c < NCB; c++) jacc[rr][c] = 0.0f;
+#pragma unroll 8
+            for (int k = 0; k < D; k++) {
+                float hk[RPW];
+                if (RPW == 4) {
+                    const float4 v4 = *reinterpret_cast<const float4 *>(hs + k * RPW);
+                    hk[0] = v4.x; hk[1] = v4.y; hk[2] = v4.z; hk[3] = v4.w;
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < RPW; rr++) hk[rr] = hs[k * RPW + rr];
                 }
-                const uint32_t off = tc::tile_off(sl, 4 * (f0 + 4 * hh), M) / 4;
-                *reinterpret_cast<float4 *>(ah + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<float4 *>(al + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-            }
-            if (gl == 0) rowid[sl] = active ? row : -1;
-        }
-        tc::fence_proxy_async();
-        __syncthreads();
-        if (t == 0) {
-            tc::fence_after();
-            tc::mma_3xtf32<M, D, D>(tmem, ah, al, bh, bl);
-            tc::commit(&mbar);
-        }
-        tc::mbar_wait(&mbar, phase);
-        phase ^= 1u;
-        tc::fence_after();
-        if (D >= 64 || warp < 4) {
-            const int qd = warp & 3, half = warp >> 2;
-            const int cb = (D >= 64) ? half * 32 : 0;
-            float v[32];
-            tc::tmem_ld32(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)cb, v);
-            const int64_t row = rowid[32 * qd + lane];
-            if (row >= 0) {
-                uint32_t w = 0;
 #pragma unroll
-                for (int j = 0; j < 32; j++) w |= (v[j] > 0.0f ? 1u : 0u) << j;
-                float4 *dst = reinterpret_cast<float4 *>(e_next + row * D + cb);
+                for (int c = 0; c < NCB; c++) {
+                    const float tk = th[k * D + lane + 32 * c];
 #pragma unroll
-                for (int j = 0; j < 8; j++)
-                    dst[j] = make_float4(v[4 * j] > 0.f ? v[4 * j] : 0.f, v[4 * j + 1] > 0.f ? v[4 * j + 1] : 0.f,
-                                         v[4 * j + 2] > 0.f ? v[4 * j + 2] : 0.f, v[4 * j + 3] > 0.f ? v[4 * j + 3] : 0.f);
-                mask[row * (D / 32) + cb / 32] = w;
+                    for (int rr = 0; rr < RPW; rr++) jacc[rr][c] = __fmaf_rn(hk[rr], tk, jacc[rr][c]);
+                }
             }
+            // ---- relu + mask: ballot over lanes gives mask word c of row rr ----
+            const int64_t base_slot = base;
+#pragma unroll
+            for (int rr = 0; rr < RPW; rr++) {
+                const int64_t sl = base_slot + rr;
+                const bool act = sl < n_light;
+                const int64_t rrow = act ? (row_order ? (int64_t)__ldg(row_order + n_heavy + sl) : sl) : 0;
+#pragma unroll
+                for (int c = 0; c < NCB; c++) {
+                    const float jv = jacc[rr][c];
+                    const uint32_t bal = __ballot_sync(0xffffffffu, jv > 0.0f);
+                    if (act) {
+                        e_next[rrow * D + lane + 32 * c] = jv > 0.0f ? jv : 0.0f;
+                        if (lane == 0) mask[rrow * (D / 32) + c] = bal;
+                    }
+                }
+            }
+            __syncwarp();
         }
-        tc::fence_before();
-        __syncthreads();
     }
-    if (warp == 0) tc::tmem_free(tmem, D < 32 ? 32 : D);
 }
+
 
 }  // namespace kgq
 
@@ -667,23 +559,14 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
                         const float *theta, uint64_t seed, uint64_t tid, const uint64_t *tid_base,
                         int64_t row_offset, uint8_t *codes, float *ranges, float *offsets,
                         float *e_next, uint32_t *mask, float *h_out, cudaStream_t s) {
-    constexpr bool TC = (D <= 64);   // tcgen05 J for d = 32/64; FFMA J for d = 128
-    const size_t heavy_smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
-    const size_t tc_smem = (size_t)(2 * 128 * D + 2 * D * D) * sizeof(float);
-    const size_t smem = TC ? (tc_smem > heavy_smem ? tc_smem : heavy_smem) : heavy_smem;
+    const size_t smem = (size_t)D * D * sizeof(float) + (n_heavy ? RG<D>::ring_bytes : 0);
     void (*kern)(const int32_t *, const int32_t *, const float *, int64_t, const int32_t *, int64_t,
                  const float *, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
                  uint8_t *, float *, float *, float *, uint32_t *, float *);
     switch (rounding) {
-        case KGQ_ROUND_NEAREST:
-            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_NEAREST> : layer_forward_kernel<D, BITS, KGQ_ROUND_NEAREST>;
-            break;
-        case KGQ_ROUND_SR_FAST:
-            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_SR_FAST> : layer_forward_kernel<D, BITS, KGQ_ROUND_SR_FAST>;
-            break;
-        case KGQ_ROUND_SR_COMPAT:
-            kern = TC ? layer_forward_tc_kernel<D, BITS, KGQ_ROUND_SR_COMPAT> : layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>;
-            break;
+        case KGQ_ROUND_NEAREST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
+        case KGQ_ROUND_SR_FAST: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
+        case KGQ_ROUND_SR_COMPAT: kern = layer_forward_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
         default: return KGQ_ERR_INVALID_ARG;
     }
     static size_t smem_set[3] = {0, 0, 0};   // per instance: largest attribute already set
@@ -692,15 +575,7 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set[rounding] = smem;
     }
-    const int64_t n_light = n_rows - n_heavy;
-    int light;
-    if (TC) {
-        int64_t tiles = (n_light + 127) / 128;
-        light = (int)(tiles < (int64_t)kSMs * 2 ? (tiles < 1 ? 1 : tiles) : (int64_t)kSMs * 2);
-    } else {
-        light = light_blocks(n_light, RG<D>::RPW, 8);
-    }
-    const int grid = (int)n_heavy + light;
+    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 8);
     kern<<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed,
                                  tid, tid_base, row_offset, codes, ranges, offsets, e_next, mask, h_out);
     KGQ_LAUNCH_CHECK();
