@@ -149,6 +149,18 @@ KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, flo
 KGQ_API int kgq_rowmm_f32(const float *a, int64_t rows, int32_t d, const float *theta,
                   int32_t transpose_theta, float *out, void *stream);
 
+/* Fused KGNN layer backward (tape.py:217-225), d in {32, 64}:
+ *   g_j = (g_read + g_e) * mask;  dh = g_j . theta^T;  dtheta (+)= Hhat^T . g_j
+ * with Hhat = dequantize(codes, ranges, offsets) never materialized.  g_read
+ * or g_e may be NULL (not both).  workspace: kgq_layer_backward_workspace_bytes.
+ * Other d -> KGQ_ERR_INVALID_ARG (the host falls back to the unfused ops). */
+KGQ_API size_t kgq_layer_backward_workspace_bytes(int64_t rows, int32_t d);
+KGQ_API int kgq_layer_backward_f32(const float *g_read, const float *g_e, const uint8_t *mask,
+                           const uint8_t *codes, const float *ranges, const float *offsets,
+                           int64_t rows, int32_t d, int32_t bits, const float *theta, float *dh,
+                           float *dtheta, void *workspace, size_t workspace_bytes,
+                           int32_t accumulate, void *stream);
+
 /* Fused KGNN layer forward (model.py:81-85 + tape.py:101-126), one pass:
  *   H = spmm(A, E); ctx = quantize(H) (group = d); J = H @ theta;
  *   E_next = relu(J); mask = J > 0.

@@ -141,9 +141,7 @@ class QuantGraphConvFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         (theta,) = ctx.saved_tensors
-        gj = mask_apply(g.contiguous(), ctx.mask)
-        dtheta = F.dequant_gemm_tn(ctx.q, gj)
-        dh = mm_theta(gj, theta, transpose=True)
+        dtheta, dh = F.layer_backward(g.contiguous(), None, ctx.mask, ctx.q, theta)
         de = spmm_t(ctx.adj, dh)
         _ledger_free(ctx.ledger, *ctx.bytes)
         ctx.q = ctx.mask = None

@@ -1,0 +1,203 @@
+// kgq_backward.cu -- fused per-layer backward of the KGNN layer (tape.py:217-225,
+// SURVEY.md 8(f) rank 1), d in {32, 64}:
+//
+//   g_j   = (g_read + g_e) * mask                      (relu backward, tape.py:224-225)
+//   dH    = g_j . theta^T                              (mm backward, tape.py:223)
+//   dtheta += Hhat^T . g_j, Hhat = dequant(ctx)        (mm backward, tape.py:220-222)
+//
+// in one pass over the rows: g_j and the dequantized Hhat exist only in
+// registers / shared memory.  Each CTA walks 32-row chunks (8 warps x 4 rows);
+// lane l owns columns l + 32c.  dH uses theta^T staged in smem (broadcast
+// LDS of g_j, conflict-free LDS of theta^T, FFMA); dtheta is accumulated in a
+// 4x4 register tile per thread over the CTA's rows and reduced across CTAs
+// in a fixed order (deterministic).  dH then feeds the SpMM (A_hat^T = A_hat).
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+constexpr int kBwdRows = 32;   // rows per chunk (8 warps x 4)
+
+static inline int bwd_grid(int64_t rows) {
+    int64_t chunks = (rows + kBwdRows - 1) / kBwdRows;
+    int64_t g = chunks < (int64_t)kSMs * 2 ? chunks : (int64_t)kSMs * 2;
+    return g < 1 ? 1 : (int)g;
+}
+
+template <int D, int BITS>
+__global__ void __launch_bounds__(256)
+layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
+                      const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
+                      const float *__restrict__ ranges, const float *__restrict__ offsets,
+                      int64_t rows, const float *__restrict__ theta, float *__restrict__ dh,
+                      float *__restrict__ partial) {
+    constexpr int NC = D / 32;                     // columns per lane
+    constexpr int RB = D * BITS / 8;
+    constexpr uint32_t CM = (1u << BITS) - 1u;
+    constexpr int TPD = D / 4;                     // 4x4 dtheta tiles per dimension
+    __shared__ __align__(16) float tht[D * D];     // theta^T: tht[k][j] = theta[j][k]
+    __shared__ __align__(16) float gs[kBwdRows][D];
+    __shared__ __align__(16) float hs[kBwdRows][D];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int i = t; i < D * D; i += 256) {
+        const int j = i / D, k = i % D;
+        tht[k * D + j] = __ldg(theta + i);         // theta[j][k]
+    }
+    // dtheta tile of this thread (only the first TPD*TPD threads own one)
+    const bool owner = t < TPD * TPD;
+    const int ti = (t / TPD) * 4, tj = (t % TPD) * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
+    __syncthreads();
+
+    const int64_t n_chunks = (rows + kBwdRows - 1) / kBwdRows;
+    for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+        // ---- per warp: 4 rows -> g_j and Hhat in smem ----
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++) {
+            const int lr = warp * 4 + rr;
+            const int64_t row = ch * kBwdRows + lr;
+            const bool ok = row < rows;
+            float r = 0.f, z = 0.f;
+            if (ok) { r = __ldg(ranges + row); z = __ldg(offsets + row); }
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const int col = lane + 32 * c;
+                float gj = 0.0f, hv = 0.0f;
+                if (ok) {
+                    // g = g_read + g_e in the reference's routing order (tape.py:204-209)
+                    float g;
+                    if (g_read && g_e) g = __fadd_rn(__ldg(g_read + row * D + col), __ldg(g_e + row * D + col));
+                    else if (g_read) g = __ldg(g_read + row * D + col);
+                    else g = __ldg(g_e + row * D + col);
+                    const uint32_t bit = (__ldg(mask + row * (D / 32) + c) >> lane) & 1u;
+                    gj = __fmul_rn(g, bit ? 1.0f : 0.0f);
+                    const int b = col * BITS;
+                    const uint32_t code = (__ldg(codes + row * RB + (b >> 3)) >> (b & 7)) & CM;
+                    hv = lut_entry<BITS>(r, z, (int)code);
+                }
+                gs[lr][col] = gj;
+                hs[lr][col] = hv;
+            }
+        }
+        __syncwarp();
+        // ---- dH for the warp's 4 rows: dh[r][j] = sum_k g_j[r][k] theta[j][k] ----
+        {
+            float o[4][NC];
+#pragma unroll
+            for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+                for (int c = 0; c < NC; c++) o[rr][c] = 0.0f;
+#pragma unroll 8
+            for (int k = 0; k < D; k++) {
+                float gk[4];
+#pragma unroll
+                for (int rr = 0; rr < 4; rr++) gk[rr] = gs[warp * 4 + rr][k];
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const float tk = tht[k * D + lane + 32 * c];
+#pragma unroll
+                    for (int rr = 0; rr < 4; rr++) o[rr][c] = __fmaf_rn(gk[rr], tk, o[rr][c]);
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 4; rr++) {
+                const int64_t row = ch * kBwdRows + warp * 4 + rr;
+                if (row < rows) {
+#pragma unroll
+                    for (int c = 0; c < NC; c++) dh[row * D + lane + 32 * c] = o[rr][c];
+                }
+            }
+        }
+        __syncthreads();
+        // ---- dtheta += Hhat^T g_j over the chunk's 32 rows (rows past the end are 0) ----
+        if (owner) {
+#pragma unroll 4
+            for (int rr = 0; rr < kBwdRows; rr++) {
+                const float4 a4 = *reinterpret_cast<const float4 *>(&hs[rr][ti]);
+                const float4 b4 = *reinterpret_cast<const float4 *>(&gs[rr][tj]);
+                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int a = 0; a < 4; a++)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) acc[a][b] = __fmaf_rn(av[a], bv[b], acc[a][b]);
+            }
+        }
+        __syncthreads();
+    }
+    if (owner) {
+        float *dst = partial + (int64_t)blockIdx.x * D * D;
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+            *reinterpret_cast<float4 *>(dst + (ti + a) * D + tj) =
+                make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+    }
+}
+
+__global__ void reduce_partials_bwd_kernel(const float *__restrict__ partial, int nparts, int dd,
+                                           float *__restrict__ out, int accumulate) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dd; i += gridDim.x * blockDim.x) {
+        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int p = 0;
+        for (; p + 8 <= nparts; p += 8)
+#pragma unroll
+            for (int u = 0; u < 8; u++) s8[u] = __fadd_rn(s8[u], __ldg(partial + (int64_t)(p + u) * dd + i));
+        for (; p < nparts; p++) s8[p & 7] = __fadd_rn(s8[p & 7], __ldg(partial + (int64_t)p * dd + i));
+        const float s = __fadd_rn(__fadd_rn(__fadd_rn(s8[0], s8[1]), __fadd_rn(s8[2], s8[3])),
+                                  __fadd_rn(__fadd_rn(s8[4], s8[5]), __fadd_rn(s8[6], s8[7])));
+        out[i] = accumulate ? __fadd_rn(out[i], s) : s;
+    }
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+extern "C" size_t kgq_layer_backward_workspace_bytes(int64_t rows, int32_t d) {
+    if (d != 32 && d != 64) return 0;
+    return (size_t)bwd_grid(rows) * d * d * sizeof(float);
+}
+
+extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, const uint8_t *mask,
+                                      const uint8_t *codes, const float *ranges,
+                                      const float *offsets, int64_t rows, int32_t d, int32_t bits,
+                                      const float *theta, float *dh, float *dtheta,
+                                      void *workspace, size_t workspace_bytes, int32_t accumulate,
+                                      void *stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (d != 32 && d != 64) return KGQ_ERR_INVALID_ARG;     // caller falls back (unfused)
+    if (rows < 0) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (rows == 0) {
+        if (!accumulate) {
+            cudaError_t e = cudaMemsetAsync(dtheta, 0, (size_t)d * d * sizeof(float), s);
+            if (e != cudaSuccess) return kgq_set_cuda_error(e);
+        }
+        return KGQ_OK;
+    }
+    if ((!g_read && !g_e) || !mask || !codes || !ranges || !offsets || !theta || !dh || !dtheta)
+        return KGQ_ERR_INVALID_ARG;
+    if (((uintptr_t)mask) & 3u) return KGQ_ERR_MISALIGNED;
+    if (!workspace || workspace_bytes < kgq_layer_backward_workspace_bytes(rows, d))
+        return KGQ_ERR_INVALID_ARG;
+    const int grid = bwd_grid(rows);
+    float *partial = reinterpret_cast<float *>(workspace);
+    const uint32_t *m32 = reinterpret_cast<const uint32_t *>(mask);
+#define KGQ_BWD(D, B) layer_backward_kernel<D, B><<<grid, 256, 0, s>>>(g_read, g_e, m32, codes, ranges, \
+                                                                       offsets, rows, theta, dh, partial)
+    if (d == 64) {
+        switch (bits) { case 1: KGQ_BWD(64, 1); break; case 2: KGQ_BWD(64, 2); break;
+                        case 4: KGQ_BWD(64, 4); break; default: KGQ_BWD(64, 8); break; }
+    } else {
+        switch (bits) { case 1: KGQ_BWD(32, 1); break; case 2: KGQ_BWD(32, 2); break;
+                        case 4: KGQ_BWD(32, 4); break; default: KGQ_BWD(32, 8); break; }
+    }
+#undef KGQ_BWD
+    const int dd = d * d;
+    reduce_partials_bwd_kernel<<<(dd + 127) / 128, 128, 0, s>>>(partial, grid, dd, dtheta, accumulate);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

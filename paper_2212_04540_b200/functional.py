@@ -112,6 +112,35 @@ def dequant_gemm_tn(q: QuantizedTensor, g: torch.Tensor, out: torch.Tensor | Non
     return out
 
 
+def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.Tensor):
+    """Fused layer backward (tape.py:217-225): returns (dtheta, dh) for
+    g_j = (g_read + g_e) * mask, dh = g_j theta^T, dtheta = Hhat^T g_j, with
+    the dequantized H never materialized.  Falls back to the separate ops for
+    d not in (32, 64) or pass-through contexts."""
+    from .tensorops import mask_apply, mm_theta
+    src = g_read if g_read is not None else g_e
+    d = src.shape[1]
+    if q.bits == PASSTHROUGH_BITS or d not in (32, 64) or q.group_size != d:
+        g = g_read if g_e is None else (g_e if g_read is None else g_read + g_e)
+        g_j = mask_apply(g, mask)
+        return dequant_gemm_tn(q, g_j), mm_theta(g_j, theta, transpose=True)
+    dev = src.device
+    rows = src.shape[0]
+    dh = torch.empty((rows, d), dtype=torch.float32, device=dev)
+    dth = torch.empty((d, d), dtype=torch.float32, device=dev)
+    L = _lib.load()
+    ws_bytes = int(L.kgq_layer_backward_workspace_bytes(rows, d))
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+    gr = None if g_read is None else g_read.contiguous()
+    ge = None if g_e is None else g_e.contiguous()
+    st = L.kgq_layer_backward_f32(_lib.ptr(gr), _lib.ptr(ge), mask.packed.data_ptr(),
+                                  q.codes.data_ptr(), q.ranges.data_ptr(), q.offsets.data_ptr(), rows,
+                                  d, q.bits, theta.contiguous().data_ptr(), dh.data_ptr(),
+                                  dth.data_ptr(), ws.data_ptr(), ws_bytes, 0, _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_layer_backward_f32")
+    return dth, dh
+
+
 def bpr_forward(u: torch.Tensor, p: torch.Tensor, n: torch.Tensor, l2: float):
     """tape.py:166-170: margins = sum(u*(p-n)); loss = mean softplus(-m) +
     l2*(|u|^2+|p|^2+|n|^2)/B.  Returns (loss 0-d tensor, margins)."""

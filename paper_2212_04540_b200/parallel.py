@@ -26,7 +26,7 @@ import torch
 from . import functional as F
 from .data import partition_rows, row_block
 from .quantize import QuantConfig, RandomStream, dequantize_tensor, quantize_tensor
-from .tensorops import CSR, mask_apply, mm_theta, spmm
+from .tensorops import CSR, mask_apply, spmm
 
 
 class Comm:
@@ -95,9 +95,7 @@ class GpuOps:
     dequantize = staticmethod(dequantize_tensor)
     scatter_rows = staticmethod(F.scatter_rows)
 
-    @staticmethod
-    def mm_t(g, theta):
-        return mm_theta(g, theta, transpose=True)
+    layer_backward = staticmethod(F.layer_backward)
 
 
 @dataclass
@@ -157,11 +155,8 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     g_e = None
     dthetas = [None] * len(thetas)
     for i in range(len(thetas) - 1, -1, -1):
-        g = g_read if g_e is None else g_read + g_e
         mask, q = saved[i]
-        g_j = ops.mask_apply(g, mask)
-        dthetas[i] = ops.dequant_gemm(q, g_j)
-        dh_local = ops.mm_t(g_j, thetas[i])
+        dthetas[i], dh_local = ops.layer_backward(g_read, g_e, mask, q, thetas[i])
         dh_full = comm.all_gather_rows(dh_local, counts)
         g_e = ops.spmm(a_local, dh_full)
     dth = comm.all_reduce_sum(torch.stack(dthetas))

@@ -324,3 +324,30 @@ def test_cuda_graph_epoch_equals_eager_epoch():
     assert s0[0]["peak_context_bytes"] == s1[0]["peak_context_bytes"]
     np.testing.assert_allclose(p0.entity_embeddings.cpu().numpy(), p1.entity_embeddings.cpu().numpy(),
                                rtol=1e-3, atol=1e-5)
+
+
+@pytest.mark.parametrize("d", [32, 64])
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("terms", ["both", "read", "e"])
+def test_fused_layer_backward_matches_fp64(d, bits, terms):
+    """g_j = (g_read + g_e)*mask; dH = g_j theta^T; dtheta = Hhat^T g_j (tape.py:217-225)."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(d * 10 + bits)
+    rows = 10007
+    x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(1), tensor_id=2)
+    j = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    _, mask = kgq.relu(j)
+    gr = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    ge = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    th = torch.from_numpy((rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
+    a, b = {"both": (gr, ge), "read": (gr, None), "e": (None, ge)}[terms]
+    dth, dh = F.layer_backward(a, b, mask, q, th)
+    g = (a if a is not None else 0) + (b if b is not None else 0)
+    gj = (g * (j > 0)).double()
+    hh = kgq.dequantize_tensor(q).double()
+    ref_dh = (gj @ th.double().t()).cpu().numpy()
+    ref_dth = (hh.t() @ gj).cpu().numpy()
+    np.testing.assert_allclose(dh.cpu().numpy(), ref_dh, rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(rows))

@@ -76,8 +76,10 @@ class OracleOps:
         return torch.from_numpy(orc.spmm_csr(ip, ix, vv, x.numpy()))
 
     @staticmethod
-    def mm_t(g, theta):
-        return g @ theta.t()
+    def layer_backward(g_read, g_e, mask, q, theta):
+        g = g_read if g_e is None else g_read + g_e
+        g_j = OracleOps.mask_apply(g, mask)
+        return OracleOps.dequant_gemm(q, g_j), g_j @ theta.t()
 
     @staticmethod
     def scatter_rows(rows, idx, g):
