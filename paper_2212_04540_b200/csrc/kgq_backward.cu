@@ -35,14 +35,14 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
     constexpr uint32_t CM = (1u << BITS) - 1u;
     constexpr int TPD = D / 4;                     // 4x4 dtheta tiles per dimension
     __shared__ __align__(16) float tht[D * D];     // theta^T: tht[k][j] = theta[j][k]
-    __shared__ __align__(16) float gs[kBwdRows][D];
-    __shared__ __align__(16) float hs[kBwdRows][D];
+    __shared__ __align__(16) float gs[kBwdRows][D];   // g_j, row-major (dtheta phase)
+    __shared__ __align__(16) float hs[kBwdRows][D];   // Hhat, row-major
+    __shared__ __align__(16) float gk[8][D][4];       // g_j per warp, k-major (dH phase)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     for (int i = t; i < D * D; i += 256) {
         const int j = i / D, k = i % D;
         tht[k * D + j] = __ldg(theta + i);         // theta[j][k]
     }
-    // dtheta tile of this thread (only the first TPD*TPD threads own one)
     const bool owner = t < TPD * TPD;
     const int ti = (t / TPD) * 4, tj = (t % TPD) * 4;
     float acc[4][4];
@@ -50,38 +50,52 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
     for (int a = 0; a < 4; a++)
 #pragma unroll
         for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
-    __syncthreads();
 
-    const int64_t n_chunks = (rows + kBwdRows - 1) / kBwdRows;
-    for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-        // ---- per warp: 4 rows -> g_j and Hhat in smem ----
+    // register prefetch of one chunk: this warp's 4 rows, columns lane + 32c
+    float pg[4][NC], pe[4][NC], pr[4], pz[4];
+    uint32_t pm[4][NC], pc[4][NC];
+    auto load = [&](int64_t ch) {
 #pragma unroll
         for (int rr = 0; rr < 4; rr++) {
-            const int lr = warp * 4 + rr;
-            const int64_t row = ch * kBwdRows + lr;
+            const int64_t row = ch * kBwdRows + warp * 4 + rr;
             const bool ok = row < rows;
-            float r = 0.f, z = 0.f;
-            if (ok) { r = __ldg(ranges + row); z = __ldg(offsets + row); }
+            pr[rr] = ok ? __ldg(ranges + row) : 0.f;
+            pz[rr] = ok ? __ldg(offsets + row) : 0.f;
 #pragma unroll
             for (int c = 0; c < NC; c++) {
                 const int col = lane + 32 * c;
-                float gj = 0.0f, hv = 0.0f;
-                if (ok) {
-                    // g = g_read + g_e in the reference's routing order (tape.py:204-209)
-                    float g;
-                    if (g_read && g_e) g = __fadd_rn(__ldg(g_read + row * D + col), __ldg(g_e + row * D + col));
-                    else if (g_read) g = __ldg(g_read + row * D + col);
-                    else g = __ldg(g_e + row * D + col);
-                    const uint32_t bit = (__ldg(mask + row * (D / 32) + c) >> lane) & 1u;
-                    gj = __fmul_rn(g, bit ? 1.0f : 0.0f);
-                    const int b = col * BITS;
-                    const uint32_t code = (__ldg(codes + row * RB + (b >> 3)) >> (b & 7)) & CM;
-                    hv = lut_entry<BITS>(r, z, (int)code);
-                }
-                gs[lr][col] = gj;
-                hs[lr][col] = hv;
+                pg[rr][c] = (ok && g_read) ? __ldg(g_read + row * D + col) : 0.f;
+                pe[rr][c] = (ok && g_e) ? __ldg(g_e + row * D + col) : 0.f;
+                pm[rr][c] = ok ? __ldg(mask + row * (D / 32) + c) : 0u;
+                const int b = col * BITS;
+                pc[rr][c] = ok ? __ldg(codes + row * RB + (b >> 3)) : 0u;
             }
         }
+    };
+    __syncthreads();
+
+    const int64_t n_chunks = (rows + kBwdRows - 1) / kBwdRows;
+    int64_t ch = blockIdx.x;
+    if (ch < n_chunks) load(ch);
+    for (; ch < n_chunks; ch += gridDim.x) {
+        // ---- stage g_j = (g_read + g_e) * mask and Hhat from the prefetched registers ----
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++) {
+            const int lr = warp * 4 + rr;
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const int col = lane + 32 * c;
+                // g = g_read + g_e in the reference's routing order (tape.py:204-209)
+                const float g = (g_read && g_e) ? __fadd_rn(pg[rr][c], pe[rr][c]) : (g_read ? pg[rr][c] : pe[rr][c]);
+                const float gj = __fmul_rn(g, ((pm[rr][c] >> lane) & 1u) ? 1.0f : 0.0f);
+                const int b = col * BITS;
+                const uint32_t code = (pc[rr][c] >> (b & 7)) & CM;
+                gs[lr][col] = gj;
+                gk[warp][col][rr] = gj;
+                hs[lr][col] = lut_entry<BITS>(pr[rr], pz[rr], (int)code);
+            }
+        }
+        if (ch + gridDim.x < n_chunks) load(ch + gridDim.x);
         __syncwarp();
         // ---- dH for the warp's 4 rows: dh[r][j] = sum_k g_j[r][k] theta[j][k] ----
         {
@@ -92,14 +106,13 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
                 for (int c = 0; c < NC; c++) o[rr][c] = 0.0f;
 #pragma unroll 8
             for (int k = 0; k < D; k++) {
-                float gk[4];
-#pragma unroll
-                for (int rr = 0; rr < 4; rr++) gk[rr] = gs[warp * 4 + rr][k];
+                const float4 g4 = *reinterpret_cast<const float4 *>(&gk[warp][k][0]);
+                const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
                     const float tk = tht[k * D + lane + 32 * c];
 #pragma unroll
-                    for (int rr = 0; rr < 4; rr++) o[rr][c] = __fmaf_rn(gk[rr], tk, o[rr][c]);
+                    for (int rr = 0; rr < 4; rr++) o[rr][c] = __fmaf_rn(gv[rr], tk, o[rr][c]);
                 }
             }
 #pragma unroll

@@ -198,7 +198,7 @@ def test_autograd_kgnn_equals_tape():
         assert ledger.peak_eq == tape.peak_fp32_equiv_bytes
         loss.backward()
         assert ledger.current == 0
-        assert float(loss) == pytest.approx(tape.loss(), rel=1e-6)
+        assert float(loss.detach()) == pytest.approx(tape.loss(), rel=1e-6)
         np.testing.assert_allclose(model.e0.grad.cpu().numpy(), tg["E0"].cpu().numpy(), rtol=1e-5, atol=1e-8)
         for i, layer in enumerate(model.layers):
             np.testing.assert_allclose(layer.weight.grad.cpu().numpy(), tg[f"theta{i}"].cpu().numpy(),
