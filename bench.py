@@ -112,10 +112,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or getattr(args, "partitioned", False):
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29000 + os.getpid() % 1000))
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -224,7 +229,7 @@ def train_bench(args, world, rank):
         rng = np.random.default_rng(0)
         stream = kgq.RandomStream(0)
         cur = torch.cuda.current_stream()
-        if world == 1:
+        if world == 1 and not args.partitioned:
             adj = D.build_adjacency(ds)
             params = init_params(ds.num_nodes, mcfg, 0)
             state = AdamState(params.as_dict())
@@ -291,21 +296,25 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     indptr, indices, vals = D.adjacency_arrays(ds)
     part = RowPartition.build(indptr, world, rank)
     a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda")
+    from paper_2212_04540_b200.train import AdamState, adam_step
     params = init_params(ds.num_nodes, mcfg, 0)
-    e0 = params.entity_embeddings[part.lo:part.hi].clone()
-    thetas = params.layer_weights
+    local = {"E0": params.entity_embeddings[part.lo:part.hi].clone()}
+    for i, t in enumerate(params.layer_weights):
+        local[f"theta{i}"] = t
+    state = AdamState(local)
     comm = Comm()
     trip = torch.from_numpy(D.sample_negatives(ds, rng)).cuda().long()
     n_users = ds.num_users
+    n_full = len(trip) // 1024
 
     def one(i):
-        b = trip[(i * 1024) % len(trip):][:1024]
-        loss, de0, dth = partitioned_step(part, a_local, e0, thetas, b[:, 0], n_users + b[:, 1],
-                                          n_users + b[:, 2], 1e-5, cfg.quant, stream, comm)
-        with torch.no_grad():
-            e0.sub_(1e-3 * de0)
-            for t, g in zip(thetas, dth):
-                t.sub_(1e-3 * g)
+        b = trip[(i % n_full) * 1024:][:1024]
+        thetas = [local[f"theta{k}"] for k in range(mcfg.layers)]
+        loss, de0, dth = partitioned_step(part, a_local, local["E0"], thetas, b[:, 0], n_users + b[:, 1],
+                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm)
+        grads = {"E0": de0}
+        grads.update({f"theta{k}": g for k, g in enumerate(dth)})
+        adam_step(local, grads, state, cfg.lr)
 
     for i in range(args.warmup + 2):
         one(i)
@@ -436,7 +445,10 @@ def run_ours(args):
     train = None
     if not args.skip_train:
         torch.cuda.empty_cache()
-        train = train_bench(args, world, rank)
+        try:
+            train = train_bench(args, world, rank)
+        except Exception as exc:            # never lose the headline line
+            train = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -479,8 +491,8 @@ def run_ours(args):
             "native_lib": os.path.relpath(_lib.LIB_PATH, ROOT),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -504,6 +516,8 @@ def main():
     ap.add_argument("--skip-compat", action="store_true")
     ap.add_argument("--skip-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="train step without CUDA graphs")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the row-partitioned (multi-GPU) training step even at 1 GPU")
     ap.add_argument("--train-shape", default="amazon", choices=["small", "lastfm", "amazon"])
     ap.add_argument("--train-steps", type=int, default=100)
     args = ap.parse_args()
