@@ -66,6 +66,14 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, h
 
 
+def layer_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
+                  stream: RandomStream | None, tensor_id: int | None = None, row_offset: int = 0):
+    """One KGNN layer: the fused kernel when it applies, else the separate ops."""
+    if can_fuse(cfg, e.shape[1]):
+        return graph_conv_forward(adj, e, theta, cfg, stream, tensor_id, row_offset)
+    return layer_forward_unfused(adj, e, theta, cfg, stream, tensor_id, row_offset)
+
+
 def layer_forward_unfused(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
                           stream: RandomStream | None, tensor_id: int | None = None,
                           row_offset: int = 0):

@@ -87,7 +87,7 @@ class GpuOps:
         ip, ix, vv = row_block(indptr, indices, vals, lo, hi)
         return CSR.from_arrays(ip, ix, vv, (hi - lo, n), device=device, symmetric=False)
 
-    graph_conv = staticmethod(F.graph_conv_forward)
+    graph_conv = staticmethod(F.layer_forward)
     dequant_gemm = staticmethod(F.dequant_gemm_tn)
     mask_apply = staticmethod(mask_apply)
     spmm = staticmethod(spmm)
