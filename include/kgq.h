@@ -135,9 +135,9 @@ KGQ_API int kgq_adam_step_f32(float *param, const float *grad, float *m, float *
                       double lr, double beta1, double beta2, double eps, int64_t step,
                       void *stream);
 
-/* Same update for CUDA-graph replay: t = *step_ptr (device int64, >= 1) and
- * the bias corrections are read from c12[2t], c12[2t+1] (host-built float32
- * table of 1 - beta1^t, 1 - beta2^t).  n % 4 == 0 and 16-byte alignment. */
+/* Same update for CUDA-graph replay: i = *step_ptr (device int64) indexes a
+ * host-built float32 table c12[2i], c12[2i+1] = 1 - beta1^t, 1 - beta2^t of
+ * the steps t the replays run.  n % 4 == 0 and 16-byte alignment. */
 KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, float *v, int64_t n,
                           double lr, double beta1, double beta2, double eps,
                           const float *c12, const int64_t *step_ptr, void *stream);

@@ -34,9 +34,10 @@ adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__
     }
 }
 
-// Graph-capturable variant: the step t is read on the device (*step_ptr) and
-// the bias corrections come from a host-built table c12[2t], c12[2t+1] =
-// float32(1 - beta^t) (Python's float pow, exactly as the reference).
+// Graph-capturable variant: the bias corrections are read from a host-built
+// table indexed on the device, c12[2i], c12[2i+1] = float32(1 - beta^t) for
+// i = *step_ptr (the table's rows map i to the absolute step t; Python's float
+// pow, exactly as the reference).
 __global__ void __launch_bounds__(256)
 adam_vec_dev_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
                     float4 *__restrict__ v, int64_t n4, AdamScalars a, const float *__restrict__ c12,
