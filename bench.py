@@ -233,7 +233,12 @@ def train_bench(args, world, rank):
             adj = D.build_adjacency(ds)
             params = init_params(ds.num_nodes, mcfg, 0)
             state = AdamState(params.as_dict())
+            # warm-up: eager steps, then (graphs) one capture of the step graph,
+            # reused by the timed call (capture cost is not in the timed region)
             train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.warmup + 2)
+            if not args.no_graphs:
+                train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=args.train_steps,
+                            graphs=True)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(cur)
