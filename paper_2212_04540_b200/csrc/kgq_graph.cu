@@ -254,6 +254,7 @@ __device__ __forceinline__ void light_row_quantize(const float4 (&h)[2], bool ac
     const uint64_t gglob = (uint64_t)(row_offset + row);
     uint32_t piece[2] = {0u, 0u};
     if (r > 0.0f) {
+        const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * p + q));
         const bool unguarded = group_div_unguarded(dv, z);
@@ -272,7 +273,7 @@ __device__ __forceinline__ void light_row_quantize(const float4 (&h)[2], bool ac
                 const float a = __fsub_rn(xs[el], z);
                 const float qv = unguarded ? div_a_unguarded(dv, a) : div_a(dv, a);
                 const float s = __fmul_rn(qv, Bf);
-                const float uf = hh ? __uint2float_rn(rw[el] >> 16) : __uint2float_rn(rw[el] & 0xFFFFu);
+                const float uf = hh ? u16_carrier_hi(rw[el], kc) : u16_carrier_lo(rw[el], kc);
                 acc += code_bits<MODE>(s, uf, cw[el] >> 11) << (BITS * el);
             }
             piece[hh] = acc - magic_sum4<BITS>();
@@ -347,7 +348,7 @@ __device__ __forceinline__ void heavy_layer_row(const int32_t *__restrict__ indp
             const float s = __fmul_rn(div_a(dv, __fsub_rn(h, z)), Bf);
             float uf = 0.0f;
             uint64_t raw53 = 0;
-            if (MODE == KGQ_ROUND_SR_FAST) uf = __uint2float_rn(fast_u16(fk, gglob, t));
+            if (MODE == KGQ_ROUND_SR_FAST) uf = u16_carrier(fast_u16(fk, gglob, t));
             if (MODE == KGQ_ROUND_SR_COMPAT) raw53 = compat_raw53(seed, tid, gglob, D, t);
             code = code_bits<MODE>(s, uf, raw53) - kMagicBits;
         }

@@ -19,6 +19,9 @@
 
 namespace kgq {
 
+#ifndef KGQ_QRING_KB
+#define KGQ_QRING_KB 64                // quantize prefetch ring per CTA
+#endif
 constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;
 constexpr int kGroupsPerWarp = 8;      // dequantize: 4 threads per group
@@ -35,7 +38,7 @@ struct Geo {
     static constexpr int NF = NBLK * Q;     // float4 per thread
     static constexpr int GPW = 32 / T;      // groups per warp tile
     // cp.async ring depth: <= 64 KB of prefetch slots per CTA
-    static constexpr int S = (NF * 512 * kWarps * 2 <= 64 * 1024) ? (64 * 1024) / (NF * 512 * kWarps) : 1;
+    static constexpr int S = (NF * 512 * kWarps * 2 <= KGQ_QRING_KB * 1024) ? (KGQ_QRING_KB * 1024) / (NF * 512 * kWarps) : 1;
 };
 
 // Codes of the NF float4 a thread owns, 4*BITS bits per float4 (LSB-first).
@@ -47,6 +50,7 @@ __device__ __forceinline__ void quant_pieces(const float4 (&v)[Geo<G, T>::NF], f
                                              uint32_t (&piece)[Geo<G, T>::NF]) {
     using GE = Geo<G, T>;
     constexpr float Bf = (float)PackInfo<BITS>::B;
+    const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
 #pragma unroll
     for (int p = 0; p < GE::NBLK / 2; p++) {
 #pragma unroll
@@ -71,7 +75,7 @@ __device__ __forceinline__ void quant_pieces(const float4 (&v)[Geo<G, T>::NF], f
                     const float a = __fsub_rn(xs[e], z);
                     const float qv = GUARD ? div_a(dv, a) : div_a_unguarded(dv, a);
                     const float s = __fmul_rn(qv, Bf);
-                    const float uf = h ? __uint2float_rn(rw[e] >> 16) : __uint2float_rn(rw[e] & 0xFFFFu);
+                    const float uf = h ? u16_carrier_hi(rw[e], kc) : u16_carrier_lo(rw[e], kc);
                     acc += code_bits<MODE>(s, uf, cw[e] >> 11) << (BITS * e);
                 }
                 piece[f] = acc - magic_sum4<BITS>();
@@ -198,9 +202,13 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
         uint8_t *dst = codes + g0 * GB;
         const int nbytes = nvalid * GB;
         if (nvalid == GPW) {   // full tile: GPW*GB bytes, a multiple of 16
+            constexpr int NCH = GPW * GB / 16;
 #pragma unroll
-            for (int b = lane * 16; b < GPW * GB; b += 32 * 16)
-                *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
+            for (int k = 0; k < (NCH + 31) / 32; k++) {
+                const int c = lane + 32 * k;
+                if (NCH % 32 == 0 || c < NCH)
+                    *reinterpret_cast<uint4 *>(dst + 16 * c) = *reinterpret_cast<const uint4 *>(st + 16 * c);
+            }
         } else if ((nbytes & 15) == 0) {
             for (int b = lane * 16; b < nbytes; b += 32 * 16)
                 *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
