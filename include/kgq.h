@@ -76,6 +76,29 @@ KGQ_API int kgq_dequantize_f32(const uint8_t *codes, const float *ranges, const 
                        int64_t n_groups, int32_t group, int32_t bits, float *out,
                        void *stream);
 
+/* Host-buffer forms of the two calls above: the reference's own calling
+ * convention (numpy arrays in, numpy arrays out; quantize.py:177-210).  The
+ * tensor streams through the device in chunks of groups on n_streams CUDA
+ * streams (H2D, kernel and D2H of different chunks overlap); the call blocks
+ * until the host outputs are written.  Bytes are identical to the device
+ * call for any chunking (noise keyed by global group index).
+ *   workspace: device memory of kgq_host_workspace_bytes(chunk, ...) bytes,
+ *              or NULL (allocated and freed inside the call).
+ *   streams:   n_streams caller streams, or NULL (3 created inside the call).
+ *   stream:    the work is ordered after this stream's pending work.
+ * KGQ_ROUND_SR_NOISE is device-only (returns KGQ_ERR_INVALID_ARG). */
+KGQ_API size_t kgq_host_workspace_bytes(int64_t chunk_groups, int32_t group, int32_t bits,
+                                        int32_t n_streams);
+KGQ_API int kgq_quantize_host_f32(const float *x, int64_t n_groups, int32_t group, int32_t bits,
+                                  int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                                  int64_t group_offset, uint8_t *codes, float *ranges,
+                                  float *offsets, void *workspace, size_t workspace_bytes,
+                                  void *const *streams, int32_t n_streams, void *stream);
+KGQ_API int kgq_dequantize_host_f32(const uint8_t *codes, const float *ranges, const float *offsets,
+                                    int64_t n_groups, int32_t group, int32_t bits, float *out,
+                                    void *workspace, size_t workspace_bytes,
+                                    void *const *streams, int32_t n_streams, void *stream);
+
 /* Export the exact SR noise a quantize call consumes (exported-noise parity route).
  * fast:   u16 per element, uniform = u16 / 65536.
  * compat: (raw >> 11) per element, uniform = value * 2^-53

@@ -10,7 +10,7 @@ CPU fallback.
 
 from . import _lib
 from .quantize import (EncodingError, QuantConfig, QuantizedTensor, RandomStream,
-                       compat_noise_raw53, dequantize_row, dequantize_tensor, fast_noise_u16,
+                       compat_noise_raw53, dequantize_row, dequantize_tensor, empty_context, fast_noise_u16,
                        fp32_equivalent_bytes, nearest_round, pack_bits, pack_codes, quantize_row,
                        quantize_tensor, stochastic_round, stored_bytes, unpack_bits, unpack_codes)
 from .tensorops import (CSR, BitMask, ShapeMismatchError, csr_nbytes, densify, make_csr, mm,

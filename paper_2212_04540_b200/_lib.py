@@ -35,6 +35,11 @@ SIGNATURES = {
     "kgq_last_cuda_error": (ctypes.c_int, []),
     "kgq_quantize_f32": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _U64, _U64, _P, _I64, _P, _P, _P, _P, _P]),
     "kgq_dequantize_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
+    "kgq_host_workspace_bytes": (ctypes.c_size_t, [_I64, _I32, _I32, _I32]),
+    "kgq_quantize_host_f32": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _U64, _U64, _I64, _P, _P, _P,
+                                              _P, ctypes.c_size_t, _P, _I32, _P]),
+    "kgq_dequantize_host_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P, ctypes.c_size_t,
+                                                _P, _I32, _P]),
     "kgq_fast_noise_u16": (ctypes.c_int, [_U64, _U64, _I64, _I64, _I32, _P, _P]),
     "kgq_compat_noise_raw53": (ctypes.c_int, [_U64, _U64, _I64, _I64, _I32, _P, _P]),
     "kgq_pack_codes": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P, _P]),

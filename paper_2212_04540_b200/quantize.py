@@ -163,12 +163,54 @@ class QuantizedTensor:
         return self.group if self.group is not None else self.cols
 
 
-def _require_fp32_2d(x, name="x"):
+def _require_fp32_2d(x, name="x", allow_host=False):
     if not isinstance(x, torch.Tensor) or x.dim() != 2:
         raise TypeError(f"{name} must be a 2-D torch.Tensor")
     if x.dtype != torch.float32:
         raise TypeError(f"{name} must be float32 (the B200 engine is fp32), got {x.dtype}")
-    _lib.require_cuda(x)
+    if not (allow_host and x.device.type == "cpu"):
+        _lib.require_cuda(x)
+
+
+class _HostPipe:
+    """Streams + device workspace for the host-buffer calls.  Three streams
+    per device are created once; the workspace comes from torch's caching
+    allocator on the current stream (the library orders its streams after
+    it), 64 MB of fp32 per chunk slot."""
+    _streams: dict = {}
+    CHUNK_ELEMS = 16 << 20
+
+    @classmethod
+    def args(cls, n_groups: int, group: int, bits: int):
+        """(workspace tensor, streams ctypes array, n_streams, order stream)
+        -- or Nones without CUDA (the library then reports the missing
+        device; there is no CPU path)."""
+        import ctypes
+        if not torch.cuda.is_available():
+            return None, None, 0, 0
+        dev = torch.cuda.current_device()
+        if dev not in cls._streams:
+            ss = [torch.cuda.Stream(dev) for _ in range(3)]
+            cls._streams[dev] = (ss, (ctypes.c_void_p * 3)(*[x.cuda_stream for x in ss]))
+        ss, arr = cls._streams[dev]
+        chunk = max(8, min(cls.CHUNK_ELEMS // max(group, 1), -(-n_groups // 8) * 8))
+        nbytes = _lib.load().kgq_host_workspace_bytes(chunk, group, bits, len(ss))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        return ws, ctypes.cast(arr, ctypes.c_void_p), len(ss), torch.cuda.current_stream().cuda_stream
+
+
+def empty_context(rows: int, cols: int, cfg: "QuantConfig", pin_memory: bool = True) -> "QuantizedTensor":
+    """Host buffers for ``quantize_tensor(host_x, ..., out=ctx)``: reusing
+    pinned buffers keeps the host-buffer path at PCIe speed (allocating
+    page-locked memory per call costs more than the transfer)."""
+    group = cols if cfg.group is None else int(cfg.group)
+    n_groups = rows * cols // group
+    return QuantizedTensor(rows, cols, cfg.bits,
+                           torch.empty((n_groups, packed_group_bytes(group, cfg.bits)), dtype=torch.uint8,
+                                       pin_memory=pin_memory),
+                           torch.empty(n_groups, dtype=torch.float32, pin_memory=pin_memory),
+                           torch.empty(n_groups, dtype=torch.float32, pin_memory=pin_memory),
+                           group=None if cfg.group is None else group)
 
 
 def packed_group_bytes(group: int, bits: int) -> int:
@@ -177,14 +219,25 @@ def packed_group_bytes(group: int, bits: int) -> int:
 
 def quantize_tensor(x: torch.Tensor, cfg: QuantConfig, stream: RandomStream | None = None,
                     tensor_id: int | None = None, *, noise: torch.Tensor | None = None,
-                    group_offset: int = 0) -> QuantizedTensor:
-    """quantize.py:177-196 on a CUDA fp32 tensor.
+                    group_offset: int = 0, out: QuantizedTensor | None = None) -> QuantizedTensor:
+    """quantize.py:177-196 on an fp32 tensor.
+
+    A CUDA tensor is quantized in place on its device.  A host (CPU) tensor
+    takes the reference's own numpy-in/numpy-out convention: it streams
+    through the GPU (``kgq_quantize_host_f32``, chunked and pipelined) and
+    the returned context lives in host memory -- computed on the GPU, not a
+    CPU fallback (without a GPU the call raises).
 
     ``noise`` (float64 uniforms, one per element) replaces the stream's
-    draws -- the exported-noise parity seam.  ``group_offset`` is the global
-    index of this tensor's first group (row-partitioned tensors).
+    draws -- the exported-noise parity seam (device tensors only).
+    ``group_offset`` is the global index of this tensor's first group
+    (row-partitioned tensors).  ``out`` (host path only): preallocated host
+    context from ``empty_context`` to write into.
     """
-    _require_fp32_2d(x)
+    _require_fp32_2d(x, allow_host=True)
+    host = x.device.type == "cpu"
+    if host and noise is not None:
+        raise ValueError("the exported-noise seam takes device tensors")
     rows, cols = x.shape
     if cfg.passthrough:
         return QuantizedTensor(rows, cols, cfg.bits, None, None, None, raw=x)
@@ -209,6 +262,25 @@ def quantize_tensor(x: torch.Tensor, cfg: QuantConfig, stream: RandomStream | No
             seed, tid = stream.seed, int(tensor_id) & 0xFFFFFFFFFFFFFFFF
     x = x.contiguous()
     dev = x.device
+    if host:
+        gb = packed_group_bytes(group, cfg.bits)
+        if out is None:
+            out = empty_context(rows, cols, cfg, pin_memory=x.is_pinned())
+        elif (out.codes.device.type != "cpu" or tuple(out.codes.shape) != (n_groups, gb)
+              or out.ranges.numel() != n_groups or out.offsets.numel() != n_groups
+              or not (out.codes.is_contiguous() and out.ranges.is_contiguous()
+                      and out.offsets.is_contiguous())):
+            raise ValueError("out must be a contiguous host context of this shape (empty_context)")
+        ws, sarr, ns, order = _HostPipe.args(n_groups, group, cfg.bits)
+        st = _lib.load().kgq_quantize_host_f32(x.data_ptr(), n_groups, group, cfg.bits, mode, seed, tid,
+                                               int(group_offset), out.codes.data_ptr(), out.ranges.data_ptr(),
+                                               out.offsets.data_ptr(), _lib.ptr(ws),
+                                               0 if ws is None else ws.numel(), sarr, ns, order)
+        _lib.check(st, "kgq_quantize_host_f32")
+        return QuantizedTensor(rows, cols, cfg.bits, out.codes, out.ranges, out.offsets,
+                               group=None if cfg.group is None else group)
+    if out is not None:
+        raise ValueError("out= is for host tensors")
     codes = torch.empty((n_groups, packed_group_bytes(group, cfg.bits)), dtype=torch.uint8, device=dev)
     ranges = torch.empty(n_groups, dtype=torch.float32, device=dev)
     offsets = torch.empty(n_groups, dtype=torch.float32, device=dev)
@@ -221,13 +293,33 @@ def quantize_tensor(x: torch.Tensor, cfg: QuantConfig, stream: RandomStream | No
                            group=None if cfg.group is None else group)
 
 
-def dequantize_tensor(q: QuantizedTensor, dtype=None) -> torch.Tensor:
-    """quantize.py:199-210: (R*c)/B + Z in fp32, R == 0 -> Z."""
+def dequantize_tensor(q: QuantizedTensor, dtype=None, *, out: torch.Tensor | None = None) -> torch.Tensor:
+    """quantize.py:199-210: (R*c)/B + Z in fp32, R == 0 -> Z.
+
+    A host context (from the host path of ``quantize_tensor``) is streamed
+    through the GPU and returns a host tensor (``out``: preallocated,
+    ideally pinned, host fp32 tensor of shape (rows, cols))."""
     if q.bits == PASSTHROUGH_BITS:
         return q.raw
     if dtype not in (None, torch.float32):
         raise ValueError("the B200 engine dequantizes to float32 only")
     dev = q.codes.device
+    if dev.type == "cpu":      # host context: streamed through the GPU (see quantize_tensor)
+        codes, ranges, offsets = q.codes.contiguous(), q.ranges.contiguous(), q.offsets.contiguous()
+        if out is None:
+            out = torch.empty((q.rows, q.cols), dtype=torch.float32, pin_memory=codes.is_pinned())
+        elif (out.device.type != "cpu" or out.dtype != torch.float32 or tuple(out.shape) != (q.rows, q.cols)
+              or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous host float32 tensor of shape (rows, cols)")
+        ws, sarr, ns, order = _HostPipe.args(q.n_groups, q.group_size, q.bits)
+        st = _lib.load().kgq_dequantize_host_f32(codes.data_ptr(), ranges.data_ptr(), offsets.data_ptr(),
+                                                 q.n_groups, q.group_size, q.bits, out.data_ptr(),
+                                                 _lib.ptr(ws), 0 if ws is None else ws.numel(), sarr, ns,
+                                                 order)
+        _lib.check(st, "kgq_dequantize_host_f32")
+        return out
+    if out is not None:
+        raise ValueError("out= is for host contexts")
     out = torch.empty((q.rows, q.cols), dtype=torch.float32, device=dev)
     st = _lib.load().kgq_dequantize_f32(q.codes.data_ptr(), q.ranges.data_ptr(), q.offsets.data_ptr(),
                                         q.n_groups, q.group_size, q.bits, out.data_ptr(),
