@@ -171,8 +171,12 @@ def test_errors_match_reference_classes():
     with pytest.raises(ValueError):
         kgq.quantize_tensor(torch.zeros((3, 8), device="cuda"), kgq.QuantConfig(bits=2, group=16),
                             kgq.RandomStream(0))
-    with pytest.raises(ValueError):
-        kgq.quantize_tensor(torch.zeros((3, 8)), kgq.QuantConfig(bits=2), kgq.RandomStream(0))
+    # a host tensor takes the host-buffer path (computed on the GPU, context in host memory)
+    qh = kgq.quantize_tensor(torch.zeros((3, 8)), kgq.QuantConfig(bits=2), kgq.RandomStream(0), tensor_id=0)
+    assert qh.codes.device.type == "cpu"
+    with pytest.raises(TypeError):
+        kgq.quantize_tensor(torch.zeros((3, 8), dtype=torch.float64, device="cuda"), kgq.QuantConfig(bits=2),
+                            kgq.RandomStream(0))
 
 
 def test_empty_and_tiny_inputs():
