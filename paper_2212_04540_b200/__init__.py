@@ -15,5 +15,7 @@ from .quantize import (EncodingError, QuantConfig, QuantizedTensor, RandomStream
                        quantize_tensor, stochastic_round, stored_bytes, unpack_bits, unpack_codes)
 from .tensorops import (CSR, BitMask, ShapeMismatchError, csr_nbytes, densify, make_csr, mm,
                         relu, spmm, spmm_t, validate_csr)
+from .formats import (CheckpointError, ParseError, load_checkpoint, load_dataset, save_checkpoint,
+                      save_dataset)
 
 __version__ = "0.1.0"

@@ -44,6 +44,36 @@ class KgDataset:
     triples: np.ndarray     # (m, 3) int32 (head, relation, tail), entity ids
     num_relations: int = 1
     _train_keys: np.ndarray | None = field(default=None, repr=False)
+    # string <-> index vocabularies (data.py:44-46); None for generated graphs
+    user_vocab: dict | None = field(default=None, repr=False)
+    entity_vocab: dict | None = field(default=None, repr=False)
+    relation_vocab: dict | None = field(default=None, repr=False)
+
+    def validate(self) -> None:
+        """data.py:67-90 (vectorized): index ranges, no pair in two splits,
+        triple endpoints / relations in range, items a prefix of entities."""
+        for name, arr in (("train", self.train), ("val", self.val), ("test", self.test)):
+            if len(arr):
+                if arr[:, 0].min() < 0 or arr[:, 0].max() >= self.num_users:
+                    raise ValueError(f"{name}: user index out of range")
+                if arr[:, 1].min() < 0 or arr[:, 1].max() >= self.num_items:
+                    raise ValueError(f"{name}: item index out of range")
+        parts = [a for a in (self.train, self.val, self.test) if len(a)]
+        if parts:
+            allp = np.concatenate(parts).astype(np.int64)
+            keys = allp[:, 0] * max(self.num_items, 1) + allp[:, 1]
+            if len(np.unique(keys)) != len(keys):
+                raise ValueError("a pair appears in more than one split")
+        if len(self.triples):
+            ends = self.triples[:, [0, 2]]
+            if ends.min() < 0 or ends.max() >= self.num_entities:
+                raise ValueError("triple endpoint out of entity range")
+            n_rel = len(self.relation_vocab) if self.relation_vocab is not None else self.num_relations
+            rels = self.triples[:, 1]
+            if rels.min() < 0 or rels.max() >= n_rel:
+                raise ValueError("triple relation out of range")
+        if self.num_items > self.num_entities:
+            raise ValueError("items must be a prefix of the entity space")
 
     @property
     def num_nodes(self) -> int:
