@@ -107,3 +107,16 @@ def test_generated_graph_roundtrip(tmp_path):
     key = lambda a: np.sort(a[:, 0].astype(np.int64) * 1000 + a[:, 1])
     allp = lambda d: np.concatenate([d.train, d.val, d.test])
     assert np.array_equal(key(allp(back)), key(allp(ds)))
+
+
+def test_half_fraction_row_and_verification_args():
+    """quantize.py:343-355 (deterministic) and the argument checks of
+    quantizer_verification (raised before any device work)."""
+    from paper_2212_04540_b200 import verification as V
+    r = V.half_fraction_row(3, 10)
+    assert r[0] == 0 and r[-1] == 3 and np.allclose(r[1:-1] % 1, 0.5)
+    assert np.array_equal(r[1:-1], (np.arange(8) % 3) + 0.5)
+    with pytest.raises(ValueError):
+        V.quantizer_verification(n_rows=0)
+    with pytest.raises(ValueError):
+        V.quantizer_verification(dim=2)
