@@ -215,11 +215,16 @@ def train_bench(args, world, rank):
     from paper_2212_04540_b200.model import ModelConfig, init_params
     from paper_2212_04540_b200.train import AdamState, TrainConfig, adam_step, memory_report, train_epoch
 
-    ds = D.synth_kg(D.SHAPES[args.train_shape], seed=0)
+    if args.train_shape in D.REFERENCE_DATASETS:
+        ds = D.reference_dataset(args.train_shape)
+        origin = "reference generator (synth_generate seed 0, datasets/)"
+    else:
+        ds = D.synth_kg(D.SHAPES[args.train_shape], seed=0)
+        origin = "vectorized generator"
     steps_per_epoch = (len(ds.train) + 1023) // 1024
-    out = {"workload": f"{args.train_shape}-shaped synthetic KG ({ds.num_users} users, {ds.num_items} items, "
-                       f"{ds.num_entities} entities, {len(ds.triples)} triples, {len(ds.train)} train pairs), "
-                       "KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
+    out = {"workload": f"{args.train_shape}-shaped synthetic KG from the {origin}: {ds.num_users} users, "
+                       f"{ds.num_items} items, {ds.num_entities} entities, {len(ds.triples)} triples, "
+                       f"{len(ds.train)} train pairs; KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
            "steps_per_epoch": steps_per_epoch, "n_gpus": world}
     res = {}
     for bits in (2, 32):
@@ -292,6 +297,36 @@ def train_bench(args, world, rank):
     return out
 
 
+def quality_bench(args):
+    """Recall@20 / NDCG@20 after ``--quality-epochs`` full epochs from the
+    reference's initial state (same params, batches, negatives: train_run,
+    train.py:175-227) at INT2 (fast and compat noise) and FP32, next to the
+    reference's own runs on the same dataset (datasets/*_reference_runs.json,
+    written by datasets/run_reference_training.py in the build container)."""
+    from paper_2212_04540_b200 import data as D
+    import paper_2212_04540_b200 as kgq
+    from paper_2212_04540_b200.model import ModelConfig
+    from paper_2212_04540_b200.train import TrainConfig, train_run
+    ds = D.reference_dataset(args.train_shape)
+    adj = D.build_adjacency(ds)
+    out = {"epochs": args.quality_epochs, "dataset": f"{args.train_shape}_seed0 (reference generator)"}
+    for name, bits, rng in (("int2_fast", 2, "fast"), ("int2_compat", 2, "compat"), ("fp32", 32, "fast")):
+        q = kgq.QuantConfig(bits=bits, rng=rng)
+        _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q),
+                           TrainConfig(epochs=args.quality_epochs, quant=q), adjacency=adj, graphs=True)
+        m = rep["metrics"]
+        out[name] = {"recall_at_20": round(m["recall_at_20"], 5), "ndcg_at_20": round(m["ndcg_at_20"], 5),
+                     "loss_curve": [round(v, 6) for v in rep["loss_curve"]],
+                     "epoch_s": [round(v, 3) for v in rep["timing"]["epoch_seconds"]],
+                     "activation_bytes_peak": rep["memory"]["activation_bytes_peak"]}
+    ref_path = os.path.join(ROOT, "datasets", f"{args.train_shape}_seed0_reference_runs.json")
+    if os.path.exists(ref_path):
+        with open(ref_path) as f:
+            ref = json.load(f)
+        out["reference"] = {k: v for k, v in ref.items() if int(v.get("epochs", -1)) == args.quality_epochs}
+    return out
+
+
 def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     """Row-partitioned step timing (parallel.partitioned_step over NCCL)."""
     import torch
@@ -300,7 +335,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     from paper_2212_04540_b200.parallel import Comm, GpuOps, RowPartition, partitioned_step
     indptr, indices, vals = D.adjacency_arrays(ds)
     part = RowPartition.build(indptr, world, rank)
-    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda")
+    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda", part=part)
     from paper_2212_04540_b200.train import AdamState, adam_step
     params = init_params(ds.num_nodes, mcfg, 0)
     local = {"E0": params.entity_embeddings[part.lo:part.hi].clone()}
@@ -316,7 +351,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
         b = trip[(i % n_full) * 1024:][:1024]
         thetas = [local[f"theta{k}"] for k in range(mcfg.layers)]
         loss, de0, dth = partitioned_step(part, a_local, local["E0"], thetas, b[:, 0], n_users + b[:, 1],
-                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm)
+                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, padded=True)
         grads = {"E0": de0}
         grads.update({f"theta{k}": g for k, g in enumerate(dth)})
         adam_step(local, grads, state, cfg.lr)
@@ -498,6 +533,12 @@ def run_ours(args):
             train = train_bench(args, world, rank)
         except Exception as exc:            # never lose the headline line
             train = {"error": f"{type(exc).__name__}: {exc}"}
+        if world == 1 and not args.skip_quality and args.train_shape in ("amazon", "lastfm"):
+            torch.cuda.empty_cache()
+            try:
+                train["quality"] = quality_bench(args)
+            except Exception as exc:
+                train["quality"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -565,6 +606,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-compat", action="store_true")
     ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--skip-quality", action="store_true")
+    ap.add_argument("--quality-epochs", type=int, default=1)
     ap.add_argument("--no-graphs", action="store_true", help="train step without CUDA graphs")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the row-partitioned (multi-GPU) training step even at 1 GPU")

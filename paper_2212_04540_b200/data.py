@@ -18,7 +18,8 @@ side of the hot path, not the hot path itself:
   large shapes (Last-FM / Amazon-book / industry), where the reference's
   Python-loop generator does not scale.  Its RNG stream
   differs from the reference's, so it is used for throughput, not parity;
-  parity runs use datasets produced by the reference (tests/golden/).
+  parity runs use datasets produced by the reference (tests/golden/, and
+  ``reference_dataset`` for the Amazon-book / Last-FM shapes).
 """
 
 from dataclasses import dataclass, field
@@ -107,6 +108,91 @@ class KgDataset:
         np.savez_compressed(path, num_users=self.num_users, num_items=self.num_items,
                             num_entities=self.num_entities, train=self.train, val=self.val,
                             test=self.test, triples=self.triples, num_relations=self.num_relations)
+
+
+def _uint(n: int):
+    return np.uint8 if n < 1 << 8 else np.uint16 if n < 1 << 16 else np.uint32
+
+
+def pack_dataset(ds: KgDataset) -> dict:
+    """Lossless compact arrays of a dataset in the reference generator's
+    canonical order (splits grouped by ascending user, split_interactions
+    data.py:200-227; triples lexsorted, data.py:392): per-user run counts +
+    narrow item ids, per-head counts + relations + within-(head, relation)
+    tail deltas as byte planes.  ~5x smaller than the raw int32 arrays
+    after compression."""
+    out = {"num_users": ds.num_users, "num_items": ds.num_items, "num_entities": ds.num_entities,
+           "num_relations": ds.num_relations}
+    for name in ("train", "val", "test"):
+        a = np.asarray(getattr(ds, name)).reshape(-1, 2)
+        if len(a) and np.any(np.diff(a[:, 0]) < 0):
+            raise ValueError(f"{name}: pairs are not grouped by ascending user")
+        cnt = np.bincount(a[:, 0], minlength=ds.num_users) if len(a) else np.zeros(ds.num_users, np.int64)
+        out[f"{name}_ucount"] = cnt.astype(_uint(int(cnt.max(initial=0)) + 1))
+        out[f"{name}_item"] = a[:, 1].astype(_uint(ds.num_items))
+    t = np.asarray(ds.triples).reshape(-1, 3).astype(np.int64)
+    if len(t):
+        order = np.lexsort((t[:, 2], t[:, 1], t[:, 0]))
+        if np.any(order != np.arange(len(t))):
+            raise ValueError("triples are not lexsorted by (head, relation, tail)")
+    hc = np.bincount(t[:, 0], minlength=ds.num_entities) if len(t) else np.zeros(ds.num_entities, np.int64)
+    out["tri_hcount"] = hc.astype(_uint(int(hc.max(initial=0)) + 1))
+    out["tri_rel"] = t[:, 1].astype(_uint(max(ds.num_relations, int(t[:, 1].max(initial=0)) + 1)))
+    start = np.ones(len(t), bool)
+    start[1:] = (t[1:, 0] != t[:-1, 0]) | (t[1:, 1] != t[:-1, 1])
+    delta = t[:, 2].copy()
+    delta[1:] -= np.where(start[1:], 0, t[:-1, 2])
+    nb = max(1, (int(delta.max(initial=0)).bit_length() + 7) // 8)
+    # byte planes: zlib finds the near-constant high bytes (~25% smaller)
+    out["tri_tdelta_planes"] = np.stack([(delta >> (8 * i)).astype(np.uint8) for i in range(nb)])
+    return out
+
+
+def unpack_dataset(z) -> KgDataset:
+    """Inverse of ``pack_dataset`` (bit-identical arrays)."""
+    U, I, E = int(z["num_users"]), int(z["num_items"]), int(z["num_entities"])
+    splits = {}
+    for name in ("train", "val", "test"):
+        cnt = z[f"{name}_ucount"].astype(np.int64)
+        users = np.repeat(np.arange(U, dtype=np.int32), cnt)
+        splits[name] = np.stack([users, z[f"{name}_item"].astype(np.int32)], axis=1).reshape(-1, 2)
+    heads = np.repeat(np.arange(E, dtype=np.int64), z["tri_hcount"].astype(np.int64))
+    rels = z["tri_rel"].astype(np.int64)
+    planes = z["tri_tdelta_planes"].astype(np.int64)
+    delta = np.zeros(planes.shape[1], np.int64)
+    for i in range(planes.shape[0]):
+        delta |= planes[i] << (8 * i)
+    start = np.ones(len(heads), bool)
+    start[1:] = (heads[1:] != heads[:-1]) | (rels[1:] != rels[:-1])
+    cs = np.cumsum(delta)
+    run = np.cumsum(start) - 1
+    base = (cs - delta)[start]
+    tails = cs - base[run] if len(heads) else cs
+    tri = np.stack([heads, rels, tails], axis=1).astype(np.int32).reshape(-1, 3)
+    return KgDataset(U, I, E, splits["train"], splits["val"], splits["test"], tri, int(z["num_relations"]))
+
+
+def save_compact(ds: KgDataset, path) -> None:
+    np.savez_compressed(path, **pack_dataset(ds))
+
+
+def load_compact(path) -> KgDataset:
+    with np.load(path) as z:
+        return unpack_dataset(z)
+
+
+REFERENCE_DATASETS = ("amazon", "lastfm")
+
+
+def reference_dataset(name: str) -> KgDataset:
+    """The Amazon-book / Last-FM-shaped datasets exactly as the REFERENCE
+    generator produces them (synth_generate, data.py:356-411, seed 0, spec
+    overrides of SURVEY.md 8(d)); written by datasets/make_reference_datasets.py."""
+    import os
+    if name not in REFERENCE_DATASETS:
+        raise ValueError(f"no reference dataset {name!r} (have {REFERENCE_DATASETS})")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    return load_compact(os.path.join(root, "datasets", f"{name}_seed0.npz"))
 
 
 def adjacency_arrays(ds: KgDataset):

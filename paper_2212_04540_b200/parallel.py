@@ -8,8 +8,11 @@ every layer's activations.  Per layer and direction there is one exchange:
     backward: dH     all-gather  -> local spmm (A_hat symmetric: dE = A_local . dH)
     params  : dtheta all-reduce (L*d*d floats), E0 rows stay local
 
-plus one all-gather of the readout so every rank evaluates the (tiny) BPR
-head on the same batch.  The quantization noise is keyed by GLOBAL row
+plus one exchange of the 3*B readout rows of the batch (all-reduce of an
+owner-filled B x d block) so every rank evaluates the (tiny) BPR head on the
+same batch.  The gathers can target a padded [world*max_count] layout whose
+row ids the local CSR is remapped to once, so the collective writes the
+SpMM's input directly (no concatenation copy of a full N x d tensor).  The quantization noise is keyed by GLOBAL row
 (``row_offset``), so the forward pass -- activations, codes, ranges, masks --
 is bit-identical to the single-GPU run at any world size; only the dtheta
 all-reduce reorders a sum (tolerance).
@@ -58,6 +61,34 @@ class Comm:
             parts = [out[r * m:(r + 1) * m] for r in range(self.world)]
         return torch.cat([parts[r][:counts[r]] for r in range(self.world)], 0).to(dev)
 
+    def all_gather_padded(self, local: torch.Tensor, m: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Every rank's block in a [world*m, ...] buffer, block r at rows
+        [r*m, r*m + count_r) (the padded layout ``RowPartition.padded_cols``
+        indexes), so no concatenation copy follows the collective."""
+        if out is None:
+            out = local.new_empty((self.world * m,) + tuple(local.shape[1:]))
+        if local.shape[0] == m:
+            buf = local.contiguous()
+        else:
+            buf = local.new_zeros((m,) + tuple(local.shape[1:]))
+            buf[:local.shape[0]] = local
+        if self.gloo:
+            parts = [torch.empty_like(buf, device="cpu") for _ in range(self.world)]
+            self.dist.all_gather(parts, buf.cpu(), group=self.group)
+            out.copy_(torch.cat(parts, 0))
+        else:
+            self.dist.all_gather_into_tensor(out, buf, group=self.group)
+        return out
+
+    def gather_index_rows(self, local: torch.Tensor, lo: int, idx: torch.Tensor) -> torch.Tensor:
+        """rows ``idx`` (global ids) of the row-partitioned tensor whose block
+        [lo, lo+len(local)) lives here: each rank fills the rows it owns and
+        the others contribute +0, so the all-reduce sum is exact."""
+        sel = (idx >= lo) & (idx < lo + local.shape[0])
+        out = local.new_zeros((idx.shape[0],) + tuple(local.shape[1:]))
+        out[sel] = local[idx[sel] - lo]
+        return self.all_reduce_sum(out)
+
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         if self.gloo and t.is_cuda:
             c = t.cpu()
@@ -75,6 +106,50 @@ class SoloComm:
     def all_gather_rows(self, local, counts):
         return local
 
+    def all_gather_padded(self, local, m, out=None):
+        return local
+
+    def gather_index_rows(self, local, lo, idx):
+        return local[idx - lo]
+
+    def all_reduce_sum(self, t):
+        return t
+
+
+class SimulatedRankComm:
+    """One rank of a ``world``-way partition run alone on one GPU (the 8-GPU
+    configurations measured on a 1-GPU box): collectives keep their shapes
+    and buffers, but the other ranks' blocks are whatever the persistent
+    gather buffers hold (initialised once, standing in for remote rows) and
+    reductions see only this rank's contribution.  Compute per rank is
+    exactly the real one; communication is not timed (bytes are reported
+    analytically by the caller).  Not for correctness runs."""
+
+    def __init__(self, world: int, rank: int, fill_std: float = 0.1, seed: int = 0):
+        self.world, self.rank = world, rank
+        self.fill_std, self.seed = fill_std, seed
+        self._bufs = {}
+
+    def _buf(self, key, shape, like):
+        b = self._bufs.get(key)
+        if b is None or tuple(b.shape) != tuple(shape):
+            g = torch.Generator(device=like.device).manual_seed(self.seed + len(self._bufs))
+            b = torch.empty(shape, dtype=like.dtype, device=like.device)
+            b.normal_(0.0, self.fill_std, generator=g).abs_()
+            self._bufs[key] = b
+        return b
+
+    def all_gather_padded(self, local, m, out=None):
+        buf = self._buf("gather", (self.world * m,) + tuple(local.shape[1:]), local) if out is None else out
+        buf[self.rank * m:self.rank * m + local.shape[0]].copy_(local)
+        return buf
+
+    def gather_index_rows(self, local, lo, idx):
+        out = self._buf(("rows", idx.shape[0]), (idx.shape[0],) + tuple(local.shape[1:]), local)
+        sel = (idx >= lo) & (idx < lo + local.shape[0])
+        out[sel] = local[idx[sel] - lo]
+        return out
+
     def all_reduce_sum(self, t):
         return t
 
@@ -83,8 +158,16 @@ class GpuOps:
     """The product path: libkgq kernels."""
 
     @staticmethod
-    def local_adjacency(indptr, indices, vals, lo, hi, n, device):
+    def local_adjacency(indptr, indices, vals, lo, hi, n, device, part: "RowPartition | None" = None):
+        """CSR rows [lo, hi); with ``part`` the column ids index the padded
+        gather buffer (``all_gather_padded``) instead of the global rows."""
         ip, ix, vv = row_block(indptr, indices, vals, lo, hi)
+        if part is not None:
+            ix = part.padded_cols(ix)
+            if part.world * part.block >= 1 << 31:
+                raise ValueError("padded gather layout exceeds int32 column ids")
+            ix = ix.astype(np.int32)
+            n = part.world * part.block
         return CSR.from_arrays(ip, ix, vv, (hi - lo, n), device=device, symmetric=False)
 
     graph_conv = staticmethod(F.layer_forward)
@@ -117,28 +200,52 @@ class RowPartition:
     def counts(self) -> list:
         return [int(self.cuts[r + 1] - self.cuts[r]) for r in range(self.world)]
 
+    @property
+    def block(self) -> int:
+        """Rows per block of the padded gather layout (max count)."""
+        return max(self.counts)
+
+    def padded_cols(self, cols: np.ndarray) -> np.ndarray:
+        """Global row id -> row of the padded [world*block] gather buffer."""
+        cols = np.asarray(cols, dtype=np.int64)
+        r = np.searchsorted(self.cuts, cols, side="right") - 1
+        return (r * self.block + (cols - self.cuts[r])).astype(np.int64)
+
     @classmethod
     def build(cls, indptr, world: int, rank: int) -> "RowPartition":
         return cls(world, rank, partition_rows(indptr, world), len(indptr) - 1)
 
 
 def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas, users, pos, neg,
-                     l2: float, cfg: QuantConfig, stream: RandomStream, comm, ops=GpuOps):
+                     l2: float, cfg: QuantConfig, stream: RandomStream, comm, ops=GpuOps,
+                     padded: bool = False):
     """One forward+backward of the KGNN backbone + BPR head on this rank's
     rows.  Returns (loss tensor, dE0 for the local rows, [dtheta_i] summed
-    over ranks).  Mirrors tape.py:193-253's routing order."""
+    over ranks).  Mirrors tape.py:193-253's routing order.
+
+    ``padded``: ``a_local`` indexes the padded gather layout
+    (``GpuOps.local_adjacency(..., part=part)``), so each exchange is one
+    all_gather_into_tensor with no concatenation copy.  The BPR head only
+    needs the 3*B batch rows of the readout: they are exchanged by index
+    (``gather_index_rows``), never the whole readout."""
     lo, counts = part.lo, part.counts
+    m = part.block
+
+    def gather(x):
+        return comm.all_gather_padded(x, m) if padded else comm.all_gather_rows(x, counts)
+
     saved = []
     e_local = e0_local
     readout_local = None
     for theta in thetas:
-        e_full = comm.all_gather_rows(e_local, counts)
+        e_full = gather(e_local)
         e_next, mask, q, _ = ops.graph_conv(a_local, e_full, theta, cfg, stream, row_offset=lo)
         saved.append((mask, q))
         readout_local = e_next if readout_local is None else readout_local + e_next
         e_local = e_next
-    readout = comm.all_gather_rows(readout_local, counts)
-    u, p, n = readout[users], readout[pos], readout[neg]
+    b = users.shape[0]
+    rows = comm.gather_index_rows(readout_local, lo, torch.cat([users, pos, neg]))
+    u, p, n = rows[:b], rows[b:2 * b], rows[2 * b:]
     loss, margins = F.bpr_forward(u, p, n, l2)
     qu, qp, qn = (ops.quantize(t, cfg, stream) for t in (u, p, n))
     one = torch.ones((), dtype=u.dtype, device=u.device)
@@ -157,7 +264,6 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     for i in range(len(thetas) - 1, -1, -1):
         mask, q = saved[i]
         dthetas[i], dh_local = ops.layer_backward(g_read, g_e, mask, q, thetas[i])
-        dh_full = comm.all_gather_rows(dh_local, counts)
-        g_e = ops.spmm(a_local, dh_full)
+        g_e = ops.spmm(a_local, gather(dh_local))
     dth = comm.all_reduce_sum(torch.stack(dthetas))
     return loss, g_e, list(dth.unbind(0))

@@ -1,5 +1,6 @@
 """Host-side input formats (the caller side of the hot path) vs the reference."""
 import numpy as np
+import pytest
 
 from paper_2212_04540_b200 import data as D
 from tests import golden_io
@@ -47,3 +48,55 @@ def test_synthetic_shapes_and_partition():
         assert sum(len(p[1]) for p in parts) == len(indices)
         nnz = [len(p[1]) for p in parts]
         assert max(nnz) <= indptr[-1] / w + np.diff(indptr).max() + 1
+
+
+def test_industry_generator_blocks_equal_adjacency():
+    """The chunked device generator (industry.py) at a small shape: its row
+    blocks, concatenated, are bit-identical to adjacency_arrays of the same
+    dataset (data.py:230-266 semantics), and its equal-nnz cuts match
+    partition_rows."""
+    from paper_2212_04540_b200.industry import IndustryGraph, IndustryShape
+    sh = IndustryShape(users=3000, items=1200, entities=9000, relations=7, groups=13,
+                       interactions_per_user=15.0, attr_links_per_item=6.0, user_chunk=700, item_chunk=250)
+    g = IndustryGraph(sh, seed=5, device="cpu")
+    ds = g.dataset()
+    ds.validate()
+    ip, ix, vv = D.adjacency_arrays(ds)
+    deg = g.degrees()
+    assert np.array_equal(np.diff(ip), deg.numpy())
+    for world in (1, 3):
+        cuts = g.partition(deg, world)
+        assert np.array_equal(cuts, D.partition_rows(ip, world))
+        parts = [g.row_block(int(cuts[r]), int(cuts[r + 1]), deg) for r in range(world)]
+        assert np.array_equal(np.concatenate([p[1].numpy() for p in parts]), ix)
+        vcat = np.concatenate([p[2].numpy() for p in parts])
+        assert np.array_equal(vcat.view(np.uint32), vv.view(np.uint32))
+        for r, p in enumerate(parts):
+            lo, hi = int(cuts[r]), int(cuts[r + 1])
+            assert np.array_equal(p[0].numpy(), ip[lo:hi + 1] - ip[lo])
+
+
+def test_compact_codec_roundtrip():
+    ds = D.synth_kg(D.SynthShape(300, 200, 700, relations=6), seed=2)
+    # reference order: splits grouped by user, triples lexsorted
+    for name in ("train", "test"):
+        a = getattr(ds, name)
+        setattr(ds, name, a[np.lexsort((a[:, 1], a[:, 0]))])
+    z = D.pack_dataset(ds)
+    back = D.unpack_dataset(z)
+    for k in ("train", "val", "test", "triples"):
+        assert np.array_equal(getattr(back, k), getattr(ds, k)), k
+    shuffled = ds.train[::-1].copy()
+    ds.train = shuffled
+    with pytest.raises(ValueError):
+        D.pack_dataset(ds)
+
+
+def test_reference_datasets_match_survey_counts():
+    """datasets/*_seed0.npz are the reference generator's output (SURVEY.md
+    8 C3/C4 probe counts: Amazon nnz 6,425,569 / train 579,759)."""
+    ds = D.reference_dataset("amazon")
+    assert (ds.num_users, ds.num_items, ds.num_entities) == (70679, 24915, 88572)
+    assert len(ds.train) == 579759
+    ip, _, _ = D.adjacency_arrays(ds)
+    assert int(ip[-1]) == 6425569

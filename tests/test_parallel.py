@@ -97,34 +97,37 @@ def _problem():
     return z, n, e0, thetas, idx
 
 
-def _run(world, rank, comm):
+def _run(world, rank, comm, padded=False):
     z, n, e0, thetas, (users, pos, neg) = _problem()
     part = RowPartition.build(z["indptr"], world, rank)
-    a_local = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
+    ip, ix, vv = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
+    if padded:                       # columns index the padded gather buffer
+        ix = part.padded_cols(ix).astype(np.int32)
     cfg = QuantConfig(bits=2)
-    loss, de0, dth = partitioned_step(part, a_local, e0[part.lo:part.hi], thetas, users, pos, neg,
-                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps)
+    loss, de0, dth = partitioned_step(part, (ip, ix, vv), e0[part.lo:part.hi], thetas, users, pos, neg,
+                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps, padded=padded)
     return part, loss, de0, dth
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, padded=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2212_04540_b200.parallel import Comm
-        part, loss, de0, dth = _run(world, rank, Comm())
+        part, loss, de0, dth = _run(world, rank, Comm(), padded)
         out_q.put((rank, part.lo, part.hi, float(loss), de0.numpy(), [t.numpy() for t in dth]))
     finally:
         dist.destroy_process_group()
 
 
-def test_partitioned_step_world2_gloo_matches_world1():
+@pytest.mark.parametrize("padded", [False, True], ids=["concat", "padded"])
+def test_partitioned_step_world2_gloo_matches_world1(padded):
     part1, loss1, de1, dth1 = _run(1, 0, SoloComm())
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + (7 if padded else 0)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, padded)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
@@ -149,3 +152,16 @@ def test_partitioned_world1_matches_reference_tape():
     for name, g in [("E0", de0)] + [(f"theta{i}", t) for i, t in enumerate(dth)]:
         ref = z["d64_b2_grad_" + name]
         assert np.abs(g.numpy() - ref).max() <= 0.05 * np.abs(ref).max() + 1e-7, name
+
+
+def test_padded_cols_layout():
+    indptr = np.array([0, 5, 9, 20, 22, 30, 31, 40], dtype=np.int64)   # 7 rows
+    for world in (1, 2, 3):
+        parts = [RowPartition.build(indptr, world, r) for r in range(world)]
+        p = parts[0]
+        cols = np.arange(7)
+        pc = p.padded_cols(cols)
+        for r in range(world):
+            lo, hi = int(p.cuts[r]), int(p.cuts[r + 1])
+            assert np.array_equal(pc[lo:hi], r * p.block + np.arange(hi - lo))
+        assert pc.max() < world * p.block
