@@ -327,6 +327,113 @@ def quality_bench(args):
     return out
 
 
+def industry_bench(args):
+    """BASELINE configs[4] (industry-scale KG, ~55M nodes, ~1e9 triples,
+    d=128, 3 layers, INT2) as a ``world``-way row partition measured one rank
+    at a time on this GPU: each simulated rank builds its own CSR row block
+    from the device generator (industry.py), then runs the real per-rank
+    partitioned step (parallel.partitioned_step, padded gather layout) with
+    the collectives replaced by SimulatedRankComm (remote rows = stand-in
+    values).  Reported: per-rank compute ms/step (max over the simulated
+    ranks is the compute part of a W-GPU step), the exchange bytes per rank
+    per step and their time at the measured NVLink peer bandwidth (an
+    estimate, not a measurement), local activation ledger."""
+    import torch
+    import paper_2212_04540_b200 as kgq
+    from paper_2212_04540_b200.industry import INDUSTRY, IndustryGraph
+    from paper_2212_04540_b200.parallel import RowPartition, SimulatedRankComm, partitioned_step
+    from paper_2212_04540_b200.tensorops import CSR
+    from paper_2212_04540_b200.train import AdamState, adam_step
+
+    W = args.industry_world
+    ranks = [int(r) for r in args.industry_ranks.split(",")]
+    d, L, B = 128, 3, 1024
+    t0 = time.perf_counter()
+    g = IndustryGraph(INDUSTRY, seed=0, device="cuda")
+    deg = g.degrees()
+    cuts = g.partition(deg, W)
+    torch.cuda.synchronize()
+    t_deg = time.perf_counter() - t0
+    U, I = INDUSTRY.users, INDUSTRY.items
+    nnz_total = int(deg.sum())
+    n_train = int(deg[:U].sum()) - U
+    n_triples_edges = (nnz_total - g.n - 2 * n_train) // 2
+    out = {"workload": f"industry-scale synthetic KG (device generator): {g.n} nodes ({U} users, {I} items, "
+                       f"{INDUSTRY.entities} entities), {n_triples_edges} KG edges + {n_train} train pairs, "
+                       f"adjacency nnz {nnz_total}; KGNN {L} layers d={d}, batch {B}, INT2 stochastic (fast rng)",
+           "world": W, "generator_degrees_s": round(t_deg, 2), "ranks": {}}
+    cfg = kgq.QuantConfig(bits=2)
+    for rank in ranks:
+        t1 = time.perf_counter()
+        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+        ip, ix, vv = g.row_block(lo, hi, deg)
+        part = RowPartition(W, rank, cuts, g.n)
+        a_local = CSR(ip, ix, vv, (hi - lo, g.n), symmetric=False)   # global column ids
+        torch.cuda.synchronize()
+        t_blk = time.perf_counter() - t1
+        gen = torch.Generator(device="cuda").manual_seed(rank)
+        bound = (6.0 / (g.n + d)) ** 0.5
+        params = {"E0": (torch.rand((hi - lo, d), device="cuda", generator=gen) * 2 - 1) * bound}
+        tb = (6.0 / (2 * d)) ** 0.5
+        for i in range(L):
+            params[f"theta{i}"] = (torch.rand((d, d), device="cuda", generator=gen) * 2 - 1) * tb
+        state = AdamState(params)
+        comm = SimulatedRankComm(W, rank)
+        stream = kgq.RandomStream(0)
+        users = torch.randint(0, U, (64, B), device="cuda", generator=gen)
+        items = U + torch.randint(0, I, (64, 2, B), device="cuda", generator=gen)
+
+        def one(k):
+            th = [params[f"theta{i}"] for i in range(L)]
+            loss, de0, dth = partitioned_step(part, a_local, params["E0"], th, users[k % 64],
+                                              items[k % 64, 0], items[k % 64, 1], 1e-5, cfg, stream,
+                                              comm, layout="global")
+            grads = {"E0": de0}
+            grads.update({f"theta{i}": t for i, t in enumerate(dth)})
+            adam_step(params, grads, state, 1e-3)
+
+        for k in range(max(args.warmup, 1)):
+            one(k)
+        torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_steps = max(1, min(args.steps, 5))
+        a.record(cur)
+        for k in range(n_steps):
+            one(100 + k)
+        b.record(cur)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n_steps
+        if os.environ.get("KGQ_PROFILE_STEP"):     # ncu --profile-from-start off: one step
+            torch.cuda.cudart().cudaProfilerStart()
+            one(200)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStop()
+        rows = hi - lo
+        out["ranks"][str(rank)] = {
+            "rows": rows, "nnz": int(a_local.nnz), "block_build_s": round(t_blk, 2),
+            "ms_per_step": round(ms, 2),
+            "spmm_gathered_GB_per_step": round(2 * L * a_local.nnz * d * 4 / 1e9, 2),
+            "activation_MB_local": round(L * rows * (d * 2 // 8 + 8 + d // 8) / 1e6, 1),
+            "fp32_equivalent_MB_local": round(L * rows * (d * 4 + d // 8) / 1e6, 1),
+            "peak_mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1)}
+        del a_local, ip, ix, vv, params, state, comm
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+    worst = max(v["ms_per_step"] for v in out["ranks"].values())
+    # all-gather-v (layout="global"): every rank receives the rows it lacks,
+    # 2L times per step; the largest receiver is the rank with fewest rows
+    xbytes = 2 * L * (g.n - min(int(cuts[r + 1] - cuts[r]) for r in range(W))) * d * 4
+    out.update({"compute_ms_per_step_max_over_simulated_ranks": worst,
+                "exchange_GB_per_rank_per_step": round(xbytes / 1e9, 2),
+                "exchange_ms_estimate_at_770GBps": round(xbytes / 770e9 * 1e3, 1),
+                "steps_per_epoch": -(-n_train // B),
+                "epoch_hours_estimate": round(-(-n_train // B) * (worst + xbytes / 770e9 * 1e3) / 3.6e6, 2),
+                "note": "1-GPU box: compute per rank measured, collectives simulated (not timed); the "
+                        "exchange time is bytes / 770 GB/s measured peer bandwidth, no overlap assumed"})
+    return out
+
+
 def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     """Row-partitioned step timing (parallel.partitioned_step over NCCL)."""
     import torch
@@ -335,7 +442,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     from paper_2212_04540_b200.parallel import Comm, GpuOps, RowPartition, partitioned_step
     indptr, indices, vals = D.adjacency_arrays(ds)
     part = RowPartition.build(indptr, world, rank)
-    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda", part=part)
+    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda")
     from paper_2212_04540_b200.train import AdamState, adam_step
     params = init_params(ds.num_nodes, mcfg, 0)
     local = {"E0": params.entity_embeddings[part.lo:part.hi].clone()}
@@ -351,7 +458,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
         b = trip[(i % n_full) * 1024:][:1024]
         thetas = [local[f"theta{k}"] for k in range(mcfg.layers)]
         loss, de0, dth = partitioned_step(part, a_local, local["E0"], thetas, b[:, 0], n_users + b[:, 1],
-                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, padded=True)
+                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, layout="global")
         grads = {"E0": de0}
         grads.update({f"theta{k}": g for k, g in enumerate(dth)})
         adam_step(local, grads, state, cfg.lr)
@@ -540,6 +647,14 @@ def run_ours(args):
             except Exception as exc:
                 train["quality"] = {"error": f"{type(exc).__name__}: {exc}"}
 
+    industry = None
+    if args.industry and world == 1:
+        torch.cuda.empty_cache()
+        try:
+            industry = industry_bench(args)
+        except Exception as exc:
+            industry = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         threads = os.cpu_count() or 1
@@ -578,6 +693,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "train": train,
+            **({"industry": industry} if industry is not None else {}),
             "native_lib": os.path.relpath(_lib.LIB_PATH, ROOT),
         }
         print(json.dumps(line), flush=True)
@@ -607,6 +723,9 @@ def main():
     ap.add_argument("--skip-compat", action="store_true")
     ap.add_argument("--skip-train", action="store_true")
     ap.add_argument("--skip-quality", action="store_true")
+    ap.add_argument("--industry", action="store_true", help="configs[4] per-rank shard measurement")
+    ap.add_argument("--industry-world", type=int, default=8)
+    ap.add_argument("--industry-ranks", default="0")
     ap.add_argument("--quality-epochs", type=int, default=1)
     ap.add_argument("--no-graphs", action="store_true", help="train step without CUDA graphs")
     ap.add_argument("--partitioned", action="store_true",

@@ -80,6 +80,26 @@ class Comm:
             self.dist.all_gather_into_tensor(out, buf, group=self.group)
         return out
 
+    def all_gather_global(self, local: torch.Tensor, cuts, out: torch.Tensor | None = None) -> torch.Tensor:
+        """All-gather-v into the GLOBAL row layout: rank r's block lands at
+        rows [cuts[r], cuts[r+1]) of one [n, ...] buffer (one broadcast per
+        source rank, issued together), so uneven equal-nnz blocks move
+        exactly n - count rows per rank and the local CSR keeps its global
+        column ids (no padding, no concatenation copy)."""
+        n = int(cuts[-1])
+        lo, hi = int(cuts[self.rank]), int(cuts[self.rank + 1])
+        if out is None:
+            out = local.new_empty((n,) + tuple(local.shape[1:]))
+        stage = out.cpu() if (self.gloo and out.is_cuda) else out
+        stage[lo:hi].copy_(local)
+        works = [self.dist.broadcast(stage[int(cuts[r]):int(cuts[r + 1])], src=r, group=self.group,
+                                     async_op=True) for r in range(self.world) if cuts[r + 1] > cuts[r]]
+        for w in works:
+            w.wait()
+        if stage is not out:
+            out.copy_(stage)
+        return out
+
     def gather_index_rows(self, local: torch.Tensor, lo: int, idx: torch.Tensor) -> torch.Tensor:
         """rows ``idx`` (global ids) of the row-partitioned tensor whose block
         [lo, lo+len(local)) lives here: each rank fills the rows it owns and
@@ -107,6 +127,9 @@ class SoloComm:
         return local
 
     def all_gather_padded(self, local, m, out=None):
+        return local
+
+    def all_gather_global(self, local, cuts, out=None):
         return local
 
     def gather_index_rows(self, local, lo, idx):
@@ -142,6 +165,13 @@ class SimulatedRankComm:
     def all_gather_padded(self, local, m, out=None):
         buf = self._buf("gather", (self.world * m,) + tuple(local.shape[1:]), local) if out is None else out
         buf[self.rank * m:self.rank * m + local.shape[0]].copy_(local)
+        return buf
+
+    def all_gather_global(self, local, cuts, out=None):
+        n = int(cuts[-1])
+        buf = self._buf("gather", (n,) + tuple(local.shape[1:]), local) if out is None else out
+        lo = int(cuts[self.rank])
+        buf[lo:lo + local.shape[0]].copy_(local)
         return buf
 
     def gather_index_rows(self, local, lo, idx):
@@ -218,21 +248,33 @@ class RowPartition:
 
 def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas, users, pos, neg,
                      l2: float, cfg: QuantConfig, stream: RandomStream, comm, ops=GpuOps,
-                     padded: bool = False):
+                     padded: bool = False, layout: str | None = None):
     """One forward+backward of the KGNN backbone + BPR head on this rank's
     rows.  Returns (loss tensor, dE0 for the local rows, [dtheta_i] summed
     over ranks).  Mirrors tape.py:193-253's routing order.
 
-    ``padded``: ``a_local`` indexes the padded gather layout
-    (``GpuOps.local_adjacency(..., part=part)``), so each exchange is one
-    all_gather_into_tensor with no concatenation copy.  The BPR head only
+    ``layout`` of the E / dH exchanges: "concat" (all_gather of padded
+    blocks, then concatenated), "padded" (``a_local`` indexes the padded
+    layout, ``GpuOps.local_adjacency(..., part=part)``: one
+    all_gather_into_tensor, no copy; best for equal-row blocks) or "global"
+    (all-gather-v by per-source broadcasts into the global layout: exact
+    bytes for uneven equal-nnz blocks, global column ids, no copy).
+    ``padded=True`` is shorthand for layout="padded".  The BPR head only
     needs the 3*B batch rows of the readout: they are exchanged by index
     (``gather_index_rows``), never the whole readout."""
     lo, counts = part.lo, part.counts
     m = part.block
 
+    layout = layout or ("padded" if padded else "concat")
+    if layout not in ("concat", "padded", "global"):
+        raise ValueError(f"unknown exchange layout {layout!r}")
+
     def gather(x):
-        return comm.all_gather_padded(x, m) if padded else comm.all_gather_rows(x, counts)
+        if layout == "padded":
+            return comm.all_gather_padded(x, m)
+        if layout == "global":
+            return comm.all_gather_global(x, part.cuts)
+        return comm.all_gather_rows(x, counts)
 
     saved = []
     e_local = e0_local

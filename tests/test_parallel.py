@@ -97,37 +97,37 @@ def _problem():
     return z, n, e0, thetas, idx
 
 
-def _run(world, rank, comm, padded=False):
+def _run(world, rank, comm, layout="concat"):
     z, n, e0, thetas, (users, pos, neg) = _problem()
     part = RowPartition.build(z["indptr"], world, rank)
     ip, ix, vv = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
-    if padded:                       # columns index the padded gather buffer
+    if layout == "padded":           # columns index the padded gather buffer
         ix = part.padded_cols(ix).astype(np.int32)
     cfg = QuantConfig(bits=2)
     loss, de0, dth = partitioned_step(part, (ip, ix, vv), e0[part.lo:part.hi], thetas, users, pos, neg,
-                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps, padded=padded)
+                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps, layout=layout)
     return part, loss, de0, dth
 
 
-def _worker(rank, world, port, out_q, padded=False):
+def _worker(rank, world, port, out_q, layout="concat"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2212_04540_b200.parallel import Comm
-        part, loss, de0, dth = _run(world, rank, Comm(), padded)
+        part, loss, de0, dth = _run(world, rank, Comm(), layout)
         out_q.put((rank, part.lo, part.hi, float(loss), de0.numpy(), [t.numpy() for t in dth]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("padded", [False, True], ids=["concat", "padded"])
-def test_partitioned_step_world2_gloo_matches_world1(padded):
+@pytest.mark.parametrize("layout", ["concat", "padded", "global"])
+def test_partitioned_step_world2_gloo_matches_world1(layout):
     part1, loss1, de1, dth1 = _run(1, 0, SoloComm())
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000) + (7 if padded else 0)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, padded)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + 7 * ["concat", "padded", "global"].index(layout)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, layout)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
