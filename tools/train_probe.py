@@ -11,7 +11,7 @@ shape = sys.argv[1] if len(sys.argv) > 1 else "amazon"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 bits = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 t0 = time.time()
-ds = D.synth_kg(D.SHAPES[shape], seed=0)
+ds = D.reference_dataset(shape) if shape in D.REFERENCE_DATASETS else D.synth_kg(D.SHAPES[shape], seed=0)
 t1 = time.time()
 adj = D.build_adjacency(ds)
 print(f"gen {t1-t0:.1f}s adj {time.time()-t1:.1f}s nodes {ds.num_nodes} nnz {adj.nnz} train {len(ds.train)} triples {len(ds.triples)}", flush=True)
