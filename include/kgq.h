@@ -172,7 +172,7 @@ KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, flo
 KGQ_API int kgq_rowmm_f32(const float *a, int64_t rows, int32_t d, const float *theta,
                   int32_t transpose_theta, float *out, void *stream);
 
-/* Fused KGNN layer backward (tape.py:217-225), d in {32, 64}:
+/* Fused KGNN layer backward (tape.py:217-225), d in {32, 64, 128}:
  *   g_j = (g_read + g_e) * mask;  dh = g_j . theta^T;  dtheta (+)= Hhat^T . g_j
  * with Hhat = dequantize(codes, ranges, offsets) never materialized.  g_read
  * or g_e may be NULL (not both).  workspace: kgq_layer_backward_workspace_bytes.

@@ -1,5 +1,5 @@
 // kgq_backward.cu -- fused per-layer backward of the KGNN layer (tape.py:217-225,
-// SURVEY.md 8(f) rank 1), d in {32, 64}:
+// SURVEY.md 8(f) rank 1), d in {32, 64, 128}:
 //
 //   g_j   = (g_read + g_e) * mask                      (relu backward, tape.py:224-225)
 //   dH    = g_j . theta^T                              (mm backward, tape.py:223)
@@ -9,8 +9,11 @@
 // registers / shared memory.  Each CTA walks 32-row chunks (8 warps x 4 rows);
 // lane l owns columns l + 32c.  dH uses theta^T staged in smem (broadcast
 // LDS of g_j, conflict-free LDS of theta^T, FFMA); dtheta is accumulated in a
-// 4x4 register tile per thread over the CTA's rows and reduced across CTAs
+// TSxTS register tile per thread (TS = 4 for d <= 64, 8 for d = 128, so the
+// d*d/TS^2 tiles fit 256 threads) over the CTA's rows and reduced across CTAs
 // in a fixed order (deterministic).  dH then feeds the SpMM (A_hat^T = A_hat).
+// Shared memory is dynamic: theta^T d*d + g_j, Hhat 2*32*d + g_j k-major 32*d
+// floats (112 KB at d = 128).
 #include "kgq_common.cuh"
 
 namespace kgq {
@@ -23,6 +26,11 @@ static inline int bwd_grid(int64_t rows) {
     return g < 1 ? 1 : (int)g;
 }
 
+template <int D>
+struct BwdSmem {
+    static constexpr size_t bytes = ((size_t)D * D + 3 * (size_t)kBwdRows * D) * sizeof(float);
+};
+
 template <int D, int BITS>
 __global__ void __launch_bounds__(256)
 layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
@@ -33,23 +41,26 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
     constexpr int NC = D / 32;                     // columns per lane
     constexpr int RB = D * BITS / 8;
     constexpr uint32_t CM = (1u << BITS) - 1u;
-    constexpr int TPD = D / 4;                     // 4x4 dtheta tiles per dimension
-    __shared__ __align__(16) float tht[D * D];     // theta^T: tht[k][j] = theta[j][k]
-    __shared__ __align__(16) float gs[kBwdRows][D];   // g_j, row-major (dtheta phase)
-    __shared__ __align__(16) float hs[kBwdRows][D];   // Hhat, row-major
-    __shared__ __align__(16) float gk[8][D][4];       // g_j per warp, k-major (dH phase)
+    constexpr int TS = D > 64 ? 8 : 4;             // dtheta register tile
+    constexpr int TPD = D / TS;                    // tiles per dimension (TPD^2 <= 256)
+    static_assert(TPD * TPD <= 256, "dtheta tiles exceed the CTA");
+    extern __shared__ __align__(16) float bwd_smem[];
+    float *tht = bwd_smem;                                                   // theta^T [D][D]
+    auto gs = reinterpret_cast<float (*)[D]>(bwd_smem + D * D);              // g_j [32][D]
+    auto hs = reinterpret_cast<float (*)[D]>(bwd_smem + D * D + kBwdRows * D);   // Hhat [32][D]
+    auto gk = reinterpret_cast<float (*)[D][4]>(bwd_smem + D * D + 2 * kBwdRows * D);  // [8][D][4]
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     for (int i = t; i < D * D; i += 256) {
         const int j = i / D, k = i % D;
         tht[k * D + j] = __ldg(theta + i);         // theta[j][k]
     }
     const bool owner = t < TPD * TPD;
-    const int ti = (t / TPD) * 4, tj = (t % TPD) * 4;
-    float acc[4][4];
+    const int ti = (t / TPD) * TS, tj = (t % TPD) * TS;
+    float acc[TS][TS];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int a = 0; a < TS; a++)
 #pragma unroll
-        for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
+        for (int b = 0; b < TS; b++) acc[a][b] = 0.0f;
 
     // register prefetch of one chunk: this warp's 4 rows, columns lane + 32c
     float pg[4][NC], pe[4][NC], pr[4], pz[4];
@@ -129,14 +140,18 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
         if (owner) {
 #pragma unroll 4
             for (int rr = 0; rr < kBwdRows; rr++) {
-                const float4 a4 = *reinterpret_cast<const float4 *>(&hs[rr][ti]);
-                const float4 b4 = *reinterpret_cast<const float4 *>(&gs[rr][tj]);
-                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+                float av[TS], bv[TS];
 #pragma unroll
-                for (int a = 0; a < 4; a++)
+                for (int v = 0; v < TS / 4; v++) {
+                    const float4 a4 = *reinterpret_cast<const float4 *>(&hs[rr][ti + 4 * v]);
+                    const float4 b4 = *reinterpret_cast<const float4 *>(&gs[rr][tj + 4 * v]);
+                    av[4 * v] = a4.x; av[4 * v + 1] = a4.y; av[4 * v + 2] = a4.z; av[4 * v + 3] = a4.w;
+                    bv[4 * v] = b4.x; bv[4 * v + 1] = b4.y; bv[4 * v + 2] = b4.z; bv[4 * v + 3] = b4.w;
+                }
 #pragma unroll
-                    for (int b = 0; b < 4; b++) acc[a][b] = __fmaf_rn(av[a], bv[b], acc[a][b]);
+                for (int a = 0; a < TS; a++)
+#pragma unroll
+                    for (int b = 0; b < TS; b++) acc[a][b] = __fmaf_rn(av[a], bv[b], acc[a][b]);
             }
         }
         __syncthreads();
@@ -144,9 +159,11 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
     if (owner) {
         float *dst = partial + (int64_t)blockIdx.x * D * D;
 #pragma unroll
-        for (int a = 0; a < 4; a++)
-            *reinterpret_cast<float4 *>(dst + (ti + a) * D + tj) =
-                make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+        for (int a = 0; a < TS; a++)
+#pragma unroll
+            for (int v = 0; v < TS / 4; v++)
+                *reinterpret_cast<float4 *>(dst + (ti + a) * D + tj + 4 * v) =
+                    make_float4(acc[a][4 * v], acc[a][4 * v + 1], acc[a][4 * v + 2], acc[a][4 * v + 3]);
     }
 }
 
@@ -170,7 +187,7 @@ __global__ void reduce_partials_bwd_kernel(const float *__restrict__ partial, in
 using namespace kgq;
 
 extern "C" size_t kgq_layer_backward_workspace_bytes(int64_t rows, int32_t d) {
-    if (d != 32 && d != 64) return 0;
+    if (d != 32 && d != 64 && d != 128) return 0;
     return (size_t)bwd_grid(rows) * d * d * sizeof(float);
 }
 
@@ -181,7 +198,7 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
                                       void *workspace, size_t workspace_bytes, int32_t accumulate,
                                       void *stream) {
     if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
-    if (d != 32 && d != 64) return KGQ_ERR_INVALID_ARG;     // caller falls back (unfused)
+    if (d != 32 && d != 64 && d != 128) return KGQ_ERR_INVALID_ARG;   // caller falls back (unfused)
     if (rows < 0) return KGQ_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     if (rows == 0) {
@@ -199,9 +216,20 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     const int grid = bwd_grid(rows);
     float *partial = reinterpret_cast<float *>(workspace);
     const uint32_t *m32 = reinterpret_cast<const uint32_t *>(mask);
-#define KGQ_BWD(D, B) layer_backward_kernel<D, B><<<grid, 256, 0, s>>>(g_read, g_e, m32, codes, ranges, \
-                                                                       offsets, rows, theta, dh, partial)
-    if (d == 64) {
+#define KGQ_BWD(D, B) do {                                                                          \
+        static bool attr_set = false;   /* > 48 KB dynamic smem needs the opt-in once per instance */ \
+        if (!attr_set) {                                                                          \
+            cudaFuncSetAttribute(layer_backward_kernel<D, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)BwdSmem<D>::bytes);                                         \
+            attr_set = true;                                                                      \
+        }                                                                                         \
+        layer_backward_kernel<D, B><<<grid, 256, BwdSmem<D>::bytes, s>>>(g_read, g_e, m32, codes, ranges, \
+                                                                         offsets, rows, theta, dh, partial); \
+    } while (0)
+    if (d == 128) {
+        switch (bits) { case 1: KGQ_BWD(128, 1); break; case 2: KGQ_BWD(128, 2); break;
+                        case 4: KGQ_BWD(128, 4); break; default: KGQ_BWD(128, 8); break; }
+    } else if (d == 64) {
         switch (bits) { case 1: KGQ_BWD(64, 1); break; case 2: KGQ_BWD(64, 2); break;
                         case 4: KGQ_BWD(64, 4); break; default: KGQ_BWD(64, 8); break; }
     } else {

@@ -124,11 +124,11 @@ def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.
     """Fused layer backward (tape.py:217-225): returns (dtheta, dh) for
     g_j = (g_read + g_e) * mask, dh = g_j theta^T, dtheta = Hhat^T g_j, with
     the dequantized H never materialized.  Falls back to the separate ops for
-    d not in (32, 64) or pass-through contexts."""
+    d not in (32, 64, 128) or pass-through contexts."""
     from .tensorops import mask_apply, mm_theta
     src = g_read if g_read is not None else g_e
     d = src.shape[1]
-    if q.bits == PASSTHROUGH_BITS or d not in (32, 64) or q.group_size != d:
+    if q.bits == PASSTHROUGH_BITS or d not in (32, 64, 128) or q.group_size != d:
         g = g_read if g_e is None else (g_e if g_read is None else g_read + g_e)
         g_j = mask_apply(g, mask)
         return dequant_gemm_tn(q, g_j), mm_theta(g_j, theta, transpose=True)

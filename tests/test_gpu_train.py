@@ -326,7 +326,7 @@ def test_cuda_graph_epoch_equals_eager_epoch():
                                rtol=1e-3, atol=1e-5)
 
 
-@pytest.mark.parametrize("d", [32, 64])
+@pytest.mark.parametrize("d", [32, 64, 128])
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
 @pytest.mark.parametrize("terms", ["both", "read", "e"])
 def test_fused_layer_backward_matches_fp64(d, bits, terms):
