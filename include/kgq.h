@@ -196,6 +196,17 @@ KGQ_API int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices,
                           const uint64_t *tid_base, int64_t row_offset, uint8_t *codes, float *ranges, float *offsets, float *e_next,
                           uint8_t *mask, float *h_out, void *stream);
 
+/* Split layer forward, part 2: the epilogue of kgq_layer_forward_f32 on an H
+ * already produced by kgq_spmm_csr_f32 (rows in natural order):
+ *   ctx = quantize(H) (group = d); J = H @ theta; E_next = relu(J); mask.
+ * Bit-identical to the fused kernel (same lanes, noise calls, FFMA order);
+ * spmm + epilogue keeps the gather kernel at full occupancy, which is faster
+ * when H is L2-resident.  d in {32, 64, 128}. */
+KGQ_API int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d, const float *theta,
+                           int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                           const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
+                           float *ranges, float *offsets, float *e_next, uint8_t *mask, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -375,6 +375,85 @@ __device__ __forceinline__ void heavy_layer_row(const int32_t *__restrict__ indp
     }
 }
 
+// Epilogue of the light path for the warp's RPW rows (slots base..base+RPW-1
+// of the schedule): quantize H (group = the row), J = H . theta (ascending k,
+// FFMA), E' = relu(J), mask words.  Shared by the fused layer kernel (H from
+// the SpMM registers) and the split epilogue kernel (H loaded from memory).
+template <int D, int BITS, int MODE>
+__device__ __forceinline__ void light_epilogue(const float4 (&h)[2], bool active, int64_t row,
+                                               int64_t base, int64_t n_light,
+                                               const int32_t *__restrict__ row_order, int64_t n_heavy,
+                                               const float *th, float *hst, const FastKey &fk,
+                                               uint64_t seed, uint64_t tid, int64_t row_offset,
+                                               uint8_t *__restrict__ codes, float *__restrict__ ranges,
+                                               float *__restrict__ offsets, float *__restrict__ e_next,
+                                               uint32_t *__restrict__ mask) {
+    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % LPR, grp = lane / LPR;
+    const int p = gl >> 2, q = gl & 3;
+    const int f0 = 8 * p + q;
+    light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
+                                      ranges, offsets);
+        // ---- J = H . theta (ascending k, FFMA) ----
+        // The warp's RPW rows are staged k-major in smem (hs[k][RPW]); lane l
+        // then computes columns l + 32c of all RPW rows: per k one broadcast
+        // LDS of H[.][k], D/32 conflict-free LDS of theta[k][.], 8 FFMA.
+        {
+            float *hs = hst + (threadIdx.x >> 5) * (D * RPW);
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                const int k0 = 4 * (f0 + 4 * hh);
+                hs[(k0 + 0) * RPW + grp] = hh ? h[1].x : h[0].x;
+                hs[(k0 + 1) * RPW + grp] = hh ? h[1].y : h[0].y;
+                hs[(k0 + 2) * RPW + grp] = hh ? h[1].z : h[0].z;
+                hs[(k0 + 3) * RPW + grp] = hh ? h[1].w : h[0].w;
+            }
+            __syncwarp();
+            constexpr int NCB = D / 32;
+            float jacc[RPW][NCB];
+#pragma unroll
+            for (int rr = 0; rr < RPW; rr++)
+#pragma unroll
+                for (int c = 0; c < NCB; c++) jacc[rr][c] = 0.0f;
+#pragma unroll 8
+            for (int k = 0; k < D; k++) {
+                float hk[RPW];
+                if (RPW == 4) {
+                    const float4 v4 = *reinterpret_cast<const float4 *>(hs + k * RPW);
+                    hk[0] = v4.x; hk[1] = v4.y; hk[2] = v4.z; hk[3] = v4.w;
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < RPW; rr++) hk[rr] = hs[k * RPW + rr];
+                }
+#pragma unroll
+                for (int c = 0; c < NCB; c++) {
+                    const float tk = th[k * D + lane + 32 * c];
+#pragma unroll
+                    for (int rr = 0; rr < RPW; rr++) jacc[rr][c] = __fmaf_rn(hk[rr], tk, jacc[rr][c]);
+                }
+            }
+            // ---- relu + mask: ballot over lanes gives mask word c of row rr ----
+            const int64_t base_slot = base;
+#pragma unroll
+            for (int rr = 0; rr < RPW; rr++) {
+                const int64_t sl = base_slot + rr;
+                const bool act = sl < n_light;
+                const int64_t rrow = act ? (row_order ? (int64_t)__ldg(row_order + n_heavy + sl) : sl) : 0;
+#pragma unroll
+                for (int c = 0; c < NCB; c++) {
+                    const float jv = jacc[rr][c];
+                    const uint32_t bal = __ballot_sync(0xffffffffu, jv > 0.0f);
+                    if (act) {
+                        e_next[rrow * D + lane + 32 * c] = jv > 0.0f ? jv : 0.0f;
+                        if (lane == 0) mask[rrow * (D / 32) + c] = bal;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+}
+
 // ---------------------------------------------------------------------------
 // Fused layer forward: H = A_hat.E (bit-exact), quantize H on chip (group =
 // d; the same arithmetic and noise as kgq_quantize_f32), J = H.theta (theta
@@ -434,65 +513,48 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
             o[f0] = h[0];
             o[f0 + 4] = h[1];
         }
-        light_row_quantize<D, BITS, MODE>(h, active, row, gl, fk, seed, tid, row_offset, codes,
-                                          ranges, offsets);
-        // ---- J = H . theta (ascending k, FFMA) ----
-        // The warp's RPW rows are staged k-major in smem (hs[k][RPW]); lane l
-        // then computes columns l + 32c of all RPW rows: per k one broadcast
-        // LDS of H[.][k], D/32 conflict-free LDS of theta[k][.], 8 FFMA.
-        {
-            float *hs = hst + (threadIdx.x >> 5) * (D * RPW);
-#pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-                const int k0 = 4 * (f0 + 4 * hh);
-                hs[(k0 + 0) * RPW + grp] = hh ? h[1].x : h[0].x;
-                hs[(k0 + 1) * RPW + grp] = hh ? h[1].y : h[0].y;
-                hs[(k0 + 2) * RPW + grp] = hh ? h[1].z : h[0].z;
-                hs[(k0 + 3) * RPW + grp] = hh ? h[1].w : h[0].w;
-            }
-            __syncwarp();
-            constexpr int NCB = D / 32;
-            float jacc[RPW][NCB];
-#pragma unroll
-            for (int rr = 0; rr < RPW; rr++)
-#pragma unroll
-                for (int c = 0; c < NCB; c++) jacc[rr][c] = 0.0f;
-#pragma unroll 8
-            for (int k = 0; k < D; k++) {
-                float hk[RPW];
-                if (RPW == 4) {
-                    const float4 v4 = *reinterpret_cast<const float4 *>(hs + k * RPW);
-                    hk[0] = v4.x; hk[1] = v4.y; hk[2] = v4.z; hk[3] = v4.w;
-                } else {
-#pragma unroll
-                    for (int rr = 0; rr < RPW; rr++) hk[rr] = hs[k * RPW + rr];
-                }
-#pragma unroll
-                for (int c = 0; c < NCB; c++) {
-                    const float tk = th[k * D + lane + 32 * c];
-#pragma unroll
-                    for (int rr = 0; rr < RPW; rr++) jacc[rr][c] = __fmaf_rn(hk[rr], tk, jacc[rr][c]);
-                }
-            }
-            // ---- relu + mask: ballot over lanes gives mask word c of row rr ----
-            const int64_t base_slot = base;
-#pragma unroll
-            for (int rr = 0; rr < RPW; rr++) {
-                const int64_t sl = base_slot + rr;
-                const bool act = sl < n_light;
-                const int64_t rrow = act ? (row_order ? (int64_t)__ldg(row_order + n_heavy + sl) : sl) : 0;
-#pragma unroll
-                for (int c = 0; c < NCB; c++) {
-                    const float jv = jacc[rr][c];
-                    const uint32_t bal = __ballot_sync(0xffffffffu, jv > 0.0f);
-                    if (act) {
-                        e_next[rrow * D + lane + 32 * c] = jv > 0.0f ? jv : 0.0f;
-                        if (lane == 0) mask[rrow * (D / 32) + c] = bal;
-                    }
-                }
-            }
-            __syncwarp();
+        light_epilogue<D, BITS, MODE>(h, active, row, base, n_light, row_order, n_heavy, th, hst, fk, seed,
+                                      tid, row_offset, codes, ranges, offsets, e_next, mask);
+    }
+}
+
+// Split layer forward, part 2 (after spmm_kernel wrote H): the same light
+// epilogue over rows in natural order, H read from memory.  Bit-identical to
+// the fused kernel (same lane layout, noise calls, FFMA order).
+template <int D, int BITS, int MODE>
+__global__ void __launch_bounds__(256)
+layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
+                      uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
+                      int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
+                      float *__restrict__ offsets, float *__restrict__ e_next,
+                      uint32_t *__restrict__ mask) {
+    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
+    extern __shared__ __align__(16) float th[];     // [D][D], dynamic (64 KB at d = 128)
+    __shared__ __align__(16) float hst[8 * 256];
+    for (int i = threadIdx.x; i < D * D / 4; i += blockDim.x)
+        reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
+    __syncthreads();
+    if (tid_base) tid += __ldg(tid_base);
+    const FastKey fk = make_fast_key(seed, tid);
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % LPR, grp = lane / LPR;
+    const int f0 = 8 * (gl >> 2) + (gl & 3);
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t base = warp * RPW; base < n_rows; base += nw * RPW) {
+        const int64_t row = base + grp;
+        const bool active = row < n_rows;
+        float4 h[2];
+        if (active) {
+            const float4 *src = reinterpret_cast<const float4 *>(hin + row * D);
+            h[0] = __ldg(src + f0);
+            h[1] = __ldg(src + f0 + 4);
+        } else {
+            h[0] = h[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        light_epilogue<D, BITS, MODE>(h, active, active ? row : 0, base, n_rows, nullptr, 0, th,
+                                      hst, fk, seed, tid, row_offset,
+                                      codes, ranges, offsets, e_next, mask);
     }
 }
 
@@ -583,6 +645,36 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
     return KGQ_OK;
 }
 
+template <int D, int BITS>
+static int launch_epilogue(int rounding, const float *h, int64_t n_rows, const float *theta,
+                           uint64_t seed, uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
+                           uint8_t *codes, float *ranges, float *offsets, float *e_next,
+                           uint32_t *mask, cudaStream_t s) {
+    const size_t smem = (size_t)D * D * sizeof(float);
+    void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
+                 uint8_t *, float *, float *, float *, uint32_t *);
+    switch (rounding) {
+        case KGQ_ROUND_NEAREST: kern = layer_epilogue_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
+        case KGQ_ROUND_SR_FAST: kern = layer_epilogue_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
+        case KGQ_ROUND_SR_COMPAT: kern = layer_epilogue_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
+        default: return KGQ_ERR_INVALID_ARG;
+    }
+    static bool smem_set[3] = {false, false, false};
+    if (!smem_set[rounding]) {
+        cudaError_t ea = ensure_smem(kern, smem);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set[rounding] = true;
+    }
+    const int64_t warps = (n_rows + RG<D>::RPW - 1) / RG<D>::RPW;
+    int64_t grid = (warps + 7) / 8;
+    const int64_t cap = (int64_t)kSMs * 8;
+    if (grid > cap) grid = cap;
+    kern<<<(int)grid, 256, smem, s>>>(h, n_rows, theta, seed, tid, tid_base, row_offset, codes, ranges,
+                                      offsets, e_next, mask);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
 template <int D>
 static int launch_layer_bits(int bits, int rounding, const int32_t *indptr, const int32_t *indices,
                              const float *vals, int64_t n_rows, const int32_t *row_order,
@@ -629,5 +721,33 @@ extern "C" int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indic
         case 64: return launch_layer_bits<64>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, tid_base, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
         case 128: return launch_layer_bits<128>(bits, rounding, indptr, indices, vals, n_rows, row_order, n_heavy, e, theta, seed, tensor_id, tid_base, row_offset, codes, ranges, offsets, e_next, m32, h_out, s);
     }
+    return KGQ_ERR_INVALID_ARG;
+}
+
+extern "C" int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d, const float *theta,
+                                      int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
+                                      const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
+                                      float *ranges, float *offsets, float *e_next, uint8_t *mask,
+                                      void *stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (n_rows < 0 || row_offset < 0 || rounding < 0 || rounding > 2) return KGQ_ERR_INVALID_ARG;
+    if (n_rows == 0) return KGQ_OK;
+    if (!h || !theta || !codes || !ranges || !offsets || !e_next || !mask) return KGQ_ERR_INVALID_ARG;
+    if (((uintptr_t)mask & 3u) || ((uintptr_t)codes & 3u) || ((uintptr_t)h & 15u) ||
+        ((uintptr_t)e_next & 15u) || ((uintptr_t)theta & 15u))
+        return KGQ_ERR_MISALIGNED;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *m32 = reinterpret_cast<uint32_t *>(mask);
+#define KGQ_EPI(D, B) launch_epilogue<D, B>(rounding, h, n_rows, theta, seed, tensor_id, tid_base, row_offset, \
+                                            codes, ranges, offsets, e_next, m32, s)
+#define KGQ_EPI_BITS(D) switch (bits) { case 1: return KGQ_EPI(D, 1); case 2: return KGQ_EPI(D, 2); \
+                                        case 4: return KGQ_EPI(D, 4); default: return KGQ_EPI(D, 8); }
+    switch (d) {
+        case 32: KGQ_EPI_BITS(32)
+        case 64: KGQ_EPI_BITS(64)
+        case 128: KGQ_EPI_BITS(128)
+    }
+#undef KGQ_EPI_BITS
+#undef KGQ_EPI
     return KGQ_ERR_INVALID_ARG;
 }

@@ -11,6 +11,7 @@ Each op is one (or two) libkgq launches on the current CUDA stream:
   :233-244) on torch ops in the reference's op order.
 """
 
+import os
 import torch
 
 from . import _lib
@@ -25,11 +26,23 @@ def can_fuse(cfg: QuantConfig, d: int) -> bool:
     return (not cfg.passthrough) and d in FUSED_DIMS and (cfg.group is None or cfg.group == d)
 
 
+# None = by width: split for d <= 64 (Amazon shape, ncu: fused 265 us vs spmm
+# 158 us + epilogue 61 us per layer), fused for d = 128 (industry shard: fused
+# 356 vs split 377 ms/step).  KGQ_SPLIT_LAYER=0/1 forces one path.
+_env_split = os.environ.get("KGQ_SPLIT_LAYER")
+SPLIT_LAYER_DEFAULT = None if _env_split is None else _env_split == "1"
+
+
 def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
                        stream: RandomStream | None, tensor_id: int | None = None,
-                       row_offset: int = 0, want_h: bool = False):
+                       row_offset: int = 0, want_h: bool = False, split: bool | None = None):
     """One fused layer.  Returns (e_next, mask, q, h) where q is the quantized
     H context (per-row groups) and h is H only if ``want_h``.
+
+    ``split``: run it as spmm_kernel (H to a scratch buffer) + the epilogue
+    kernel instead of the single fused kernel; bit-identical results.  None
+    = ``SPLIT_LAYER_DEFAULT`` (by width; the split path is faster on B200 at
+    d <= 64, where the gather kernel alone keeps full occupancy).
 
     ``adj`` may be a row block of the global adjacency (rows ``row_offset``..)
     with global column ids; ``e`` then holds all the rows it references.
@@ -53,7 +66,22 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     offsets = torch.empty(n_rows, dtype=torch.float32, device=dev)
     e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
-    h = torch.empty((n_rows, d), dtype=torch.float32, device=dev) if want_h else None
+    if split is None:
+        split = SPLIT_LAYER_DEFAULT if SPLIT_LAYER_DEFAULT is not None else d <= 64
+    h = torch.empty((n_rows, d), dtype=torch.float32, device=dev) if (want_h or split) else None
+    if split:
+        L = _lib.load()
+        st = L.kgq_spmm_csr_f32(adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows,
+                                *adj.schedule(), e.data_ptr(), d, h.data_ptr(), _lib.stream_ptr(dev))
+        _lib.check(st, "kgq_spmm_csr_f32")
+        st = L.kgq_layer_epilogue_f32(
+            h.data_ptr(), n_rows, d, theta.data_ptr(), cfg.bits, cfg.mode, seed,
+            int(tensor_id) & 0xFFFFFFFFFFFFFFFF, stream.tid_base_ptr() if stream is not None else None,
+            row_offset, codes.data_ptr(), ranges.data_ptr(), offsets.data_ptr(), e_next.data_ptr(),
+            mask.data_ptr(), _lib.stream_ptr(dev))
+        _lib.check(st, "kgq_layer_epilogue_f32")
+        q = QuantizedTensor(n_rows, d, cfg.bits, codes, ranges, offsets)
+        return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, (h if want_h else None)
     st = _lib.load().kgq_layer_forward_f32(
         adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows,
         *adj.schedule(), e.data_ptr(), d,

@@ -156,6 +156,33 @@ def test_fused_layer_matches_unfused_and_oracle():
                 assert np.array_equal(m1.packed.cpu().numpy(), r_mask)
 
 
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_split_layer_bit_identical_to_fused(d):
+    """spmm_kernel + layer_epilogue_kernel (kgq_layer_epilogue_f32) produce the
+    same bytes as the single fused kernel: E_next, codes, ranges, offsets,
+    mask, at every bit width and rounding mode, with hub (CTA-path) rows and
+    a row offset."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(d)
+    n = 3000
+    a = _hub_graph(n, d)
+    A = kgq.CSR.from_scipy(a)
+    e = torch.from_numpy(rng.standard_normal((n, d), dtype=np.float32)).cuda()
+    th = torch.from_numpy((rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
+    for bits in (1, 2, 4, 8):
+        for rng_mode, rounding in (("fast", "stochastic"), ("compat", "stochastic"), ("fast", "nearest")):
+            cfg = kgq.QuantConfig(bits=bits, rounding=rounding, rng=rng_mode)
+            outs = [F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(5), 3, row_offset=17, split=sp)
+                    for sp in (False, True)]
+            (e0, m0, q0, _), (e1, m1, q1, _) = outs
+            assert torch.equal(e0.view(torch.int32), e1.view(torch.int32)), (bits, rounding, rng_mode)
+            assert torch.equal(q0.codes, q1.codes)
+            assert torch.equal(q0.ranges.view(torch.int32), q1.ranges.view(torch.int32))
+            assert torch.equal(q0.offsets.view(torch.int32), q1.offsets.view(torch.int32))
+            assert torch.equal(m0.packed, m1.packed)
+
+
 def test_dequant_gemm_matches_dequantize_then_matmul():
     kgq = _kgq()
     from paper_2212_04540_b200 import functional as F
