@@ -44,7 +44,22 @@ struct RG {
 // together; the nonzero loop runs to the warp's longest row with per-row
 // predicates so shuffles stay convergent).
 // ---------------------------------------------------------------------------
-template <int D>
+// Feature layout of the two float4 a lane owns:
+//  NOISE_LAYOUT (fused layer): float4 f0 = 8(gl>>2) + (gl&3) and f0 + 4, so a
+//    lane's 8 features are one fast-noise call;
+//  contiguous (plain SpMM): float4 gl and gl + LPR, so each warp-wide load
+//    touches whole 128-byte lines of every row (half the L1 tag lookups of
+//    the noise layout, whose two loads each touch half of the same lines).
+template <int D, bool NOISE_LAYOUT>
+__device__ __forceinline__ int rg_f4a(int gl) {
+    return NOISE_LAYOUT ? 8 * (gl >> 2) + (gl & 3) : gl;
+}
+template <int D, bool NOISE_LAYOUT>
+__device__ __forceinline__ int rg_f4b(int gl) {
+    return NOISE_LAYOUT ? 8 * (gl >> 2) + (gl & 3) + 4 : gl + RG<D>::LPR;
+}
+
+template <int D, bool NOISE_LAYOUT = true>
 __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
                                             const int32_t *__restrict__ indices,
                                             const float *__restrict__ vals,
@@ -61,7 +76,7 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
     int maxlen = len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-    const int f0 = 8 * (gl >> 2) + (gl & 3);
+    const int fa = rg_f4a<D, NOISE_LAYOUT>(gl), fb = rg_f4b<D, NOISE_LAYOUT>(gl);
     int32_t nx_col = 0;
     float nx_val = 0.0f;
     if (gl < len) {
@@ -86,8 +101,8 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
                 av[u] = __shfl_sync(0xffffffffu, my_val, t + u, LPR);
                 if (t + u < cnt) {
                     const float4 *xr = reinterpret_cast<const float4 *>(x + (int64_t)col * D);
-                    xa[u] = __ldg(xr + f0);
-                    xb[u] = __ldg(xr + f0 + 4);
+                    xa[u] = __ldg(xr + fa);
+                    xb[u] = __ldg(xr + fb);
                 }
             }
 #pragma unroll
@@ -173,8 +188,11 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
     return acc;
 }
 
+#ifndef KGQ_SPMM_MINB
+#define KGQ_SPMM_MINB 4     // 4 CTAs/SM (<= 64 registers): the gather is latency-bound
+#endif
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, KGQ_SPMM_MINB)
 spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
             const float *__restrict__ vals, int64_t n_rows, const int32_t *__restrict__ row_order,
             int64_t n_heavy, const float *__restrict__ x, float *__restrict__ out) {
@@ -193,17 +211,17 @@ spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indi
     const int64_t warp = lb * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nw = nlb * (blockDim.x >> 5);
     const int64_t n_light = n_rows - n_heavy;
-    const int f0 = 8 * (gl >> 2) + (gl & 3);
+    const int fa = rg_f4a<D, false>(gl), fb = rg_f4b<D, false>(gl);
     for (int64_t base = warp * RPW; base < n_light; base += nw * RPW) {
         const int64_t slot = base + grp;
         const bool active = slot < n_light;
         const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
         float4 acc[2];
-        rg_spmm_row<D>(indptr, indices, vals, x, row, active, gl, acc);
+        rg_spmm_row<D, false>(indptr, indices, vals, x, row, active, gl, acc);
         if (active) {
             float4 *o = reinterpret_cast<float4 *>(out + row * D);
-            o[f0] = acc[0];
-            o[f0 + 4] = acc[1];
+            o[fa] = acc[0];
+            o[fb] = acc[1];
         }
     }
 }
@@ -518,9 +536,26 @@ layer_forward_kernel(const int32_t *__restrict__ indptr, const int32_t *__restri
     }
 }
 
-// Split layer forward, part 2 (after spmm_kernel wrote H): the same light
-// epilogue over rows in natural order, H read from memory.  Bit-identical to
-// the fused kernel (same lane layout, noise calls, FFMA order).
+// Split layer forward, part 2 (after spmm_kernel wrote H).  Tiles of
+// ROWS = 4096/d rows per CTA:
+//  1. each warp loads RPW rows at a time in the fused kernel's lane layout
+//     (LPR = d/8 lanes per row, a lane's 8 features = one fast-noise call) and
+//     quantizes them with the same code (light_row_quantize), then stages H
+//     k-major in smem;
+//  2. J = H.theta as a register-blocked FFMA GEMM: thread (tr, tc) owns rows
+//     4tr..4tr+3 x columns 4tc..4tc+3, per k one LDS.128 of H and one of theta
+//     for 16 FFMA; every J element is the same ascending-k fmaf chain from 0
+//     as in the fused kernel, so E_next and the mask are bit-identical;
+//  3. relu, float4 stores, mask words from 8-lane nibble ORs.
+template <int D>
+struct EpiTile {
+    static constexpr int ROWS = 4096 / D;    // 128 / 64 / 32 rows for d = 32 / 64 / 128
+    static constexpr int TC = D / 4;         // column groups
+    static constexpr int TR = 256 / TC;      // row groups (= ROWS / 4)
+    static constexpr int RS = ROWS + 4;      // padded k-major row stride
+    static constexpr size_t smem = ((size_t)D * D + (size_t)D * RS) * sizeof(float);
+};
+
 template <int D, int BITS, int MODE>
 __global__ void __launch_bounds__(256)
 layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
@@ -528,33 +563,83 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
                       int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
                       float *__restrict__ offsets, float *__restrict__ e_next,
                       uint32_t *__restrict__ mask) {
-    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
-    extern __shared__ __align__(16) float th[];     // [D][D], dynamic (64 KB at d = 128)
-    __shared__ __align__(16) float hst[8 * 256];
+    using ET = EpiTile<D>;
+    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW, ROWS = ET::ROWS, RS = ET::RS, TC = ET::TC;
+    static_assert(ET::TR * 4 == ROWS, "tile geometry");
+    extern __shared__ __align__(16) float epi_smem[];
+    float *th = epi_smem;                    // [D][D]
+    float *hs = epi_smem + D * D;            // [D][RS], k-major
     for (int i = threadIdx.x; i < D * D / 4; i += blockDim.x)
         reinterpret_cast<float4 *>(th)[i] = __ldg(reinterpret_cast<const float4 *>(theta) + i);
-    __syncthreads();
     if (tid_base) tid += __ldg(tid_base);
     const FastKey fk = make_fast_key(seed, tid);
-    const int lane = threadIdx.x & 31;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int gl = lane % LPR, grp = lane / LPR;
-    const int f0 = 8 * (gl >> 2) + (gl & 3);
-    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t base = warp * RPW; base < n_rows; base += nw * RPW) {
-        const int64_t row = base + grp;
-        const bool active = row < n_rows;
-        float4 h[2];
-        if (active) {
-            const float4 *src = reinterpret_cast<const float4 *>(hin + row * D);
-            h[0] = __ldg(src + f0);
-            h[1] = __ldg(src + f0 + 4);
-        } else {
-            h[0] = h[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int fa = rg_f4a<D, true>(gl), fb = rg_f4b<D, true>(gl);
+    const int tc = t % TC, tr = t / TC;
+    const int64_t n_tiles = (n_rows + ROWS - 1) / ROWS;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * ROWS;
+        // ---- 1. load + quantize + stage (ROWS / (8 * RPW) = 2 passes) ----
+#pragma unroll
+        for (int pass = 0; pass < ROWS / (8 * RPW); pass++) {
+            const int lr = (pass * 8 + warp) * RPW + grp;
+            const int64_t row = r0 + lr;
+            const bool active = row < n_rows;
+            float4 h[2];
+            if (active) {
+                const float4 *src = reinterpret_cast<const float4 *>(hin + row * D);
+                h[0] = __ldg(src + fa);
+                h[1] = __ldg(src + fb);
+            } else {
+                h[0] = h[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            light_row_quantize<D, BITS, MODE>(h, active, active ? row : 0, gl, fk, seed, tid, row_offset,
+                                              codes, ranges, offsets);
+            const float hv[8] = {h[0].x, h[0].y, h[0].z, h[0].w, h[1].x, h[1].y, h[1].z, h[1].w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                hs[(4 * fa + e) * RS + lr] = hv[e];
+                hs[(4 * fb + e) * RS + lr] = hv[4 + e];
+            }
         }
-        light_epilogue<D, BITS, MODE>(h, active, active ? row : 0, base, n_rows, nullptr, 0, th,
-                                      hst, fk, seed, tid, row_offset,
-                                      codes, ranges, offsets, e_next, mask);
+        __syncthreads();
+        // ---- 2. J tile = H . theta, ascending k ----
+        float acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+#pragma unroll 8
+        for (int k = 0; k < D; k++) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(hs + k * RS + 4 * tr);
+            const float4 b4 = *reinterpret_cast<const float4 *>(th + k * D + 4 * tc);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+            const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+        }
+        // ---- 3. relu, E_next, mask (columns 32c..32c+31 = lanes with tc in [8c, 8c+8)) ----
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int64_t row = r0 + 4 * tr + i;
+            uint32_t nib = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) nib |= (acc[i][j] > 0.0f ? 1u : 0u) << j;
+            uint32_t word = nib << (4 * (tc & 7));
+            word |= __shfl_xor_sync(0xffffffffu, word, 1);
+            word |= __shfl_xor_sync(0xffffffffu, word, 2);
+            word |= __shfl_xor_sync(0xffffffffu, word, 4);
+            if (row < n_rows) {
+                *reinterpret_cast<float4 *>(e_next + row * D + 4 * tc) =
+                    make_float4(acc[i][0] > 0.0f ? acc[i][0] : 0.0f, acc[i][1] > 0.0f ? acc[i][1] : 0.0f,
+                                acc[i][2] > 0.0f ? acc[i][2] : 0.0f, acc[i][3] > 0.0f ? acc[i][3] : 0.0f);
+                if ((tc & 7) == 0) mask[row * (D / 32) + (tc >> 3)] = word;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -650,7 +735,7 @@ static int launch_epilogue(int rounding, const float *h, int64_t n_rows, const f
                            uint64_t seed, uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
                            uint8_t *codes, float *ranges, float *offsets, float *e_next,
                            uint32_t *mask, cudaStream_t s) {
-    const size_t smem = (size_t)D * D * sizeof(float);
+    const size_t smem = EpiTile<D>::smem;
     void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
                  uint8_t *, float *, float *, float *, uint32_t *);
     switch (rounding) {
@@ -665,12 +750,11 @@ static int launch_epilogue(int rounding, const float *h, int64_t n_rows, const f
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set[rounding] = true;
     }
-    const int64_t warps = (n_rows + RG<D>::RPW - 1) / RG<D>::RPW;
-    int64_t grid = (warps + 7) / 8;
-    const int64_t cap = (int64_t)kSMs * 8;
-    if (grid > cap) grid = cap;
-    kern<<<(int)grid, 256, smem, s>>>(h, n_rows, theta, seed, tid, tid_base, row_offset, codes, ranges,
-                                      offsets, e_next, mask);
+    const int64_t tiles = (n_rows + EpiTile<D>::ROWS - 1) / EpiTile<D>::ROWS;
+    const int64_t cap = (int64_t)kSMs * (D > 64 ? 2 : 6);
+    const int grid = (int)(tiles < cap ? tiles : cap);
+    kern<<<grid, 256, smem, s>>>(h, n_rows, theta, seed, tid, tid_base, row_offset, codes, ranges,
+                                 offsets, e_next, mask);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

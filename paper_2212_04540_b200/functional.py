@@ -26,9 +26,12 @@ def can_fuse(cfg: QuantConfig, d: int) -> bool:
     return (not cfg.passthrough) and d in FUSED_DIMS and (cfg.group is None or cfg.group == d)
 
 
-# None = by width: split for d <= 64 (Amazon shape, ncu: fused 265 us vs spmm
-# 158 us + epilogue 61 us per layer), fused for d = 128 (industry shard: fused
-# 356 vs split 377 ms/step).  KGQ_SPLIT_LAYER=0/1 forces one path.
+# None = by the size of the gathered table: split while E fits in L2 (Amazon
+# shape d=64: fused 229 us vs split 202 us per layer; d=128: 782 vs 488 us),
+# fused when E streams from HBM (industry shard, 28 GB table: the gather is
+# HBM-latency-bound and hides the epilogue; fused 41 vs split ~48 ms per
+# layer).  KGQ_SPLIT_LAYER=0/1 forces one path.
+SPLIT_L2_BYTES = 96 << 20
 _env_split = os.environ.get("KGQ_SPLIT_LAYER")
 SPLIT_LAYER_DEFAULT = None if _env_split is None else _env_split == "1"
 
@@ -41,8 +44,8 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
 
     ``split``: run it as spmm_kernel (H to a scratch buffer) + the epilogue
     kernel instead of the single fused kernel; bit-identical results.  None
-    = ``SPLIT_LAYER_DEFAULT`` (by width; the split path is faster on B200 at
-    d <= 64, where the gather kernel alone keeps full occupancy).
+    = ``SPLIT_LAYER_DEFAULT`` (by table size: split while the gathered E is
+    L2-resident, where the gather kernel alone keeps full occupancy).
 
     ``adj`` may be a row block of the global adjacency (rows ``row_offset``..)
     with global column ids; ``e`` then holds all the rows it references.
@@ -67,7 +70,8 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
     if split is None:
-        split = SPLIT_LAYER_DEFAULT if SPLIT_LAYER_DEFAULT is not None else d <= 64
+        split = (SPLIT_LAYER_DEFAULT if SPLIT_LAYER_DEFAULT is not None
+                 else e.numel() * e.element_size() <= SPLIT_L2_BYTES)
     h = torch.empty((n_rows, d), dtype=torch.float32, device=dev) if (want_h or split) else None
     if split:
         L = _lib.load()
