@@ -34,4 +34,8 @@ for d in (64, 128):
     for split in (False, True):
         res[f"layer_d{d}_{'split' if split else 'fused'}_us"] = timeit(
             lambda: F.graph_conv_forward(A, x, th, cfg, st, 1, split=split))
+    # fused layer backward on the same rows
+    e_next, mask, q, _ = F.graph_conv_forward(A, x, th, cfg, st, 1)
+    gr, ge = torch.randn_like(x), torch.randn_like(x)
+    res[f"layer_bwd_d{d}_us"] = timeit(lambda: F.layer_backward(gr, ge, mask, q, th))
 print(json.dumps(res))
