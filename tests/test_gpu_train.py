@@ -378,3 +378,28 @@ def test_fused_layer_backward_matches_fp64(d, bits, terms):
     ref_dth = (hh.t() @ gj).cpu().numpy()
     np.testing.assert_allclose(dh.cpu().numpy(), ref_dh, rtol=1e-4, atol=1e-5)
     np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(rows))
+
+
+@pytest.mark.gpu
+def test_industry_generator_on_device_matches_host_adjacency():
+    """industry.IndustryGraph on cuda at a small shape: degrees and row blocks
+    equal adjacency_arrays (the reference's build_adjacency semantics) of the
+    dataset the same device generator yields."""
+    _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.industry import IndustryGraph, IndustryShape
+    sh = IndustryShape(users=4000, items=1500, entities=12000, relations=9, groups=17,
+                       interactions_per_user=20.0, attr_links_per_item=9.0, user_chunk=900, item_chunk=300)
+    g = IndustryGraph(sh, seed=3, device="cuda")
+    ds = g.dataset()
+    ds.validate()
+    ip, ix, vv = D.adjacency_arrays(ds)
+    deg = g.degrees()
+    assert np.array_equal(np.diff(ip), deg.cpu().numpy())
+    cuts = g.partition(deg, 4)
+    for r in range(4):
+        lo, hi = int(cuts[r]), int(cuts[r + 1])
+        bip, bix, bvv = (t.cpu().numpy() for t in g.row_block(lo, hi, deg))
+        assert np.array_equal(bip, ip[lo:hi + 1] - ip[lo])
+        assert np.array_equal(bix, ix[ip[lo]:ip[hi]])
+        assert np.array_equal(bvv.view(np.uint32), vv[ip[lo]:ip[hi]].view(np.uint32))

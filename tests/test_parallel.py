@@ -165,3 +165,25 @@ def test_padded_cols_layout():
             lo, hi = int(p.cuts[r]), int(p.cuts[r + 1])
             assert np.array_equal(pc[lo:hi], r * p.block + np.arange(hi - lo))
         assert pc.max() < world * p.block
+
+
+def test_simulated_rank_comm_shapes_and_local_rows():
+    """SimulatedRankComm (1-GPU measurement of one rank of a W-way partition)
+    keeps the collective shapes, writes this rank's block where the real
+    collective would, and fills remote rows once (stable across calls)."""
+    from paper_2212_04540_b200.parallel import SimulatedRankComm
+    cuts = np.array([0, 3, 10, 12])
+    comm = SimulatedRankComm(world=3, rank=1)
+    local = torch.arange(14, dtype=torch.float32).reshape(7, 2)
+    full = comm.all_gather_global(local, cuts)
+    assert full.shape == (12, 2) and torch.equal(full[3:10], local)
+    remote = full[:3].clone()
+    full2 = comm.all_gather_global(local + 1, cuts)
+    assert full2.data_ptr() == full.data_ptr() and torch.equal(full2[:3], remote)
+    idx = torch.tensor([4, 0, 9])
+    rows = comm.gather_index_rows(local, 3, idx)
+    assert torch.equal(rows[0], local[1]) and torch.equal(rows[2], local[6])
+    padded = comm.all_gather_padded(local, 7)
+    assert padded.shape == (21, 2) and torch.equal(padded[7:14], local)
+    t = torch.ones(3)
+    assert comm.all_reduce_sum(t) is t
