@@ -205,7 +205,7 @@ def workload_config(args):
                   % (args.rows * args.cols * 4 / 1e9)}
 
 
-def train_bench(args, world, rank):
+def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
     """KGNN training on the Amazon-book-shaped synthetic KG (BASELINE configs[3];
     159,251 nodes, 3 layers, d=64, B=1024) at INT2: ms/step, epochs/s and the
     activation ledger.  world > 1: row-partitioned step (parallel.py, NCCL)."""
@@ -215,19 +215,20 @@ def train_bench(args, world, rank):
     from paper_2212_04540_b200.model import ModelConfig, init_params
     from paper_2212_04540_b200.train import AdamState, TrainConfig, adam_step, memory_report, train_epoch
 
-    if args.train_shape in D.REFERENCE_DATASETS:
-        ds = D.reference_dataset(args.train_shape)
+    shape = shape or args.train_shape
+    if shape in D.REFERENCE_DATASETS:
+        ds = D.reference_dataset(shape)
         origin = "reference generator (synth_generate seed 0, datasets/)"
     else:
-        ds = D.synth_kg(D.SHAPES[args.train_shape], seed=0)
+        ds = D.synth_kg(D.SHAPES[shape], seed=0)
         origin = "vectorized generator"
     steps_per_epoch = (len(ds.train) + 1023) // 1024
-    out = {"workload": f"{args.train_shape}-shaped synthetic KG from the {origin}: {ds.num_users} users, "
+    out = {"workload": f"{shape}-shaped synthetic KG from the {origin}: {ds.num_users} users, "
                        f"{ds.num_items} items, {ds.num_entities} entities, {len(ds.triples)} triples, "
                        f"{len(ds.train)} train pairs; KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
            "steps_per_epoch": steps_per_epoch, "n_gpus": world}
     res = {}
-    for bits in (2, 32):
+    for bits in ((2, 32) if with_fp32 else (2,)):
         q = kgq.QuantConfig(bits=bits)
         mcfg = ModelConfig(layers=3, dim=64, quant=q)
         cfg = TrainConfig(quant=q)
@@ -258,13 +259,12 @@ def train_bench(args, world, rank):
             ms = _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args)
             res[bits] = (ms, None, None)
     ms2, mem2, loss2 = res[2]
-    ms32 = res[32][0]
     out.update({"ms_per_step": round(ms2, 3), "epoch_s": round(ms2 * steps_per_epoch / 1e3, 3),
-                "epochs_per_s": round(1e3 / (ms2 * steps_per_epoch), 4),
-                "fp32_ms_per_step": round(ms32, 3),
-                "int2_time_overhead_vs_fp32": round(ms2 / ms32 - 1.0, 4),
-                "timed_steps": args.train_steps})
-    if world == 1 and rank == 0 and not args.skip_cpu:
+                "epochs_per_s": round(1e3 / (ms2 * steps_per_epoch), 4), "timed_steps": args.train_steps})
+    if with_fp32:
+        ms32 = res[32][0]
+        out.update({"fp32_ms_per_step": round(ms32, 3), "int2_time_overhead_vs_fp32": round(ms2 / ms32 - 1.0, 4)})
+    if world == 1 and rank == 0 and not args.skip_cpu and with_cpu:
         # CPU port of the reference step (oracle/oracle.py dense engine: scipy
         # CSR spmm + numpy GEMMs, the reference's op structure), 2 steps
         from oracle import oracle as orc
@@ -640,6 +640,13 @@ def run_ours(args):
             train = train_bench(args, world, rank)
         except Exception as exc:            # never lose the headline line
             train = {"error": f"{type(exc).__name__}: {exc}"}
+        if world == 1 and args.train_shape == "amazon" and not args.skip_lastfm:
+            torch.cuda.empty_cache()
+            try:      # BASELINE configs[2]: the Last-FM-shaped KG on one B200
+                train["lastfm"] = train_bench(args, world, rank, shape="lastfm", with_fp32=False,
+                                              with_cpu=False)
+            except Exception as exc:
+                train["lastfm"] = {"error": f"{type(exc).__name__}: {exc}"}
         if world == 1 and not args.skip_quality and args.train_shape in ("amazon", "lastfm"):
             torch.cuda.empty_cache()
             try:
@@ -723,6 +730,7 @@ def main():
     ap.add_argument("--skip-compat", action="store_true")
     ap.add_argument("--skip-train", action="store_true")
     ap.add_argument("--skip-quality", action="store_true")
+    ap.add_argument("--skip-lastfm", action="store_true")
     ap.add_argument("--industry", action="store_true", help="configs[4] per-rank shard measurement")
     ap.add_argument("--industry-world", type=int, default=8)
     ap.add_argument("--industry-ranks", default="0")

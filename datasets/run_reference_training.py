@@ -6,6 +6,7 @@ Run in the build container (needs /root/reference; CPU, ~26 min per epoch at
 Amazon shape):
 
     python datasets/run_reference_training.py amazon BITS EPOCHS
+    python datasets/run_reference_training.py amazon --record-json REPORT.json
 
 Merges {"b<BITS>_e<EPOCHS>": {...}} into datasets/<name>_seed0_reference_runs.json.
 Quantization config is passed to both ModelConfig and TrainConfig as the
@@ -19,11 +20,6 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, os.path.dirname(HERE))
-
-from kgact.data import KgDataset  # noqa: E402
-from kgact.model import ModelConfig  # noqa: E402
-from kgact.quantize import QuantConfig  # noqa: E402
-from kgact.train import TrainConfig, train_run  # noqa: E402
 
 from paper_2212_04540_b200 import data as D  # noqa: E402
 
@@ -42,6 +38,10 @@ def record(name, key, rep, wall):
 
 
 def main(name, bits, epochs):
+    from kgact.data import KgDataset
+    from kgact.model import ModelConfig
+    from kgact.quantize import QuantConfig
+    from kgact.train import TrainConfig, train_run
     d = D.reference_dataset(name)
     ds = KgDataset(d.num_users, d.num_items, d.num_entities, d.train, d.val, d.test, d.triples,
                    {f"u{u}": u for u in range(d.num_users)}, {f"e{e}": e for e in range(d.num_entities)},
@@ -54,4 +54,10 @@ def main(name, bits, epochs):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]))
+    if sys.argv[2] == "--record-json":
+        # a train_run report the same code path saved as JSON (long runs were
+        # started detached): python ... amazon --record-json report.json
+        rep = json.load(open(sys.argv[3]))
+        record(sys.argv[1], f"b{rep['config']['bits']}_e{rep['config']['epochs']}", rep, rep.get("wall_s", 0.0))
+    else:
+        main(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]))
