@@ -135,20 +135,26 @@ dequant_gemm_tn_kernel(const uint8_t *__restrict__ codes, const float *__restric
     for (int i = t; i < D * D; i += kGemmThreads) dst[i] = red[i];
 }
 
-// Fixed-order reduction of the per-CTA partials: 8 interleaved running sums
-// (independent loads in flight) combined in a fixed order -> deterministic.
-__global__ void reduce_partials_kernel(const float *__restrict__ partial, int nparts, int dd,
-                                       float *__restrict__ out, int accumulate) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dd; i += gridDim.x * blockDim.x) {
-        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        int p = 0;
-        for (; p + 8 <= nparts; p += 8)
-#pragma unroll
-            for (int u = 0; u < 8; u++) s8[u] = __fadd_rn(s8[u], __ldg(partial + (int64_t)(p + u) * dd + i));
-        for (; p < nparts; p++) s8[p & 7] = __fadd_rn(s8[p & 7], __ldg(partial + (int64_t)p * dd + i));
-        const float s = __fadd_rn(__fadd_rn(__fadd_rn(s8[0], s8[1]), __fadd_rn(s8[2], s8[3])),
-                                  __fadd_rn(__fadd_rn(s8[4], s8[5]), __fadd_rn(s8[6], s8[7])));
-        out[i] = accumulate ? __fadd_rn(out[i], s) : s;
+// Fixed-order reduction of the per-CTA partials: 8 interleaved ascending
+// chains (partials p = u mod 8) combined as ((0+1)+(2+3))+((4+5)+(6+7)) ->
+// deterministic.  A CTA owns 32 consecutive outputs, warp u runs chain u.
+__global__ void __launch_bounds__(256)
+reduce_partials_kernel(const float *__restrict__ partial, int nparts, int dd,
+                       float *__restrict__ out, int accumulate) {
+    __shared__ float s8[8][32];
+    const int c = threadIdx.x & 31, u = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + c;
+    float acc = 0.0f;
+    if (i < dd) {
+#pragma unroll 4
+        for (int p = u; p < nparts; p += 8) acc = __fadd_rn(acc, __ldg(partial + (int64_t)p * dd + i));
+    }
+    s8[u][c] = acc;
+    __syncthreads();
+    if (u == 0 && i < dd) {
+        const float sum = __fadd_rn(__fadd_rn(__fadd_rn(s8[0][c], s8[1][c]), __fadd_rn(s8[2][c], s8[3][c])),
+                                    __fadd_rn(__fadd_rn(s8[4][c], s8[5][c]), __fadd_rn(s8[6][c], s8[7][c])));
+        out[i] = accumulate ? __fadd_rn(out[i], sum) : sum;
     }
 }
 
@@ -235,7 +241,7 @@ extern "C" int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges
         }
         if (st != KGQ_OK) return st;
         const int dd = d * d;
-        reduce_partials_kernel<<<(dd + 127) / 128, 128, 0, s>>>(partial, dq_gemm_grid(rows), dd,
+        reduce_partials_kernel<<<(dd + 31) / 32, 256, 0, s>>>(partial, dq_gemm_grid(rows), dd,
                                                                 dtheta, accumulate);
     } else {
         dequant_gemm_generic_kernel<<<(d * d + 255) / 256, 256, 0, s>>>(
