@@ -207,6 +207,19 @@ KGQ_API int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d, co
                            const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
                            float *ranges, float *offsets, float *e_next, uint8_t *mask, void *stream);
 
+/* BPR + L2 head forward (tape.py:154-170): margins[r] = sum_k u*(p-n);
+ * loss[0] = mean logaddexp(0, -margins) + (l2 * (|u|^2+|p|^2+|n|^2)) / batch,
+ * one CTA, fixed reduction order.  u, p, n: batch x d fp32 row-major. */
+KGQ_API int kgq_bpr_forward_f32(const float *u, const float *p, const float *n, int64_t batch, int32_t d,
+                        float l2, float *margins, float *loss, void *stream);
+
+/* BPR head backward (tape.py:233-244) against the dequantized blocks:
+ * coef = sigmoid(-m)/batch; gu = g*(-coef*(ph-nh) + reg*uh); gp = g*(-coef*uh
+ * + reg*ph); gn = g*(coef*uh + reg*nh); g is a device scalar, reg = fp32(2*l2/batch). */
+KGQ_API int kgq_bpr_backward_f32(const float *g, const float *margins, const float *uh, const float *ph,
+                         const float *nh, int64_t batch, int32_t d, float reg, float *gu,
+                         float *gp, float *gn, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,112 @@
+// kgq_bpr.cu -- the BPR + L2 head of a training step (tape.py:154-183 forward,
+// tape.py:233-244 backward) as two kernels instead of ~30 framework launches.
+//
+// Forward (one CTA): margins[r] = sum_k u[r,k] * (p[r,k] - n[r,k]);
+//   loss = mean_r logaddexp(0, -margins[r]) + (l2 * (|u|^2 + |p|^2 + |n|^2)) / B
+// in fp32 with a fixed reduction tree (deterministic; the reference's numpy
+// pairwise sums differ from any GPU order in the last bits -> tolerance).
+// Backward (elementwise): with coef = sigmoid(-m)/B and reg = fp32(2*l2/B),
+//   gu = g * (-coef * (ph - nh) + reg * uh)
+//   gp = g * (-coef * uh + reg * ph)
+//   gn = g * ( coef * uh + reg * nh)
+// against the dequantized blocks, each product / sum rounded separately in
+// the reference's evaluation order (no FMA contraction).
+#include "kgq_common.cuh"
+
+namespace kgq {
+
+constexpr int kBprThreads = 1024;
+
+__global__ void __launch_bounds__(kBprThreads)
+bpr_forward_kernel(const float *__restrict__ u, const float *__restrict__ p, const float *__restrict__ n,
+                   int64_t batch, int d, float l2, float *__restrict__ margins, float *__restrict__ loss) {
+    __shared__ float s_sp[32], s_rg[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float sp = 0.0f, rg = 0.0f;                  // per-warp running sums (lane 0)
+    for (int64_t r = warp; r < batch; r += kBprThreads / 32) {
+        float m = 0.0f, q = 0.0f;
+        for (int k = lane; k < d; k += 32) {
+            const float uv = __ldg(u + r * d + k), pv = __ldg(p + r * d + k), nv = __ldg(n + r * d + k);
+            m = __fadd_rn(m, __fmul_rn(uv, __fsub_rn(pv, nv)));
+            q = __fadd_rn(q, __fadd_rn(__fadd_rn(__fmul_rn(uv, uv), __fmul_rn(pv, pv)), __fmul_rn(nv, nv)));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m = __fadd_rn(m, __shfl_xor_sync(0xffffffffu, m, o));
+            q = __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
+        }
+        if (lane == 0) {
+            margins[r] = m;
+            // logaddexp(0, -m) = max(0, -m) + log1p(exp(-|m|))
+            const float x = -m;
+            sp = __fadd_rn(sp, __fadd_rn(fmaxf(x, 0.0f), log1pf(expf(-fabsf(x)))));
+            rg = __fadd_rn(rg, q);
+        }
+    }
+    if (lane == 0) {
+        s_sp[warp] = sp;
+        s_rg[warp] = rg;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        float a = s_sp[lane], b = s_rg[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) {
+            const float fb = (float)batch;
+            const float data = __fdiv_rn(a, fb);
+            const float reg = __fdiv_rn(__fmul_rn(l2, b), fb);
+            *loss = __fadd_rn(data, reg);
+        }
+    }
+}
+
+__global__ void bpr_backward_kernel(const float *__restrict__ g, const float *__restrict__ margins,
+                                    const float *__restrict__ uh, const float *__restrict__ ph,
+                                    const float *__restrict__ nh, int64_t batch, int d, float reg,
+                                    float *__restrict__ gu, float *__restrict__ gp, float *__restrict__ gn) {
+    const int64_t total = batch * d;
+    const float gg = __ldg(g);
+    const float fb = (float)batch;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d;
+        const float m = __ldg(margins + r);
+        const float sg = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(m)));      // sigmoid(-m)
+        const float coef = __fdiv_rn(sg, fb);
+        const float u = __ldg(uh + i), pv = __ldg(ph + i), nv = __ldg(nh + i);
+        const float ru = __fmul_rn(reg, u);
+        gu[i] = __fmul_rn(gg, __fadd_rn(__fmul_rn(-coef, __fsub_rn(pv, nv)), ru));
+        gp[i] = __fmul_rn(gg, __fadd_rn(__fmul_rn(-coef, u), __fmul_rn(reg, pv)));
+        gn[i] = __fmul_rn(gg, __fadd_rn(__fmul_rn(coef, u), __fmul_rn(reg, nv)));
+    }
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+extern "C" int kgq_bpr_forward_f32(const float *u, const float *p, const float *n, int64_t batch, int32_t d,
+                                   float l2, float *margins, float *loss, void *stream) {
+    if (batch < 1 || d < 1 || !u || !p || !n || !margins || !loss) return KGQ_ERR_INVALID_ARG;
+    bpr_forward_kernel<<<1, kBprThreads, 0, (cudaStream_t)stream>>>(u, p, n, batch, d, l2, margins, loss);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+extern "C" int kgq_bpr_backward_f32(const float *g, const float *margins, const float *uh, const float *ph,
+                                    const float *nh, int64_t batch, int32_t d, float reg, float *gu,
+                                    float *gp, float *gn, void *stream) {
+    if (batch < 1 || d < 1 || !g || !margins || !uh || !ph || !nh || !gu || !gp || !gn)
+        return KGQ_ERR_INVALID_ARG;
+    const int64_t total = batch * d;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)kSMs * 8) blocks = (int64_t)kSMs * 8;
+    bpr_backward_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(g, margins, uh, ph, nh, batch, d, reg,
+                                                                      gu, gp, gn);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -12,6 +12,8 @@ Each op is one (or two) libkgq launches on the current CUDA stream:
 """
 
 import os
+
+import numpy as np
 import torch
 
 from . import _lib
@@ -182,22 +184,32 @@ def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.
 
 
 def bpr_forward(u: torch.Tensor, p: torch.Tensor, n: torch.Tensor, l2: float):
-    """tape.py:166-170: margins = sum(u*(p-n)); loss = mean softplus(-m) +
-    l2*(|u|^2+|p|^2+|n|^2)/B.  Returns (loss 0-d tensor, margins)."""
-    batch = u.shape[0]
-    margins = (u * (p - n)).sum(dim=1)
-    data = torch.logaddexp(torch.zeros_like(margins), -margins).mean()
-    reg = l2 * ((u * u).sum() + (p * p).sum() + (n * n).sum()) / batch
-    return data + reg, margins
+    """tape.py:162-166: margins = sum(u*(p-n)); loss = mean softplus(-m) +
+    l2*(|u|^2+|p|^2+|n|^2)/B, one kernel (kgq_bpr_forward_f32).  Returns
+    (loss 0-d tensor, margins)."""
+    batch, d = u.shape
+    dev = u.device
+    u, p, n = u.contiguous(), p.contiguous(), n.contiguous()
+    margins = torch.empty(batch, dtype=torch.float32, device=dev)
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    st = _lib.load().kgq_bpr_forward_f32(u.data_ptr(), p.data_ptr(), n.data_ptr(), batch, d, float(l2),
+                                         margins.data_ptr(), loss.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_bpr_forward_f32")
+    return loss, margins
 
 
 def bpr_backward(g, margins, uh, ph, nh, l2: float, batch: int):
-    """tape.py:233-244 (against the dequantized blocks, exact margins)."""
-    coef = (torch.sigmoid(-margins) / batch)[:, None]
-    reg = 2.0 * l2 / batch
-    gu = g * (-coef * (ph - nh) + reg * uh)
-    gp = g * (-coef * uh + reg * ph)
-    gn = g * (coef * uh + reg * nh)
+    """tape.py:233-244 (against the dequantized blocks, exact margins), one
+    elementwise kernel (kgq_bpr_backward_f32); g is a 0-d device tensor."""
+    d = uh.shape[1]
+    dev = uh.device
+    gu, gp, gn = (torch.empty_like(t) for t in (uh, ph, nh))
+    g = g.reshape(()).to(device=dev, dtype=torch.float32).contiguous()
+    reg = float(np.float32(2.0 * l2 / batch))
+    st = _lib.load().kgq_bpr_backward_f32(g.data_ptr(), margins.contiguous().data_ptr(), uh.contiguous().data_ptr(),
+                                          ph.contiguous().data_ptr(), nh.contiguous().data_ptr(), batch, d, reg,
+                                          gu.data_ptr(), gp.data_ptr(), gn.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_bpr_backward_f32")
     return gu, gp, gn
 
 

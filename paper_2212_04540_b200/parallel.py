@@ -207,6 +207,8 @@ class GpuOps:
     quantize = staticmethod(quantize_tensor)
     dequantize = staticmethod(dequantize_tensor)
     scatter_rows = staticmethod(F.scatter_rows)
+    bpr_forward = staticmethod(F.bpr_forward)
+    bpr_backward = staticmethod(F.bpr_backward)
 
     layer_backward = staticmethod(F.layer_backward)
 
@@ -288,10 +290,10 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     b = users.shape[0]
     rows = comm.gather_index_rows(readout_local, lo, torch.cat([users, pos, neg]))
     u, p, n = rows[:b], rows[b:2 * b], rows[2 * b:]
-    loss, margins = F.bpr_forward(u, p, n, l2)
+    loss, margins = ops.bpr_forward(u, p, n, l2)
     qu, qp, qn = (ops.quantize(t, cfg, stream) for t in (u, p, n))
     one = torch.ones((), dtype=u.dtype, device=u.device)
-    gu, gp, gn = F.bpr_backward(one, margins, ops.dequantize(qu), ops.dequantize(qp),
+    gu, gp, gn = ops.bpr_backward(one, margins, ops.dequantize(qu), ops.dequantize(qp),
                                 ops.dequantize(qn), l2, u.shape[0])
     # readout gradient rows owned here: (scat_n + scat_p) + scat_u (reference.py:59-67)
     hi = lo + counts[part.rank]

@@ -403,3 +403,30 @@ def test_industry_generator_on_device_matches_host_adjacency():
         assert np.array_equal(bip, ip[lo:hi + 1] - ip[lo])
         assert np.array_equal(bix, ix[ip[lo]:ip[hi]])
         assert np.array_equal(bvv.view(np.uint32), vv[ip[lo]:ip[hi]].view(np.uint32))
+
+
+@pytest.mark.parametrize("batch,d", [(1024, 64), (1000, 128), (7, 32), (3, 48)])
+def test_bpr_head_kernels_match_reference_formula(batch, d):
+    """kgq_bpr_forward/backward_f32 vs the reference formulas (tape.py:162-166,
+    233-244) in float64: margins / loss within fp32 reduction tolerance,
+    gradients elementwise (same op order as the reference, fp32)."""
+    _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(batch + d)
+    u, p, n = (rng.standard_normal((batch, d), dtype=np.float32) for _ in range(3))
+    l2 = 1e-5
+    loss, m = F.bpr_forward(*(torch.from_numpy(t).cuda() for t in (u, p, n)), l2)
+    m64 = (u.astype(np.float64) * (p.astype(np.float64) - n)).sum(1)
+    np.testing.assert_allclose(m.cpu().numpy(), m64, rtol=1e-5, atol=1e-5)
+    ref = np.logaddexp(0, -m64).mean() + l2 * ((u.astype(np.float64) ** 2).sum() + (p.astype(np.float64) ** 2).sum()
+                                                 + (n.astype(np.float64) ** 2).sum()) / batch
+    assert float(loss) == pytest.approx(ref, rel=1e-5)
+    g = torch.ones((), device="cuda")
+    uh, ph, nh = (torch.from_numpy(t).cuda() for t in (u, p, n))
+    gu, gp, gn = F.bpr_backward(g, m, uh, ph, nh, l2, batch)
+    mf = m.cpu().numpy()
+    coef = ((1.0 / (1.0 + np.exp(mf.astype(np.float64)))) / batch).astype(np.float32)[:, None]
+    reg = np.float32(2.0 * l2 / batch)
+    np.testing.assert_allclose(gu.cpu().numpy(), -coef * (p - n) + reg * u, rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(gp.cpu().numpy(), -coef * u + reg * p, rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(gn.cpu().numpy(), coef * u + reg * n, rtol=1e-5, atol=1e-9)

@@ -82,6 +82,22 @@ class OracleOps:
         return OracleOps.dequant_gemm(q, g_j), g_j @ theta.t()
 
     @staticmethod
+    def bpr_forward(u, p, n, l2):
+        """tape.py:162-166 in numpy-order torch ops (CPU checker)."""
+        batch = u.shape[0]
+        margins = (u * (p - n)).sum(dim=1)
+        data = torch.logaddexp(torch.zeros_like(margins), -margins).mean()
+        reg = l2 * ((u * u).sum() + (p * p).sum() + (n * n).sum()) / batch
+        return data + reg, margins
+
+    @staticmethod
+    def bpr_backward(g, margins, uh, ph, nh, l2, batch):
+        coef = (torch.sigmoid(-margins) / batch)[:, None]
+        reg = 2.0 * l2 / batch
+        return (g * (-coef * (ph - nh) + reg * uh), g * (-coef * uh + reg * ph),
+                g * (coef * uh + reg * nh))
+
+    @staticmethod
     def scatter_rows(rows, idx, g):
         out = np.zeros((rows, g.shape[1]), dtype=np.float32)
         np.add.at(out, idx.numpy().astype(np.int64), g.numpy())
