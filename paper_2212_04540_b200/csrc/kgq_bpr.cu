@@ -17,25 +17,33 @@ namespace kgq {
 
 constexpr int kBprThreads = 1024;
 
+// 8 lanes per row (lane j of the group sums features j, j+8, ...), 4 rows per
+// warp and 128 rows per CTA pass: the batch is covered in B/128 passes with
+// every load of a pass in flight together.  Row terms are accumulated per
+// lane group in pass order, then reduced over the CTA in a fixed tree.
 __global__ void __launch_bounds__(kBprThreads)
 bpr_forward_kernel(const float *__restrict__ u, const float *__restrict__ p, const float *__restrict__ n,
                    int64_t batch, int d, float l2, float *__restrict__ margins, float *__restrict__ loss) {
     __shared__ float s_sp[32], s_rg[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float sp = 0.0f, rg = 0.0f;                  // per-warp running sums (lane 0)
-    for (int64_t r = warp; r < batch; r += kBprThreads / 32) {
+    const int j = lane & 7, grp = lane >> 3;
+    float sp = 0.0f, rg = 0.0f;                  // per lane-group running sums (j == 0 holds sp)
+    for (int64_t r0 = 0; r0 < batch; r0 += kBprThreads / 8) {
+        const int64_t r = r0 + warp * 4 + grp;
         float m = 0.0f, q = 0.0f;
-        for (int k = lane; k < d; k += 32) {
-            const float uv = __ldg(u + r * d + k), pv = __ldg(p + r * d + k), nv = __ldg(n + r * d + k);
-            m = __fadd_rn(m, __fmul_rn(uv, __fsub_rn(pv, nv)));
-            q = __fadd_rn(q, __fadd_rn(__fadd_rn(__fmul_rn(uv, uv), __fmul_rn(pv, pv)), __fmul_rn(nv, nv)));
+        if (r < batch) {
+            for (int k = j; k < d; k += 8) {
+                const float uv = __ldg(u + r * d + k), pv = __ldg(p + r * d + k), nv = __ldg(n + r * d + k);
+                m = __fadd_rn(m, __fmul_rn(uv, __fsub_rn(pv, nv)));
+                q = __fadd_rn(q, __fadd_rn(__fadd_rn(__fmul_rn(uv, uv), __fmul_rn(pv, pv)), __fmul_rn(nv, nv)));
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 4; o > 0; o >>= 1) {
             m = __fadd_rn(m, __shfl_xor_sync(0xffffffffu, m, o));
             q = __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
         }
-        if (lane == 0) {
+        if (j == 0 && r < batch) {
             margins[r] = m;
             // logaddexp(0, -m) = max(0, -m) + log1p(exp(-|m|))
             const float x = -m;
@@ -43,22 +51,27 @@ bpr_forward_kernel(const float *__restrict__ u, const float *__restrict__ p, con
             rg = __fadd_rn(rg, q);
         }
     }
+    // lane groups of the warp (lanes 0, 8, 16, 24), then warps, fixed order
+    sp = __fadd_rn(sp, __shfl_xor_sync(0xffffffffu, sp, 8));
+    rg = __fadd_rn(rg, __shfl_xor_sync(0xffffffffu, rg, 8));
+    sp = __fadd_rn(sp, __shfl_xor_sync(0xffffffffu, sp, 16));
+    rg = __fadd_rn(rg, __shfl_xor_sync(0xffffffffu, rg, 16));
     if (lane == 0) {
         s_sp[warp] = sp;
         s_rg[warp] = rg;
     }
     __syncthreads();
     if (warp == 0) {
-        float a = s_sp[lane], b = s_rg[lane];
+        float a = s_sp[lane], b2 = s_rg[lane];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
-            b = __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+            b2 = __fadd_rn(b2, __shfl_xor_sync(0xffffffffu, b2, o));
         }
         if (lane == 0) {
             const float fb = (float)batch;
             const float data = __fdiv_rn(a, fb);
-            const float reg = __fdiv_rn(__fmul_rn(l2, b), fb);
+            const float reg = __fdiv_rn(__fmul_rn(l2, b2), fb);
             *loss = __fadd_rn(data, reg);
         }
     }

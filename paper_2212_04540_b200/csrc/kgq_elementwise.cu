@@ -129,3 +129,64 @@ extern "C" int kgq_mask_apply_f32(const float *g, const uint8_t *mask, int64_t n
     return KGQ_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Deterministic scatter-add of several gathers' gradients into one source
+// (tape.py:229-232 + the routing order of tape.py:204-209): list i is
+// np.add.at(zeros, idx_i, g_i) -- duplicates accumulated sequentially in
+// occurrence order, starting from +0 -- and the lists are combined as
+// ((s_0 + s_1) + s_2) ... with absent rows contributing +0, exactly the
+// reference's dense sums.  The caller sorts positions by (row, position)
+// (positions are list-major), so one warp walks each row's occurrences in
+// order; rows that occur in no list are left untouched (the caller zeroes).
+// ---------------------------------------------------------------------------
+constexpr int kMaxScatterLists = 8;
+struct ListEnds { int64_t e[kMaxScatterLists]; };
+
+__global__ void __launch_bounds__(256)
+scatter_rows_multi_kernel(const int64_t *__restrict__ order, const int32_t *__restrict__ idx, int64_t m,
+                          ListEnds list_end, int n_lists, const float *__restrict__ g,
+                          int d, float *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= m) return;
+    const int64_t pos0 = __ldg(order + i);
+    const int32_t row = __ldg(idx + pos0);
+    if (i > 0 && __ldg(idx + __ldg(order + i - 1)) == row) return;   // not the first occurrence
+    for (int f0 = 0; f0 < d; f0 += 32) {
+        const int f = f0 + lane;
+        float total = 0.0f, acc = 0.0f;
+        int li = 0;                                   // next list to fold into total
+        for (int64_t j = i; j < m; j++) {
+            const int64_t pos = __ldg(order + j);
+            if (__ldg(idx + pos) != row) break;
+            int l = 0;
+            while (l + 1 < n_lists && pos >= list_end.e[l]) l++;
+            for (; li < l; li++) {                    // finish list li (complete or absent)
+                total = li == 0 ? acc : __fadd_rn(total, acc);
+                acc = 0.0f;
+            }
+            if (f < d) acc = __fadd_rn(acc, __ldg(g + pos * d + f));
+        }
+        for (; li < n_lists; li++) {
+            total = li == 0 ? acc : __fadd_rn(total, acc);
+            acc = 0.0f;
+        }
+        if (f < d) out[(int64_t)row * d + f] = total;
+    }
+}
+
+extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx, int64_t m,
+                                          const int64_t *list_end, int32_t n_lists, const float *g,
+                                          int32_t d, float *out, void *stream) {
+    if (m < 0 || d < 1 || n_lists < 1 || n_lists > kMaxScatterLists || !list_end) return KGQ_ERR_INVALID_ARG;
+    if (m == 0) return KGQ_OK;
+    if (!order || !idx || !g || !out) return KGQ_ERR_INVALID_ARG;
+    ListEnds ends;                                  // host array -> kernel parameter (graph-capturable)
+    for (int i = 0; i < kMaxScatterLists; i++) ends.e[i] = i < n_lists ? list_end[i] : m;
+    const int64_t blocks = (m * 32 + 255) / 256;
+    scatter_rows_multi_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(order, idx, m, ends, n_lists,
+                                                                           g, d, out);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -214,7 +214,29 @@ def bpr_backward(g, margins, uh, ph, nh, l2: float, batch: int):
 
 
 def scatter_rows(src_rows: int, idx: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
-    """np.add.at(zeros, idx, g) (tape.py:229-231)."""
-    out = torch.zeros((src_rows, g.shape[1]), dtype=g.dtype, device=g.device)
-    out.index_add_(0, idx.to(torch.int64), g)
+    """np.add.at(zeros, idx, g) (tape.py:229-231), deterministic."""
+    return scatter_rows_multi(src_rows, [idx], [g])
+
+
+def scatter_rows_multi(src_rows: int, idxs, gs) -> torch.Tensor:
+    """((s_0 + s_1) + ...) with s_i = np.add.at(zeros, idxs[i], gs[i]): the
+    reference's dense sum of several gathers' scatters (tape.py:204-209,
+    229-232), bit-deterministic (kgq_scatter_rows_multi_f32; positions
+    sorted by (row, position), one warp per row)."""
+    dev = gs[0].device
+    d = gs[0].shape[1]
+    idx = torch.cat([i.reshape(-1).to(torch.int32) for i in idxs])
+    g = torch.cat([x.reshape(-1, d).to(torch.float32) for x in gs]).contiguous()
+    m = idx.numel()
+    out = torch.zeros((src_rows, d), dtype=torch.float32, device=dev)
+    if m == 0:
+        return out
+    ends = np.ascontiguousarray(np.cumsum([i.numel() for i in idxs]), dtype=np.int64)   # host, by value
+    key = idx.to(torch.int64) * m + torch.arange(m, device=dev, dtype=torch.int64)
+    order = torch.sort(key).indices
+    if len(idxs) > 8:
+        raise ValueError("at most 8 gathers per scatter")
+    st = _lib.load().kgq_scatter_rows_multi_f32(order.data_ptr(), idx.data_ptr(), m, ends.ctypes.data, len(idxs),
+                                                g.data_ptr(), d, out.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_scatter_rows_multi_f32")
     return out
