@@ -36,7 +36,9 @@ struct RG {
     // heavy-path ring: P stages of kCH neighbour rows (<= 32 KB) + values
     static constexpr int P = (32 * 1024) / (kCH * D * 4) > 4 ? 4 : (32 * 1024) / (kCH * D * 4);
     static constexpr int NI = kCH * D / 4 / 256;           // cp.async per thread per stage
-    static constexpr size_t ring_bytes = (size_t)P * kCH * (D + 1) * 4;
+    // + column-id / value blocks: 2 x 256 ids and values (8 stages each),
+    // streamed with cp.async a block ahead so no id load is on the chain
+    static constexpr size_t ring_bytes = (size_t)P * kCH * (D + 1) * 4 + 2 * 256 * 8;
 };
 
 // ---------------------------------------------------------------------------
@@ -134,54 +136,69 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
                                                 const float *__restrict__ x, int64_t row,
                                                 float *ring) {
     constexpr int P = RG<D>::P, NI = RG<D>::NI;
+    constexpr int SPB = 256 / kCH;                  // stages per id block
     float *xs = ring;                               // [P][kCH][D]
     float *vs = ring + P * kCH * D;                 // [P][kCH]
+    int32_t *ids = reinterpret_cast<int32_t *>(vs + P * kCH);   // [2][256]
+    float *vls = reinterpret_cast<float *>(ids + 512);           // [2][256]
     const int t = threadIdx.x;
     const int32_t beg = __ldg(indptr + row), end = __ldg(indptr + row + 1);
     const int n = end - beg;
     const int nch = (n + kCH - 1) / kCH;
-    int32_t pcol[NI];
-    float pval = 0.0f;
-    auto load_idx = [&](int c) {
-#pragma unroll
-        for (int m = 0; m < NI; m++) {
-            const int i = t + 256 * m, r = i / (D / 4);
-            const int k = c * kCH + r;
-            pcol[m] = (k < n) ? __ldg(indices + beg + k) : -1;
+    auto load_block = [&](int b) {                  // ids/values of stages [b*SPB, (b+1)*SPB)
+        const int k = b * 256 + t;
+        if (k < n) {
+            cp_async4(ids + (b & 1) * 256 + t, indices + beg + k);
+            cp_async4(vls + (b & 1) * 256 + t, vals + beg + k);
         }
-        if (t < kCH) pval = (c * kCH + t < n) ? __ldg(vals + beg + c * kCH + t) : 0.0f;
     };
-    auto issue = [&](int c) {
+    auto issue = [&](int c) {                       // data of stage c (ids already in smem)
         const int st = c % P;
+        if (c < nch) {
+            const int32_t *blk = ids + ((c / SPB) & 1) * 256 + (c % SPB) * kCH;
 #pragma unroll
-        for (int m = 0; m < NI; m++) {
-            const int i = t + 256 * m, r = i / (D / 4), f4 = i % (D / 4);
-            if (pcol[m] >= 0)
-                cp_async16(xs + (st * kCH + r) * D + f4 * 4, x + (int64_t)pcol[m] * D + f4 * 4);
+            for (int m = 0; m < NI; m++) {
+                const int i = t + 256 * m, r = i / (D / 4), f4 = i % (D / 4);
+                if (c * kCH + r < n)
+                    cp_async16(xs + (st * kCH + r) * D + f4 * 4, x + (int64_t)blk[r] * D + f4 * 4);
+            }
+            if (t < kCH) vs[st * kCH + t] = (c * kCH + t < n) ? vls[((c / SPB) & 1) * 256 + (c % SPB) * kCH + t] : 0.0f;
         }
-        if (t < kCH) vs[st * kCH + t] = pval;
         cp_async_commit();
     };
+    // prologue: id blocks 0 and 1, then the first P-1 stages
+    load_block(0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    load_block(1);
 #pragma unroll
-    for (int c = 0; c < P - 1; c++) {
-        load_idx(c);
-        issue(c);
-    }
-    load_idx(P - 1);
+    for (int c = 0; c < P - 1; c++) issue(c);
     float acc = 0.0f;
     for (int c = 0; c < nch; c++) {
         cp_async_wait<P - 2>();
         __syncthreads();
+        // chunk c+P-1 opens id block kb: block kb-1 is fully issued, so its
+        // buffer takes block kb+1 (landing long before chunk 8(kb+1) issues)
+        const int cn = c + P - 1;
+        if (cn % SPB == 0 && cn >= SPB) load_block(cn / SPB + 1);
         const int st = c % P;
         if (t < D) {
             const int cnt = min(kCH, n - c * kCH);
             const float *xr = xs + st * kCH * D + t;
             const float *vr = vs + st * kCH;
-            for (int r = 0; r < cnt; r++) acc = __fadd_rn(acc, __fmul_rn(vr[r], xr[r * D]));
+            if (cnt == kCH) {       // full stage: all products first (independent LDS), then the chain
+                float pr[kCH];
+#pragma unroll
+                for (int r = 0; r < kCH; r++) pr[r] = __fmul_rn(vr[r], xr[r * D]);
+#pragma unroll
+                for (int r = 0; r < kCH; r++) acc = __fadd_rn(acc, pr[r]);
+            } else {
+                for (int r = 0; r < cnt; r++) acc = __fadd_rn(acc, __fmul_rn(vr[r], xr[r * D]));
+            }
         }
         __syncthreads();
-        issue(c + P - 1);
-        load_idx(c + P);
+        issue(cn);
     }
     cp_async_wait<0>();
     __syncthreads();

@@ -7,7 +7,7 @@ import torch
 from paper_2212_04540_b200 import data, tensorops
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "amazon"
-ds = data.synth_kg(data.SHAPES[shape], seed=0)
+ds = data.reference_dataset(shape) if shape in data.REFERENCE_DATASETS else data.synth_kg(data.SHAPES[shape], seed=0)
 A = data.build_adjacency(ds)
 N = A.shape[0]
 x = torch.randn(N, 64, device="cuda")
@@ -24,7 +24,7 @@ def timeit(f, n=20):
 
 
 ref = tensorops.spmm(A, x)
-for th in (64, 128, 256, 512, 1024, 1 << 30):
+for th in (128, 256, 512, 1024, 2048, 4096, 1 << 30):
     A._row_order = None
     A.HEAVY_NNZ = th
     A.schedule()

@@ -9,7 +9,7 @@ from paper_2212_04540_b200 import data as D
 from paper_2212_04540_b200.model import ModelConfig, init_params
 from paper_2212_04540_b200.train import TrainConfig, AdamState, train_epoch
 
-ds = D.reference_dataset("amazon")
+ds = D.reference_dataset(sys.argv[1] if len(sys.argv) > 1 else "amazon")
 adj = D.build_adjacency(ds)
 q = kgq.QuantConfig(bits=2)
 mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), TrainConfig(quant=q)
