@@ -31,8 +31,11 @@ struct BwdSmem {
     static constexpr size_t bytes = ((size_t)D * D + 3 * (size_t)kBwdRows * D) * sizeof(float);
 };
 
+#ifndef KGQ_BWD_MINB
+#define KGQ_BWD_MINB 1
+#endif
 template <int D, int BITS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, D > 64 ? 1 : KGQ_BWD_MINB)
 layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
                       const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
                       const float *__restrict__ ranges, const float *__restrict__ offsets,
