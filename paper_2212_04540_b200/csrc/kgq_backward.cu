@@ -15,6 +15,7 @@
 // Shared memory is dynamic: theta^T d*d + g_j, Hhat 2*32*d + g_j k-major 32*d
 // floats (112 KB at d = 128).
 #include "kgq_common.cuh"
+#include <cstdlib>
 
 namespace kgq {
 
@@ -198,6 +199,24 @@ reduce_partials_bwd_kernel(const float *__restrict__ partial, int nparts, int dd
 
 using namespace kgq;
 
+// d = 64: opt-in tcgen05 kernel (kgq_backward_tc.cu), KGQ_BWD_TC=1 (read once).
+// Measured at Amazon shape: 118 us vs 110 us for the FFMA kernel below, which
+// stays the default: ncu shows 85 % of its shared-store wavefronts are bank
+// conflicts (the three operand layouts are written element-wise); the
+// conflict-free padded strides need ~1 KB more than the 227 KB per CTA.
+int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
+                                 const uint8_t *codes, const float *ranges, const float *offsets,
+                                 int64_t rows, int32_t bits, const float *theta, float *dh,
+                                 float *partial, int grid, cudaStream_t s);
+static bool use_tc_backward() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KGQ_BWD_TC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 extern "C" size_t kgq_layer_backward_workspace_bytes(int64_t rows, int32_t d) {
     if (d != 32 && d != 64 && d != 128) return 0;
     return (size_t)bwd_grid(rows) * d * d * sizeof(float);
@@ -225,9 +244,22 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     if (((uintptr_t)mask) & 3u) return KGQ_ERR_MISALIGNED;
     if (!workspace || workspace_bytes < kgq_layer_backward_workspace_bytes(rows, d))
         return KGQ_ERR_INVALID_ARG;
-    const int grid = bwd_grid(rows);
+    int grid = bwd_grid(rows);
     float *partial = reinterpret_cast<float *>(workspace);
     const uint32_t *m32 = reinterpret_cast<const uint32_t *>(mask);
+    const bool aligned16 = ((((uintptr_t)g_read) | ((uintptr_t)g_e) | ((uintptr_t)dh)) & 15u) == 0 &&
+                           ((uintptr_t)codes & 3u) == 0;
+    if (d == 64 && aligned16 && use_tc_backward()) {
+        const int64_t tiles = (rows + 127) / 128;
+        grid = (int)(tiles < kSMs ? tiles : kSMs);
+        const int st = kgq_launch_layer_backward_tc(g_read, g_e, m32, codes, ranges, offsets, rows, bits, theta,
+                                                    dh, partial, grid, s);
+        if (st != KGQ_OK) return st;
+        const int dd = d * d;
+        reduce_partials_bwd_kernel<<<(dd + 31) / 32, 256, 0, s>>>(partial, grid, dd, dtheta, accumulate);
+        KGQ_LAUNCH_CHECK();
+        return KGQ_OK;
+    }
 #define KGQ_BWD(D, B) do {                                                                          \
         static bool attr_set = false;   /* > 48 KB dynamic smem needs the opt-in once per instance */ \
         if (!attr_set) {                                                                          \

@@ -1,0 +1,222 @@
+// kgq_backward_tc.cu -- the fused layer backward (tape.py:217-225) on the
+// 5th-generation tensor cores for d = 64:
+//
+//   g_j = (g_read + g_e) * mask;  dH = g_j . theta^T;  dtheta += Hhat^T . g_j
+//
+// One CTA per SM walks 128-row tiles.  All 256 threads stage the tile: thread
+// t owns row t/2, columns 32*(t&1)..+31, forms g_j and the IEEE-dequantized
+// Hhat in registers and writes their 3xTF32 hi/lo splits into shared memory in
+// the K-major interleaved layout (kgq_tc.cuh) three times over:
+//   Ag  (r, k=c)        A of dH       (M = 128 rows, K = 64)
+//   Ah' (i=c, k=r)      A of dtheta   (M = 64,       K = 128 rows)
+//   Bg' (j=c, k=r)      B of dtheta   (N = 64,       K = 128 rows)
+// theta^T's split (B of dH, B(n,k) = theta[n][k]) is staged once per CTA.
+// One elected thread issues 3 x 8 MMAs for dH into TMEM columns [0, 64) and
+// 3 x 16 MMAs accumulating dtheta into columns [64, 128) across the CTA's
+// tiles, then commits to an mbarrier; the 8 warps drain dH with tcgen05.ld.
+// The M = 64 dtheta accumulator lives in TMEM lanes 32q + (0..15) for rows
+// 16q..16q+15 (probed: tools/tc_probe/m64_layout.cu).  Per-CTA dtheta
+// partials are reduced in a fixed order (reduce_partials_bwd_kernel).
+// 3xTF32 = hi*hi + hi*lo + lo*hi with fp32 accumulation: fp32-level accuracy
+// (the reference's BLAS GEMMs are tolerance-compared).
+#include "kgq_tc.cuh"
+
+namespace kgq {
+
+constexpr int kTcRows = 128;
+constexpr int kTcD = 64;
+
+struct BwdTcSmem {
+    static constexpr int AG = kTcRows * kTcD;        // floats per hi or lo tile
+    static constexpr int TH = kTcD * kTcD;
+    static constexpr size_t bytes = (size_t)(2 * TH + 6 * AG) * sizeof(float);   // 224 KB
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(256, 1)
+layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
+                         const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
+                         const float *__restrict__ ranges, const float *__restrict__ offsets,
+                         int64_t rows, const float *__restrict__ theta, float *__restrict__ dh,
+                         float *__restrict__ partial) {
+    constexpr int M = kTcRows, D = kTcD, RB = D * BITS / 8;
+    constexpr uint32_t CM = (1u << BITS) - 1u;
+    extern __shared__ __align__(128) float tsm[];
+    float *th_hi = tsm, *th_lo = tsm + BwdTcSmem::TH;
+    float *ag_hi = tsm + 2 * BwdTcSmem::TH, *ag_lo = ag_hi + BwdTcSmem::AG;
+    float *ah_hi = ag_lo + BwdTcSmem::AG, *ah_lo = ah_hi + BwdTcSmem::AG;
+    float *bg_hi = ah_lo + BwdTcSmem::AG, *bg_lo = bg_hi + BwdTcSmem::AG;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+
+    // theta^T split: B(n, k) = theta[n][k]
+    for (int i = t; i < D * D; i += 256) {
+        const int n = i / D, k = i % D;
+        float hi, lo;
+        tc::split_tf32(__ldg(theta + i), hi, lo);
+        th_hi[tc::tile_off(n, k, D) / 4] = hi;
+        th_lo[tc::tile_off(n, k, D) / 4] = lo;
+    }
+    if (t == 0) tc::mbar_init(&mbar, 1);
+    if (warp == 0) tc::tmem_alloc(&tmem_base, 128);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    const int r = t >> 1, c0 = (t & 1) * 32;       // staging: my row and column half
+    uint32_t phase = 0;
+    bool first = true;
+    const int64_t n_tiles = (rows + M - 1) / M;
+    // register prefetch of one tile's inputs (issued while the previous
+    // tile's MMAs run, so the loads overlap the tensor-core work)
+    float4 pa[8], pe[8];
+    float prg = 0.f, pzz = 0.f;
+    uint32_t pmw = 0u, pcw[BITS];
+    auto load = [&](int64_t tl) {
+        const int64_t row = tl * M + r;
+        const bool ok = tl < n_tiles && row < rows;
+        prg = ok ? __ldg(ranges + row) : 0.f;
+        pzz = ok ? __ldg(offsets + row) : 0.f;
+        pmw = ok ? __ldg(mask + row * (D / 32) + (t & 1)) : 0u;
+        const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB + c0 * BITS / 8);
+#pragma unroll
+        for (int w = 0; w < BITS; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
+        const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D + c0);
+        const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D + c0);
+#pragma unroll
+        for (int v = 0; v < 8; v++) {
+            pa[v] = (ok && g_read) ? __ldg(gr4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pe[v] = (ok && g_e) ? __ldg(ge4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    load(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t row = tile * M + r;
+        const bool ok = row < rows;
+        // ---- 1. stage g_j and Hhat (hi/lo, three layouts) from the prefetched registers ----
+        {
+            const float rg = prg, zz = pzz;
+            const uint32_t mw = pmw;
+#pragma unroll
+            for (int v = 0; v < 8; v++) {
+                const float av[4] = {pa[v].x, pa[v].y, pa[v].z, pa[v].w}, ev[4] = {pe[v].x, pe[v].y, pe[v].z, pe[v].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int cl = 4 * v + q, c = c0 + cl;
+                    // g = g_read + g_e in the reference's routing order (tape.py:204-209)
+                    const float g = (g_read && g_e) ? __fadd_rn(av[q], ev[q]) : (g_read ? av[q] : ev[q]);
+                    const float gj = __fmul_rn(g, ((mw >> cl) & 1u) ? 1.0f : 0.0f);
+                    const int bp = cl * BITS;
+                    const uint32_t code = (pcw[bp >> 5] >> (bp & 31)) & CM;
+                    const float hv = ok ? lut_entry<BITS>(rg, zz, (int)code) : 0.0f;
+                    float gh, gl, hh, hl;
+                    tc::split_tf32(gj, gh, gl);
+                    tc::split_tf32(hv, hh, hl);
+                    const uint32_t oa = tc::tile_off(r, c, M) / 4;     // Ag  (r, k=c)
+                    const uint32_t ob = tc::tile_off(c, r, D) / 4;     // Ah', Bg' (c, k=r)
+                    ag_hi[oa] = gh; ag_lo[oa] = gl;
+                    bg_hi[ob] = gh; bg_lo[ob] = gl;
+                    ah_hi[ob] = hh; ah_lo[ob] = hl;
+                }
+            }
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+        // ---- 2. MMAs: dH (cols 0..63), dtheta accumulate (cols 64..127) ----
+        if (t == 0) {
+            tc::fence_after();
+            tc::mma_3xtf32<M, D, D>(tmem, ag_hi, ag_lo, th_hi, th_lo);
+            constexpr uint32_t LBO = (D / 8) * 128;
+            constexpr uint32_t idesc = tc::idesc_tf32(D, D);         // M = 64, N = 64
+            const uint32_t sah = tc::smem_u32(ah_hi), sal = tc::smem_u32(ah_lo);
+            const uint32_t sbh = tc::smem_u32(bg_hi), sbl = tc::smem_u32(bg_lo);
+            uint32_t acc = first ? 0u : 1u;
+#pragma unroll
+            for (int pass = 0; pass < 3; pass++) {
+                const uint32_t sa = pass == 0 ? sal : sah;
+                const uint32_t sb = pass == 1 ? sbl : sbh;
+#pragma unroll
+                for (int s = 0; s < M / 8; s++) {
+                    tc::mma_tf32(tmem + 64, tc::smem_desc(sa + 2 * s * LBO, LBO, 128),
+                                 tc::smem_desc(sb + 2 * s * LBO, LBO, 128), idesc, acc);
+                    acc = 1u;
+                }
+            }
+            tc::commit(&mbar);
+        }
+        first = false;
+        load(tile + gridDim.x);                     // next tile's inputs, in flight during the MMAs
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        // ---- 3. drain dH: warp w -> lanes 32*(w%4).., columns 32*(w/4).. ----
+        {
+            const int q = warp & 3, cb = (warp >> 2) * 32;
+            float v[32];
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
+            const int64_t orow = tile * M + 32 * q + lane;
+            if (orow < rows) {
+                float4 *dst = reinterpret_cast<float4 *>(dh + orow * D + cb);
+#pragma unroll
+                for (int j = 0; j < 8; j++) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+        }
+        tc::fence_before();
+        __syncthreads();
+    }
+    // ---- dtheta partial of this CTA: rows i = 16q + l live in lanes 32q + l ----
+    if (warp < 4) {
+        float *dst = partial + (int64_t)blockIdx.x * D * D;
+#pragma unroll
+        for (int cb = 0; cb < 64; cb += 32) {
+            float v[32];
+            if (first) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) v[j] = 0.0f;     // no tile: zero partial
+            } else {
+                tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 64u + (uint32_t)cb, v);
+            }
+            if (lane < 16) {
+                float4 *o = reinterpret_cast<float4 *>(dst + (16 * warp + lane) * D + cb);
+#pragma unroll
+                for (int j = 0; j < 8; j++) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free(tmem, 128);
+}
+
+}  // namespace kgq
+
+using namespace kgq;
+
+// Launch helper used by kgq_layer_backward_f32 (kgq_backward.cu) for d = 64.
+int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
+                                 const uint8_t *codes, const float *ranges, const float *offsets,
+                                 int64_t rows, int32_t bits, const float *theta, float *dh,
+                                 float *partial, int grid, cudaStream_t s) {
+    static bool attr[9] = {false};
+#define KGQ_BTC(B) do {                                                                            \
+        if (!attr[B]) {                                                                            \
+            cudaError_t e = cudaFuncSetAttribute(layer_backward_tc_kernel<B>,                        \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                                 (int)BwdTcSmem::bytes);                            \
+            if (e != cudaSuccess) return kgq_set_cuda_error(e);                                    \
+            attr[B] = true;                                                                        \
+        }                                                                                          \
+        layer_backward_tc_kernel<B><<<grid, 256, BwdTcSmem::bytes, s>>>(g_read, g_e, mask, codes,   \
+                                                                        ranges, offsets, rows, theta, dh, partial); \
+    } while (0)
+    switch (bits) {
+        case 1: KGQ_BTC(1); break;
+        case 2: KGQ_BTC(2); break;
+        case 4: KGQ_BTC(4); break;
+        default: KGQ_BTC(8); break;
+    }
+#undef KGQ_BTC
+    return KGQ_OK;
+}

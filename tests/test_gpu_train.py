@@ -484,3 +484,37 @@ def test_scatter_rows_multi_matches_reference_dense_sums():
     s0 = np.zeros((rows, d), np.float32)
     np.add.at(s0, idxs[0], gs[0])
     assert np.array_equal(one.cpu().numpy().view(np.uint32), s0.view(np.uint32))
+
+
+def test_tcgen05_layer_backward_matches_fp64_subprocess():
+    """The opt-in tcgen05 backward (KGQ_BWD_TC=1, kgq_backward_tc.cu: 3xTF32
+    MMAs, TMEM accumulators) against float64 on a fresh process."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+import paper_2212_04540_b200 as kgq
+from paper_2212_04540_b200 import functional as F
+rng = np.random.default_rng(5)
+for bits in (1, 2, 4, 8):
+    rows, d = 10007, 64
+    x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(1), tensor_id=2)
+    j = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    _, mask = kgq.relu(j)
+    gr = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    ge = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    th = torch.from_numpy((rng.standard_normal((d, d)) / 8).astype(np.float32)).cuda()
+    dth, dh = F.layer_backward(gr, ge, mask, q, th)
+    gj = ((gr + ge) * (j > 0)).double()
+    hh = kgq.dequantize_tensor(q).double()
+    np.testing.assert_allclose(dh.cpu().numpy(), (gj @ th.double().t()).cpu().numpy(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(dth.cpu().numpy(), (hh.t() @ gj).cpu().numpy(), rtol=1e-4, atol=1e-4 * np.sqrt(rows))
+print("ok")
+"""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KGQ_BWD_TC="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
