@@ -199,11 +199,8 @@ reduce_partials_bwd_kernel(const float *__restrict__ partial, int nparts, int dd
 
 using namespace kgq;
 
-// d = 64: opt-in tcgen05 kernel (kgq_backward_tc.cu), KGQ_BWD_TC=1 (read once).
-// Measured at Amazon shape: 118 us vs 110 us for the FFMA kernel below, which
-// stays the default: ncu shows 85 % of its shared-store wavefronts are bank
-// conflicts (the three operand layouts are written element-wise); the
-// conflict-free padded strides need ~1 KB more than the 227 KB per CTA.
+// d = 64: the tcgen05 kernel (kgq_backward_tc.cu) by default; KGQ_BWD_TC=0
+// selects the FFMA kernel below (read once).  Amazon shape: 89 us vs 110 us.
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t bits, const float *theta, float *dh,
@@ -212,7 +209,7 @@ static bool use_tc_backward() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("KGQ_BWD_TC");
-        v = (e && e[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }

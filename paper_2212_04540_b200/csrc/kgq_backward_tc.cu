@@ -26,11 +26,19 @@ namespace kgq {
 constexpr int kTcRows = 128;
 constexpr int kTcD = 64;
 
+// The transposed operands (k = row) use a padded K-quad stride LBO_T = 1040 B
+// (1024 + 16): with thread (row r, column quads 2j+h) the 32 scalar stores of
+// a warp then hit 32 distinct banks.  Ag is written with 128-bit stores.
+constexpr uint32_t kLboT = 1040;
 struct BwdTcSmem {
-    static constexpr int AG = kTcRows * kTcD;        // floats per hi or lo tile
+    static constexpr int AG = kTcRows * kTcD;                              // Ag hi or lo (floats)
+    static constexpr int AT = ((kTcRows / 4 - 1) * kLboT + 1024) / 4;      // Ah'/Bg' hi or lo (floats)
     static constexpr int TH = kTcD * kTcD;
-    static constexpr size_t bytes = (size_t)(2 * TH + 6 * AG) * sizeof(float);   // 224 KB
+    static constexpr size_t bytes = (size_t)(2 * TH + 2 * AG + 4 * AT) * sizeof(float);   // 225.9 KB
 };
+__device__ __forceinline__ uint32_t toff_t(int c, int r) {   // (row c, k = r), padded K-quad stride
+    return (uint32_t)((r >> 2) * kLboT + (c >> 3) * 128 + (c & 7) * 16 + (r & 3) * 4);
+}
 
 template <int BITS>
 __global__ void __launch_bounds__(256, 1)
@@ -44,8 +52,8 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     extern __shared__ __align__(128) float tsm[];
     float *th_hi = tsm, *th_lo = tsm + BwdTcSmem::TH;
     float *ag_hi = tsm + 2 * BwdTcSmem::TH, *ag_lo = ag_hi + BwdTcSmem::AG;
-    float *ah_hi = ag_lo + BwdTcSmem::AG, *ah_lo = ah_hi + BwdTcSmem::AG;
-    float *bg_hi = ah_lo + BwdTcSmem::AG, *bg_lo = bg_hi + BwdTcSmem::AG;
+    float *ah_hi = ag_lo + BwdTcSmem::AG, *ah_lo = ah_hi + BwdTcSmem::AT;
+    float *bg_hi = ah_lo + BwdTcSmem::AT, *bg_lo = bg_hi + BwdTcSmem::AT;
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tmem_base;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -65,7 +73,8 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     tc::fence_after();
     const uint32_t tmem = tmem_base;
 
-    const int r = t >> 1, c0 = (t & 1) * 32;       // staging: my row and column half
+    // staging: thread owns row r = t/2 and the column quads 2j + h (j = 0..7)
+    const int r = t >> 1, h = t & 1;
     uint32_t phase = 0;
     bool first = true;
     const int64_t n_tiles = (rows + M - 1) / M;
@@ -73,22 +82,23 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     // tile's MMAs run, so the loads overlap the tensor-core work)
     float4 pa[8], pe[8];
     float prg = 0.f, pzz = 0.f;
-    uint32_t pmw = 0u, pcw[BITS];
+    uint32_t pm0 = 0u, pm1 = 0u, pcw[2 * BITS];
     auto load = [&](int64_t tl) {
         const int64_t row = tl * M + r;
         const bool ok = tl < n_tiles && row < rows;
         prg = ok ? __ldg(ranges + row) : 0.f;
         pzz = ok ? __ldg(offsets + row) : 0.f;
-        pmw = ok ? __ldg(mask + row * (D / 32) + (t & 1)) : 0u;
-        const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB + c0 * BITS / 8);
+        pm0 = ok ? __ldg(mask + row * 2) : 0u;
+        pm1 = ok ? __ldg(mask + row * 2 + 1) : 0u;
+        const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB);
 #pragma unroll
-        for (int w = 0; w < BITS; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
-        const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D + c0);
-        const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D + c0);
+        for (int w = 0; w < 2 * BITS; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
+        const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D);
+        const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D);
 #pragma unroll
-        for (int v = 0; v < 8; v++) {
-            pa[v] = (ok && g_read) ? __ldg(gr4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-            pe[v] = (ok && g_e) ? __ldg(ge4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < 8; j++) {
+            pa[j] = (ok && g_read) ? __ldg(gr4 + 2 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pe[j] = (ok && g_e) ? __ldg(ge4 + 2 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
     load(blockIdx.x);
@@ -98,28 +108,30 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         // ---- 1. stage g_j and Hhat (hi/lo, three layouts) from the prefetched registers ----
         {
             const float rg = prg, zz = pzz;
-            const uint32_t mw = pmw;
 #pragma unroll
-            for (int v = 0; v < 8; v++) {
-                const float av[4] = {pa[v].x, pa[v].y, pa[v].z, pa[v].w}, ev[4] = {pe[v].x, pe[v].y, pe[v].z, pe[v].w};
+            for (int j = 0; j < 8; j++) {
+                const float av[4] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w}, ev[4] = {pe[j].x, pe[j].y, pe[j].z, pe[j].w};
+                float gh[4], gl[4];
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    const int cl = 4 * v + q, c = c0 + cl;
+                    const int c = 8 * j + 4 * h + q;
                     // g = g_read + g_e in the reference's routing order (tape.py:204-209)
                     const float g = (g_read && g_e) ? __fadd_rn(av[q], ev[q]) : (g_read ? av[q] : ev[q]);
-                    const float gj = __fmul_rn(g, ((mw >> cl) & 1u) ? 1.0f : 0.0f);
-                    const int bp = cl * BITS;
+                    const uint32_t mw = c < 32 ? pm0 : pm1;
+                    const float gj = __fmul_rn(g, ((mw >> (c & 31)) & 1u) ? 1.0f : 0.0f);
+                    const int bp = c * BITS;
                     const uint32_t code = (pcw[bp >> 5] >> (bp & 31)) & CM;
                     const float hv = ok ? lut_entry<BITS>(rg, zz, (int)code) : 0.0f;
-                    float gh, gl, hh, hl;
-                    tc::split_tf32(gj, gh, gl);
+                    float hh, hl;
+                    tc::split_tf32(gj, gh[q], gl[q]);
                     tc::split_tf32(hv, hh, hl);
-                    const uint32_t oa = tc::tile_off(r, c, M) / 4;     // Ag  (r, k=c)
-                    const uint32_t ob = tc::tile_off(c, r, D) / 4;     // Ah', Bg' (c, k=r)
-                    ag_hi[oa] = gh; ag_lo[oa] = gl;
-                    bg_hi[ob] = gh; bg_lo[ob] = gl;
+                    const uint32_t ob = toff_t(c, r) / 4;              // Ah', Bg' (c, k=r)
+                    bg_hi[ob] = gh[q]; bg_lo[ob] = gl[q];
                     ah_hi[ob] = hh; ah_lo[ob] = hl;
                 }
+                const uint32_t oa = tc::tile_off(r, 8 * j + 4 * h, M) / 4;   // Ag (r, k=c..c+3): 16 B
+                *reinterpret_cast<float4 *>(ag_hi + oa) = make_float4(gh[0], gh[1], gh[2], gh[3]);
+                *reinterpret_cast<float4 *>(ag_lo + oa) = make_float4(gl[0], gl[1], gl[2], gl[3]);
             }
         }
         tc::fence_proxy_async();
@@ -128,7 +140,7 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         if (t == 0) {
             tc::fence_after();
             tc::mma_3xtf32<M, D, D>(tmem, ag_hi, ag_lo, th_hi, th_lo);
-            constexpr uint32_t LBO = (D / 8) * 128;
+            constexpr uint32_t LBO = kLboT;                          // padded K-quad stride
             constexpr uint32_t idesc = tc::idesc_tf32(D, D);         // M = 64, N = 64
             const uint32_t sah = tc::smem_u32(ah_hi), sal = tc::smem_u32(ah_lo);
             const uint32_t sbh = tc::smem_u32(bg_hi), sbl = tc::smem_u32(bg_lo);

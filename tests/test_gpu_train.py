@@ -486,9 +486,10 @@ def test_scatter_rows_multi_matches_reference_dense_sums():
     assert np.array_equal(one.cpu().numpy().view(np.uint32), s0.view(np.uint32))
 
 
-def test_tcgen05_layer_backward_matches_fp64_subprocess():
-    """The opt-in tcgen05 backward (KGQ_BWD_TC=1, kgq_backward_tc.cu: 3xTF32
-    MMAs, TMEM accumulators) against float64 on a fresh process."""
+def test_ffma_layer_backward_matches_fp64_subprocess():
+    """The FFMA backward kernel (KGQ_BWD_TC=0; d=64 defaults to the tcgen05
+    kernel, which the in-process backward tests cover) against float64 on a
+    fresh process."""
     import subprocess
     import sys
     code = r"""
@@ -515,6 +516,6 @@ print("ok")
 """
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, KGQ_BWD_TC="1")
+    env = dict(os.environ, KGQ_BWD_TC="0")
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
