@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[1], the largest single-GPU microbench shape):
 fp32 activations 64M x 128 (32 GB, far larger than the 126 MB L2, so no L2
 flush is needed), INT2, group 64, stochastic rounding with the fast
-Philox4x32 noise.  One step = one fused quantize+pack (K1) plus one
+Philox4x32-7 noise.  One step = one fused quantize+pack (K1) plus one
 unpack+dequantize (K2) pass over the whole tensor through the public API.
 
 Bytes are algorithmic: per element 4 (fp32) + b/8 (codes)

@@ -47,7 +47,7 @@ enum kgq_status {
 /* Rounding modes (QuantConfig.rounding, quantize.py:25-26, :48-49). */
 enum kgq_rounding {
     KGQ_ROUND_NEAREST = 0,    /* np.rint, round-half-even (quantize.py:129-130)           */
-    KGQ_ROUND_SR_FAST = 1,    /* stochastic, Philox4x32-10 16-bit uniforms    */
+    KGQ_ROUND_SR_FAST = 1,    /* stochastic, Philox4x32-7 16-bit uniforms     */
     KGQ_ROUND_SR_COMPAT = 2,  /* stochastic, numpy Philox4x64-10 stream (quantize.py:61-102) */
     KGQ_ROUND_SR_NOISE = 3    /* stochastic, caller-supplied float64 uniforms (test seam)  */
 };

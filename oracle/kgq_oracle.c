@@ -20,7 +20,7 @@
 #include <string.h>
 
 #define KGQ_MODE_NEAREST 0      /* np.rint, quantize.py:129-130            */
-#define KGQ_MODE_SR_FAST 1      /* Philox4x32-10, 16-bit uniforms (ours)   */
+#define KGQ_MODE_SR_FAST 1      /* Philox4x32-7, 16-bit uniforms (ours)    */
 #define KGQ_MODE_SR_COMPAT 2    /* numpy Philox4x64-10 stream, quantize.py:61-102 */
 #define KGQ_MODE_SR_NOISE 3     /* caller-supplied float64 uniforms        */
 
@@ -49,11 +49,13 @@ void oracle_philox4x64_10(const uint64_t ctr_in[4], const uint64_t key_in[2], ui
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* Philox4x32-10 (Random123 constants).  Used by our "fast" SR mode.       */
-void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+/* Philox4x32-R (Random123 constants).  R = 10 is the Random123 reference
+ * (pinned by its KAT); our "fast" SR mode uses R = 7.          */
+#define ORACLE_FAST_ROUNDS 7
+void oracle_philox4x32_r(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4], int rounds) {
     uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
     uint32_t k0 = key_in[0], k1 = key_in[1];
-    for (int r = 0; r < 10; r++) {
+    for (int r = 0; r < rounds; r++) {
         if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
         uint64_t p0 = (uint64_t)0xD2511F53u * c0;
         uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
@@ -62,6 +64,10 @@ void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], ui
         c0 = n0; c1 = n1; c2 = n2; c3 = n3;
     }
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    oracle_philox4x32_r(ctr_in, key_in, out, 10);
 }
 
 /* Compat stream: element k of quantization group g (group = row of the
@@ -85,7 +91,7 @@ uint32_t oracle_fast_u16(uint64_t seed, uint64_t tid, uint64_t g, int64_t k) {
     uint32_t ctr[4] = {call, (uint32_t)g, (uint32_t)(g >> 32), (uint32_t)tid};
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32) ^ (uint32_t)(tid >> 32)};
     uint32_t out[4];
-    oracle_philox4x32_10(ctr, key, out);
+    oracle_philox4x32_r(ctr, key, out, ORACLE_FAST_ROUNDS);
     return (out[k & 3] >> (16 * ((k >> 4) & 1))) & 0xFFFFu;
 }
 

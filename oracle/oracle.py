@@ -9,7 +9,7 @@ Two layers:
 
 * ``kgq_oracle.c`` (ctypes, built by ``oracle/Makefile``): bit-exact fp32
   restatement of the reference quantizer (quantize.py:177-247), numpy's
-  Philox4x64-10 stream (quantize.py:61-102), our fast Philox4x32-10 noise,
+  Philox4x64-10 stream (quantize.py:61-102), our fast Philox4x32-7 noise,
   the ordered CSR SpMM (tensorops.py:37-50) and ReLU + bit mask
   (tensorops.py:57-92).
 * numpy restatements of the dense engine (tape.py:193-253 accumulation order,
@@ -54,6 +54,7 @@ def lib():
         i64, u64, i32 = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
         L.oracle_philox4x64_10.argtypes = [P, P, P]
         L.oracle_philox4x32_10.argtypes = [P, P, P]
+        L.oracle_philox4x32_r.argtypes = [P, P, P, i32]
         L.oracle_fast_noise_u16.argtypes = [u64, u64, i64, i64, P]
         L.oracle_compat_noise_raw53.argtypes = [u64, u64, i64, i64, P]
         L.oracle_quantize.argtypes = [P, i64, i64, i32, i32, u64, u64, i64, P, P, P, P, i32]
@@ -84,6 +85,17 @@ def philox4x32_10(ctr, key):
     out = np.zeros(4, dtype=np.uint32)
     lib().oracle_philox4x32_10(_p(c), _p(k), _p(out))
     return out
+
+
+def philox4x32(ctr, key, rounds: int):
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().oracle_philox4x32_r(_p(c), _p(k), _p(out), rounds)
+    return out
+
+
+FAST_ROUNDS = 7     # the fast SR stream: Philox4x32-7
 
 
 def fast_noise_u16(seed: int, tid: int, n_groups: int, group: int) -> np.ndarray:

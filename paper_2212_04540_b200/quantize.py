@@ -17,7 +17,7 @@ reference's behaviour where it is defined:
   of the ``(-1, G)`` view of the row-major tensor.
 * ``QuantConfig.rng``: ``"compat"`` draws the reference's numpy
   Philox4x64-10 stream bit-for-bit (quantize.py:61-102); ``"fast"`` (default)
-  draws Philox4x32-10 16-bit uniforms and is checked bit-exact
+  draws Philox4x32-7 16-bit uniforms and is checked bit-exact
   against the reference through the exported-noise route.
 """
 

@@ -114,3 +114,35 @@ def test_dense_oracle_matches_reference_tape_b32():
         assert loss == pytest.approx(float(z[pre + "loss"]), rel=1e-6)
         for name, g in grads.items():
             np.testing.assert_allclose(g, z[pre + "grad_" + name], rtol=1e-5, atol=1e-7)
+
+
+def _philox4x32_py(ctr, key, rounds):
+    """Random123 Philox4x32 round function restated in plain Python."""
+    c0, c1, c2, c3 = (int(v) for v in ctr)
+    k0, k1 = (int(v) for v in key)
+    m = 0xFFFFFFFF
+    for r in range(rounds):
+        if r:
+            k0, k1 = (k0 + 0x9E3779B9) & m, (k1 + 0xBB67AE85) & m
+        p0, p1 = 0xD2511F53 * c0, 0xCD9E8D57 * c2
+        c0, c1, c2, c3 = ((p1 >> 32) ^ c1 ^ k0) & m, p1 & m, ((p0 >> 32) ^ c3 ^ k1) & m, p0 & m
+    return [c0, c1, c2, c3]
+
+
+def test_fast_stream_is_philox4x32_7():
+    """The fast SR stream = Philox4x32 with 7 rounds: the C oracle's
+    R-round primitive equals the plain restatement (which at R = 10 reproduces
+    the Random123 KAT above), and fast_noise_u16 draws element k of group g
+    from call 4(k>>5)+((k>>2)&3), word k&3, half (k>>4)&1."""
+    assert orc.FAST_ROUNDS == 7
+    assert _philox4x32_py([0, 0, 0, 0], [0, 0], 10) == [int(v) for v in orc.philox4x32_10([0, 0, 0, 0], [0, 0])]
+    for ctr, key in (([1, 2, 3, 4], [5, 6]), ([0xFFFFFFFF, 7, 0, 9], [0xDEADBEEF, 0x12345678])):
+        assert [int(v) for v in orc.philox4x32(ctr, key, 7)] == _philox4x32_py(ctr, key, 7)
+    seed, tid = 0x0123456789ABCDEF, 0xFEDCBA9876543210
+    u = orc.fast_noise_u16(seed, tid, 3, 64)
+    key = [seed & 0xFFFFFFFF, ((seed >> 32) ^ (tid >> 32)) & 0xFFFFFFFF]
+    for g in range(3):
+        for k in (0, 5, 17, 33, 63):
+            call = 4 * (k >> 5) + ((k >> 2) & 3)
+            w = _philox4x32_py([call, g, 0, tid & 0xFFFFFFFF], key, 7)[k & 3]
+            assert int(u[g, k]) == (w >> (16 * ((k >> 4) & 1))) & 0xFFFF
