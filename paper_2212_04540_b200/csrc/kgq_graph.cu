@@ -595,22 +595,32 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
     const int fa = rg_f4a<D, true>(gl), fb = rg_f4b<D, true>(gl);
     const int tc = t % TC, tr = t / TC;
     const int64_t n_tiles = (n_rows + ROWS - 1) / ROWS;
+    constexpr int NP = ROWS / (8 * RPW);            // passes per tile (2)
+    // register prefetch: the next pass's two float4 are in flight while the
+    // current pass quantizes (and, across tiles, while the GEMM runs)
+    float4 nh[2];
+    auto fetch = [&](int64_t tl, int ps) {
+        const int64_t rw = tl * ROWS + (ps * 8 + warp) * RPW + grp;
+        if (tl < n_tiles && rw < n_rows) {
+            const float4 *src = reinterpret_cast<const float4 *>(hin + rw * D);
+            nh[0] = __ldg(src + fa);
+            nh[1] = __ldg(src + fb);
+        } else {
+            nh[0] = nh[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    fetch(blockIdx.x, 0);
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t r0 = tile * ROWS;
         // ---- 1. load + quantize + stage (ROWS / (8 * RPW) = 2 passes) ----
 #pragma unroll
-        for (int pass = 0; pass < ROWS / (8 * RPW); pass++) {
+        for (int pass = 0; pass < NP; pass++) {
             const int lr = (pass * 8 + warp) * RPW + grp;
             const int64_t row = r0 + lr;
             const bool active = row < n_rows;
-            float4 h[2];
-            if (active) {
-                const float4 *src = reinterpret_cast<const float4 *>(hin + row * D);
-                h[0] = __ldg(src + fa);
-                h[1] = __ldg(src + fb);
-            } else {
-                h[0] = h[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+            float4 h[2] = {nh[0], nh[1]};
+            if (pass + 1 < NP) fetch(tile, pass + 1);
+            else fetch(tile + gridDim.x, 0);
             light_row_quantize<D, BITS, MODE>(h, active, active ? row : 0, gl, fk, seed, tid, row_offset,
                                               codes, ranges, offsets);
             const float hv[8] = {h[0].x, h[0].y, h[0].z, h[0].w, h[1].x, h[1].y, h[1].z, h[1].w};
