@@ -9,8 +9,8 @@ every layer's activations.  Per layer and direction there is one exchange:
     params  : dtheta all-reduce (L*d*d floats), E0 rows stay local
 
 plus one exchange of the 3*B readout rows of the batch (all-reduce of an
-owner-filled B x d block) so every rank evaluates the (tiny) BPR head on the
-same batch.  The gathers can target a padded [world*max_count] layout whose
+owner-filled 3B x d block, the readout summed over layers at those rows only)
+so every rank evaluates the (tiny) BPR head on the same batch.  The gathers can target a padded [world*max_count] layout whose
 row ids the local CSR is remapped to once, so the collective writes the
 SpMM's input directly (no concatenation copy of a full N x d tensor).  The quantization noise is keyed by GLOBAL row
 (``row_offset``), so the forward pass -- activations, codes, ranges, masks --
@@ -280,15 +280,25 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
 
     saved = []
     e_local = e0_local
-    readout_local = None
+    # the sum readout is only read at the batch rows: accumulate those rows
+    # layer by layer ((E1 + E2) + E3, the reference's order, on 3B x d
+    # instead of N x d), owner-filled, then one exact all-reduce
+    idx = torch.cat([users, pos, neg])
+    n_loc = e0_local.shape[0]
+    own = (idx >= lo) & (idx < lo + n_loc)
+    li = (idx[own] - lo).to(torch.int64)
+    acc_rows = None
     for theta in thetas:
         e_full = gather(e_local)
         e_next, mask, q, _ = ops.graph_conv(a_local, e_full, theta, cfg, stream, row_offset=lo)
         saved.append((mask, q))
-        readout_local = e_next if readout_local is None else readout_local + e_next
+        r_l = e_next[li]
+        acc_rows = r_l if acc_rows is None else acc_rows + r_l
         e_local = e_next
     b = users.shape[0]
-    rows = comm.gather_index_rows(readout_local, lo, torch.cat([users, pos, neg]))
+    block = e_local.new_zeros((idx.shape[0], e_local.shape[1]))
+    block[own] = acc_rows
+    rows = comm.all_reduce_sum(block)
     u, p, n = rows[:b], rows[b:2 * b], rows[2 * b:]
     loss, margins = ops.bpr_forward(u, p, n, l2)
     qu, qp, qn = (ops.quantize(t, cfg, stream) for t in (u, p, n))
