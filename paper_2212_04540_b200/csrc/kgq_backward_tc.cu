@@ -3,8 +3,9 @@
 //
 //   g_j = (g_read + g_e) * mask;  dH = g_j . theta^T;  dtheta += Hhat^T . g_j
 //
-// One CTA per SM walks 128-row tiles.  All 256 threads stage the tile: thread
-// t owns row t/2, columns 32*(t&1)..+31, forms g_j and the IEEE-dequantized
+// One CTA (512 threads) per SM walks 128-row tiles.  All threads stage the
+// tile: thread t owns row t/4 and column quads 4j + (t&3), forms g_j and the
+// IEEE-dequantized
 // Hhat in registers and writes their 3xTF32 hi/lo splits into shared memory in
 // the K-major interleaved layout (kgq_tc.cuh) three times over:
 //   Ag  (r, k=c)        A of dH       (M = 128 rows, K = 64)
@@ -30,18 +31,20 @@ constexpr int kTcD = 64;
 // (1024 + 16): with thread (row r, column quads 2j+h) the 32 scalar stores of
 // a warp then hit 32 distinct banks.  Ag is written with 128-bit stores.
 constexpr uint32_t kLboT = 1040;
+constexpr uint32_t kLboA = 2080;     // Ag K-quad stride: 2048 + 32 B spreads a row's 4 quarter-threads
+constexpr int kBtcThreads = 512;     // 4 threads per row: 16 warps keep more loads in flight
 struct BwdTcSmem {
-    static constexpr int AG = kTcRows * kTcD;                              // Ag hi or lo (floats)
+    static constexpr int AG = ((kTcD / 4 - 1) * kLboA + 2048) / 4;          // Ag hi or lo (floats)
     static constexpr int AT = ((kTcRows / 4 - 1) * kLboT + 1024) / 4;      // Ah'/Bg' hi or lo (floats)
     static constexpr int TH = kTcD * kTcD;
-    static constexpr size_t bytes = (size_t)(2 * TH + 2 * AG + 4 * AT) * sizeof(float);   // 225.9 KB
+    static constexpr size_t bytes = (size_t)(2 * TH + 2 * AG + 4 * AT) * sizeof(float);   // 226.9 KB
 };
 __device__ __forceinline__ uint32_t toff_t(int c, int r) {   // (row c, k = r), padded K-quad stride
     return (uint32_t)((r >> 2) * kLboT + (c >> 3) * 128 + (c & 7) * 16 + (r & 3) * 4);
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kBtcThreads, 1)
 layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
                          const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
                          const float *__restrict__ ranges, const float *__restrict__ offsets,
@@ -59,7 +62,7 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
 
     // theta^T split: B(n, k) = theta[n][k]
-    for (int i = t; i < D * D; i += 256) {
+    for (int i = t; i < D * D; i += kBtcThreads) {
         const int n = i / D, k = i % D;
         float hi, lo;
         tc::split_tf32(__ldg(theta + i), hi, lo);
@@ -73,14 +76,14 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     tc::fence_after();
     const uint32_t tmem = tmem_base;
 
-    // staging: thread owns row r = t/2 and the column quads 2j + h (j = 0..7)
-    const int r = t >> 1, h = t & 1;
+    // staging: thread owns row r = t/4 and the column quads 4j + h (j = 0..3)
+    const int r = t >> 2, h = t & 3;
     uint32_t phase = 0;
     bool first = true;
     const int64_t n_tiles = (rows + M - 1) / M;
     // register prefetch of one tile's inputs (issued while the previous
     // tile's MMAs run, so the loads overlap the tensor-core work)
-    float4 pa[8], pe[8];
+    float4 pa[4], pe[4];
     float prg = 0.f, pzz = 0.f;
     uint32_t pm0 = 0u, pm1 = 0u, pcw[2 * BITS];
     auto load = [&](int64_t tl) {
@@ -96,9 +99,9 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D);
         const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D);
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            pa[j] = (ok && g_read) ? __ldg(gr4 + 2 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
-            pe[j] = (ok && g_e) ? __ldg(ge4 + 2 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < 4; j++) {
+            pa[j] = (ok && g_read) ? __ldg(gr4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pe[j] = (ok && g_e) ? __ldg(ge4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
     load(blockIdx.x);
@@ -109,12 +112,12 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         {
             const float rg = prg, zz = pzz;
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < 4; j++) {
                 const float av[4] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w}, ev[4] = {pe[j].x, pe[j].y, pe[j].z, pe[j].w};
                 float gh[4], gl[4];
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    const int c = 8 * j + 4 * h + q;
+                    const int c = 16 * j + 4 * h + q;
                     // g = g_read + g_e in the reference's routing order (tape.py:204-209)
                     const float g = (g_read && g_e) ? __fadd_rn(av[q], ev[q]) : (g_read ? av[q] : ev[q]);
                     const uint32_t mw = c < 32 ? pm0 : pm1;
@@ -129,7 +132,7 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
                     bg_hi[ob] = gh[q]; bg_lo[ob] = gl[q];
                     ah_hi[ob] = hh; ah_lo[ob] = hl;
                 }
-                const uint32_t oa = tc::tile_off(r, 8 * j + 4 * h, M) / 4;   // Ag (r, k=c..c+3): 16 B
+                const uint32_t oa = ((4 * j + h) * kLboA + (r >> 3) * 128 + (r & 7) * 16) / 4;   // Ag (r, quad)
                 *reinterpret_cast<float4 *>(ag_hi + oa) = make_float4(gh[0], gh[1], gh[2], gh[3]);
                 *reinterpret_cast<float4 *>(ag_lo + oa) = make_float4(gl[0], gl[1], gl[2], gl[3]);
             }
@@ -139,7 +142,23 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         // ---- 2. MMAs: dH (cols 0..63), dtheta accumulate (cols 64..127) ----
         if (t == 0) {
             tc::fence_after();
-            tc::mma_3xtf32<M, D, D>(tmem, ag_hi, ag_lo, th_hi, th_lo);
+            {   // dH: A = Ag (K-quad stride kLboA), B = theta^T split (standard stride)
+                constexpr uint32_t idA = tc::idesc_tf32(M, D), LBO_B = (D / 8) * 128;
+                const uint32_t gah = tc::smem_u32(ag_hi), gal = tc::smem_u32(ag_lo);
+                const uint32_t tbh = tc::smem_u32(th_hi), tbl = tc::smem_u32(th_lo);
+                uint32_t acc0 = 0;
+#pragma unroll
+                for (int pass = 0; pass < 3; pass++) {
+                    const uint32_t sa = pass == 0 ? gal : gah;
+                    const uint32_t sb = pass == 1 ? tbl : tbh;
+#pragma unroll
+                    for (int st = 0; st < D / 8; st++) {
+                        tc::mma_tf32(tmem, tc::smem_desc(sa + 2 * st * kLboA, kLboA, 128),
+                                     tc::smem_desc(sb + 2 * st * LBO_B, LBO_B, 128), idA, acc0);
+                        acc0 = 1u;
+                    }
+                }
+            }
             constexpr uint32_t LBO = kLboT;                          // padded K-quad stride
             constexpr uint32_t idesc = tc::idesc_tf32(D, D);         // M = 64, N = 64
             const uint32_t sah = tc::smem_u32(ah_hi), sal = tc::smem_u32(ah_lo);
@@ -163,8 +182,8 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         tc::mbar_wait(&mbar, phase);
         phase ^= 1u;
         tc::fence_after();
-        // ---- 3. drain dH: warp w -> lanes 32*(w%4).., columns 32*(w/4).. ----
-        {
+        // ---- 3. drain dH: warp w < 8 -> lanes 32*(w%4).., columns 32*(w/4).. ----
+        if (warp < 8) {
             const int q = warp & 3, cb = (warp >> 2) * 32;
             float v[32];
             tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
@@ -220,7 +239,7 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
             if (e != cudaSuccess) return kgq_set_cuda_error(e);                                    \
             attr[B] = true;                                                                        \
         }                                                                                          \
-        layer_backward_tc_kernel<B><<<grid, 256, BwdTcSmem::bytes, s>>>(g_read, g_e, mask, codes,   \
+        layer_backward_tc_kernel<B><<<grid, kBtcThreads, BwdTcSmem::bytes, s>>>(g_read, g_e, mask, codes, \
                                                                         ranges, offsets, rows, theta, dh, partial); \
     } while (0)
     switch (bits) {
