@@ -176,15 +176,67 @@ scatter_rows_multi_kernel(const int64_t *__restrict__ order, const int32_t *__re
     }
 }
 
+// Sort-free variant (order == NULL, m <= 16384): warp w takes position w;
+// it proceeds only if no earlier position holds the same row (a 32-wide
+// ballot scan), then walks the later positions in order, so each row is
+// still folded in position order by exactly one warp.  O(m^2 / 32) compares,
+// all L1/L2-resident for a training batch (m = 3B).
+__global__ void __launch_bounds__(256)
+scatter_rows_multi_nosort_kernel(const int32_t *__restrict__ idx, int64_t m, ListEnds list_end, int n_lists,
+                                 const float *__restrict__ g, int d, float *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= m) return;
+    const int32_t row = __ldg(idx + i);
+    for (int64_t j0 = 0; j0 < i; j0 += 32) {       // an earlier occurrence owns the row
+        const int64_t j = j0 + lane;
+        const bool hit = j < i && __ldg(idx + j) == row;
+        if (__ballot_sync(0xffffffffu, hit)) return;
+    }
+    for (int f0 = 0; f0 < d; f0 += 32) {
+        const int f = f0 + lane;
+        float total = 0.0f, acc = 0.0f;
+        int li = 0;
+        for (int64_t j0 = i; j0 < m; j0 += 32) {
+            const int64_t jl = j0 + lane;
+            uint32_t hits = __ballot_sync(0xffffffffu, jl < m && __ldg(idx + jl) == row);
+            while (hits) {
+                const int b = __ffs(hits) - 1;
+                hits &= hits - 1;
+                const int64_t pos = j0 + b;
+                int l = 0;
+                while (l + 1 < n_lists && pos >= list_end.e[l]) l++;
+                for (; li < l; li++) {
+                    total = li == 0 ? acc : __fadd_rn(total, acc);
+                    acc = 0.0f;
+                }
+                if (f < d) acc = __fadd_rn(acc, __ldg(g + pos * d + f));
+            }
+        }
+        for (; li < n_lists; li++) {
+            total = li == 0 ? acc : __fadd_rn(total, acc);
+            acc = 0.0f;
+        }
+        if (f < d) out[(int64_t)row * d + f] = total;
+    }
+}
+
 extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx, int64_t m,
                                           const int64_t *list_end, int32_t n_lists, const float *g,
                                           int32_t d, float *out, void *stream) {
     if (m < 0 || d < 1 || n_lists < 1 || n_lists > kMaxScatterLists || !list_end) return KGQ_ERR_INVALID_ARG;
     if (m == 0) return KGQ_OK;
-    if (!order || !idx || !g || !out) return KGQ_ERR_INVALID_ARG;
+    if (!idx || !g || !out) return KGQ_ERR_INVALID_ARG;
     ListEnds ends;                                  // host array -> kernel parameter (graph-capturable)
     for (int i = 0; i < kMaxScatterLists; i++) ends.e[i] = i < n_lists ? list_end[i] : m;
     const int64_t blocks = (m * 32 + 255) / 256;
+    if (!order) {
+        if (m > 16384) return KGQ_ERR_INVALID_ARG;  // sort-free path is quadratic: sort first
+        scatter_rows_multi_nosort_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(idx, m, ends, n_lists,
+                                                                                      g, d, out);
+        KGQ_LAUNCH_CHECK();
+        return KGQ_OK;
+    }
     scatter_rows_multi_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(order, idx, m, ends, n_lists,
                                                                            g, d, out);
     KGQ_LAUNCH_CHECK();

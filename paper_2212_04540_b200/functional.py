@@ -232,11 +232,13 @@ def scatter_rows_multi(src_rows: int, idxs, gs) -> torch.Tensor:
     if m == 0:
         return out
     ends = np.ascontiguousarray(np.cumsum([i.numel() for i in idxs]), dtype=np.int64)   # host, by value
-    key = idx.to(torch.int64) * m + torch.arange(m, device=dev, dtype=torch.int64)
-    order = torch.sort(key).indices
+    order = None
+    if m > 16384:        # the sort-free kernel is quadratic in m
+        key = idx.to(torch.int64) * m + torch.arange(m, device=dev, dtype=torch.int64)
+        order = torch.sort(key).indices
     if len(idxs) > 8:
         raise ValueError("at most 8 gathers per scatter")
-    st = _lib.load().kgq_scatter_rows_multi_f32(order.data_ptr(), idx.data_ptr(), m, ends.ctypes.data, len(idxs),
+    st = _lib.load().kgq_scatter_rows_multi_f32(_lib.ptr(order), idx.data_ptr(), m, ends.ctypes.data, len(idxs),
                                                 g.data_ptr(), d, out.data_ptr(), _lib.stream_ptr(dev))
     _lib.check(st, "kgq_scatter_rows_multi_f32")
     return out

@@ -480,6 +480,18 @@ def test_scatter_rows_multi_matches_reference_dense_sums():
     out = F.scatter_rows_multi(rows, [torch.from_numpy(i).cuda() for i in idxs],
                                [torch.from_numpy(g).cuda() for g in gs])
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    # the sort path (m > 16384) gives the same bytes
+    big_i = [np.tile(i, 30) for i in idxs]
+    big_g = [np.tile(g, (30, 1)) for g in gs]
+    ref2 = None
+    for i, g in zip(big_i, big_g):
+        s2 = np.zeros((rows, d), np.float32)
+        np.add.at(s2, i, g)
+        ref2 = s2 if ref2 is None else ref2 + s2
+    out2 = F.scatter_rows_multi(rows, [torch.from_numpy(i).cuda() for i in big_i],
+                                [torch.from_numpy(g).cuda() for g in big_g])
+    assert sum(len(i) for i in big_i) > 16384
+    assert np.array_equal(out2.cpu().numpy().view(np.uint32), ref2.view(np.uint32))
     one = F.scatter_rows(rows, torch.from_numpy(idxs[0]).cuda(), torch.from_numpy(gs[0]).cuda())
     s0 = np.zeros((rows, d), np.float32)
     np.add.at(s0, idxs[0], gs[0])
