@@ -227,7 +227,8 @@ KGQ_API int kgq_bpr_backward_f32(const float *g, const float *margins, const flo
  * list_end[i]: a HOST int64 array, n_lists <= 8, passed by value to the
  * kernel so the call is graph-capturable); order = positions sorted by
  * (idx, position), device int64, or NULL for the sort-free kernel (m <= 16384;
- * a warp per first occurrence); rows in no list are not written (zero first). */
+ * a warp per first occurrence); rows in no list are not written (zero first);
+ * negative indices are skipped (rows owned by another rank). */
 KGQ_API int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx, int64_t m,
                                const int64_t *list_end, int32_t n_lists, const float *g,
                                int32_t d, float *out, void *stream);

@@ -152,6 +152,7 @@ scatter_rows_multi_kernel(const int64_t *__restrict__ order, const int32_t *__re
     if (i >= m) return;
     const int64_t pos0 = __ldg(order + i);
     const int32_t row = __ldg(idx + pos0);
+    if (row < 0) return;                                             // not owned here: skipped
     if (i > 0 && __ldg(idx + __ldg(order + i - 1)) == row) return;   // not the first occurrence
     for (int f0 = 0; f0 < d; f0 += 32) {
         const int f = f0 + lane;
@@ -188,6 +189,7 @@ scatter_rows_multi_nosort_kernel(const int32_t *__restrict__ idx, int64_t m, Lis
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= m) return;
     const int32_t row = __ldg(idx + i);
+    if (row < 0) return;                            // not owned here: skipped
     for (int64_t j0 = 0; j0 < i; j0 += 32) {       // an earlier occurrence owns the row
         const int64_t j = j0 + lane;
         const bool hit = j < i && __ldg(idx + j) == row;

@@ -207,6 +207,7 @@ class GpuOps:
     quantize = staticmethod(quantize_tensor)
     dequantize = staticmethod(dequantize_tensor)
     scatter_rows = staticmethod(F.scatter_rows)
+    scatter_rows_multi = staticmethod(F.scatter_rows_multi)
     bpr_forward = staticmethod(F.bpr_forward)
     bpr_backward = staticmethod(F.bpr_backward)
 
@@ -283,21 +284,21 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     # the sum readout is only read at the batch rows: accumulate those rows
     # layer by layer ((E1 + E2) + E3, the reference's order, on 3B x d
     # instead of N x d), owner-filled, then one exact all-reduce
+    # (no boolean indexing: fixed shapes, no host synchronisation)
     idx = torch.cat([users, pos, neg])
     n_loc = e0_local.shape[0]
     own = (idx >= lo) & (idx < lo + n_loc)
-    li = (idx[own] - lo).to(torch.int64)
+    li = torch.clamp(idx - lo, 0, max(n_loc - 1, 0)).to(torch.int64)
     acc_rows = None
     for theta in thetas:
         e_full = gather(e_local)
         e_next, mask, q, _ = ops.graph_conv(a_local, e_full, theta, cfg, stream, row_offset=lo)
         saved.append((mask, q))
-        r_l = e_next[li]
+        r_l = e_next.index_select(0, li)
         acc_rows = r_l if acc_rows is None else acc_rows + r_l
         e_local = e_next
     b = users.shape[0]
-    block = e_local.new_zeros((idx.shape[0], e_local.shape[1]))
-    block[own] = acc_rows
+    block = torch.where(own[:, None], acc_rows, torch.zeros((), dtype=acc_rows.dtype, device=acc_rows.device))
     rows = comm.all_reduce_sum(block)
     u, p, n = rows[:b], rows[b:2 * b], rows[2 * b:]
     loss, margins = ops.bpr_forward(u, p, n, l2)
@@ -305,14 +306,14 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     one = torch.ones((), dtype=u.dtype, device=u.device)
     gu, gp, gn = ops.bpr_backward(one, margins, ops.dequantize(qu), ops.dequantize(qp),
                                 ops.dequantize(qn), l2, u.shape[0])
-    # readout gradient rows owned here: (scat_n + scat_p) + scat_u (reference.py:59-67)
+    # readout gradient rows owned here: (scat_n + scat_p) + scat_u (reference.py:59-67),
+    # one deterministic scatter; rows owned by other ranks carry index -1 (skipped)
     hi = lo + counts[part.rank]
 
-    def local_scatter(idx, g):
-        sel = (idx >= lo) & (idx < hi)
-        return ops.scatter_rows(hi - lo, (idx[sel] - lo).to(torch.int32), g[sel])
+    def local_idx(ix):
+        return torch.where((ix >= lo) & (ix < hi), ix - lo, torch.full_like(ix, -1)).to(torch.int32)
 
-    g_read = (local_scatter(neg, gn) + local_scatter(pos, gp)) + local_scatter(users, gu)
+    g_read = ops.scatter_rows_multi(hi - lo, [local_idx(neg), local_idx(pos), local_idx(users)], [gn, gp, gu])
     g_e = None
     dthetas = [None] * len(thetas)
     for i in range(len(thetas) - 1, -1, -1):

@@ -98,6 +98,18 @@ class OracleOps:
                 g * (coef * uh + reg * nh))
 
     @staticmethod
+    def scatter_rows_multi(rows, idxs, gs):
+        """(s_0 + s_1) + ... with s_i = np.add.at over list i; index -1 skipped."""
+        total = None
+        for idx, g in zip(idxs, gs):
+            ix = idx.numpy().astype(np.int64)
+            keep = ix >= 0
+            s = np.zeros((rows, g.shape[1]), dtype=np.float32)
+            np.add.at(s, ix[keep], g.numpy()[keep])
+            total = s if total is None else total + s
+        return torch.from_numpy(total)
+
+    @staticmethod
     def scatter_rows(rows, idx, g):
         out = np.zeros((rows, g.shape[1]), dtype=np.float32)
         np.add.at(out, idx.numpy().astype(np.int64), g.numpy())
