@@ -229,7 +229,7 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
                        f"{len(ds.train)} train pairs; KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
            "steps_per_epoch": steps_per_epoch, "n_gpus": world}
     res = {}
-    for bits in ((2, 32) if with_fp32 else (2,)):
+    for bits in ((2, 4, 32) if with_fp32 else (2,)):
         q = kgq.QuantConfig(bits=bits)
         mcfg = ModelConfig(layers=3, dim=64, quant=q)
         cfg = TrainConfig(quant=q)
@@ -297,6 +297,15 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
     if with_fp32:
         ms32 = res[32][0]
         out.update({"fp32_ms_per_step": round(ms32, 3), "int2_time_overhead_vs_fp32": round(ms2 / ms32 - 1.0, 4)})
+    if 4 in res:
+        ms4, mem4, _, ep4 = res[4]
+        out["int4"] = {"ms_per_step": round(ms4, 3)}
+        if ep4 is not None:
+            out["int4"]["epoch_s"] = round(ep4, 3)
+        if mem4 is not None:
+            out["int4"]["activation_MB_incl_adjacency"] = round(mem4["activation_bytes_peak"] / 1e6, 3)
+            out["int4"]["activation_MB_excl_adjacency"] = round(mem4["activation_bytes_excl_adjacency"] / 1e6, 3)
+            out["int4"]["ratio_excl_adjacency"] = round(mem4["compression_ratio_excl_adjacency"], 3)
     if world == 1 and rank == 0 and not args.skip_cpu and with_cpu:
         # CPU port of the reference step (oracle/oracle.py dense engine: scipy
         # CSR spmm + numpy GEMMs, the reference's op structure), 2 steps
