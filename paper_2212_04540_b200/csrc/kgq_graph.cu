@@ -29,6 +29,20 @@ namespace kgq {
 
 constexpr int kCH = 32;             // neighbours per ring stage (heavy path)
 
+// The CSR column ids / values and the SpMM output are streamed once per call;
+// loading / storing them evict-first (.cs) keeps the gathered embedding table
+// resident in L2 (table + CSR + output exceed the 126 MB L2 at Amazon shape).
+#ifndef KGQ_SPMM_CS
+#define KGQ_SPMM_CS 1
+#endif
+#if KGQ_SPMM_CS
+#define KGQ_LD_STREAM(p) __ldcs(p)
+#define KGQ_ST_STREAM(p, v) __stcs((p), (v))
+#else
+#define KGQ_LD_STREAM(p) __ldg(p)
+#define KGQ_ST_STREAM(p, v) (*(p) = (v))
+#endif
+
 template <int D>
 struct RG {
     static constexpr int LPR = D / 8;      // lanes per row (light path)
@@ -82,16 +96,16 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
     int32_t nx_col = 0;
     float nx_val = 0.0f;
     if (gl < len) {
-        nx_col = __ldg(indices + beg + gl);
-        nx_val = __ldg(vals + beg + gl);
+        nx_col = KGQ_LD_STREAM(indices + beg + gl);
+        nx_val = KGQ_LD_STREAM(vals + beg + gl);
     }
     for (int base = 0; base < maxlen; base += LPR) {
         const int cnt = min(LPR, len - base);         // may be <= 0 for short rows
         const int32_t my_col = nx_col;
         const float my_val = nx_val;
         if (gl < len - base - LPR) {                  // prefetch the next LPR column ids
-            nx_col = __ldg(indices + beg + base + LPR + gl);
-            nx_val = __ldg(vals + beg + base + LPR + gl);
+            nx_col = KGQ_LD_STREAM(indices + beg + base + LPR + gl);
+            nx_val = KGQ_LD_STREAM(vals + beg + base + LPR + gl);
         }
 #pragma unroll
         for (int t = 0; t < LPR; t += 4) {
@@ -237,8 +251,8 @@ spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indi
         rg_spmm_row<D, false>(indptr, indices, vals, x, row, active, gl, acc);
         if (active) {
             float4 *o = reinterpret_cast<float4 *>(out + row * D);
-            o[fa] = acc[0];
-            o[fb] = acc[1];
+            KGQ_ST_STREAM(o + fa, acc[0]);
+            KGQ_ST_STREAM(o + fb, acc[1]);
         }
     }
 }
