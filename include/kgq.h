@@ -209,9 +209,12 @@ KGQ_API int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d, co
 
 /* BPR + L2 head forward (tape.py:154-170): margins[r] = sum_k u*(p-n);
  * loss[0] = mean logaddexp(0, -margins) + (l2 * (|u|^2+|p|^2+|n|^2)) / batch,
- * one CTA, fixed reduction order.  u, p, n: batch x d fp32 row-major. */
+ * fixed reduction order (deterministic).  u, p, n: batch x d fp32 row-major.
+ * workspace: kgq_bpr_forward_workspace_bytes(batch) of device memory. */
+KGQ_API size_t kgq_bpr_forward_workspace_bytes(int64_t batch);
 KGQ_API int kgq_bpr_forward_f32(const float *u, const float *p, const float *n, int64_t batch, int32_t d,
-                        float l2, float *margins, float *loss, void *stream);
+                        float l2, float *margins, float *loss, void *workspace, size_t workspace_bytes,
+                        void *stream);
 
 /* BPR head backward (tape.py:233-244) against the dequantized blocks:
  * coef = sigmoid(-m)/batch; gu = g*(-coef*(ph-nh) + reg*uh); gp = g*(-coef*uh

@@ -185,41 +185,95 @@ scatter_rows_multi_kernel(const int64_t *__restrict__ order, const int32_t *__re
 __global__ void __launch_bounds__(256)
 scatter_rows_multi_nosort_kernel(const int32_t *__restrict__ idx, int64_t m, ListEnds list_end, int n_lists,
                                  const float *__restrict__ g, int d, float *__restrict__ out) {
+    constexpr int NF = 4;                           // features per lane: d <= 128
+    extern __shared__ int32_t sidx[];               // the whole id list (m <= 16384), staged once per CTA
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) sidx[k] = __ldg(idx + k);
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= m) return;
-    const int32_t row = __ldg(idx + i);
+    const int32_t row = sidx[i];
     if (row < 0) return;                            // not owned here: skipped
-    for (int64_t j0 = 0; j0 < i; j0 += 32) {       // an earlier occurrence owns the row
-        const int64_t j = j0 + lane;
-        const bool hit = j < i && __ldg(idx + j) == row;
-        if (__ballot_sync(0xffffffffu, hit)) return;
-    }
-    for (int f0 = 0; f0 < d; f0 += 32) {
-        const int f = f0 + lane;
-        float total = 0.0f, acc = 0.0f;
-        int li = 0;
-        for (int64_t j0 = i; j0 < m; j0 += 32) {
-            const int64_t jl = j0 + lane;
-            uint32_t hits = __ballot_sync(0xffffffffu, jl < m && __ldg(idx + jl) == row);
+    // one pass over the lists, 4 chunks of 32 ids per step (independent
+    // loads in flight): an earlier occurrence owns the row -> exit; later
+    // ones are folded in position order, all features at once
+    float total[NF], acc[NF];
+#pragma unroll
+    for (int k = 0; k < NF; k++) total[k] = acc[k] = 0.0f;
+    int li = 0;
+    for (int64_t j0 = 0; j0 < m; j0 += 128) {
+        uint32_t hit[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t j = j0 + 32 * u + lane;
+            hit[u] = __ballot_sync(0xffffffffu, j < m && sidx[j] == row);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            uint32_t hits = hit[u];
+            const int64_t base = j0 + 32 * u;
+            if (base + 32 <= i) {
+                if (hits) return;                   // an earlier position holds the row
+                continue;
+            }
+            if (base < i) {                         // chunk containing i
+                if (hits & ((1u << (int)(i - base)) - 1u)) return;
+                hits &= ~((1u << (int)(i - base)) - 1u);
+            }
             while (hits) {
-                const int b = __ffs(hits) - 1;
-                hits &= hits - 1;
-                const int64_t pos = j0 + b;
-                int l = 0;
-                while (l + 1 < n_lists && pos >= list_end.e[l]) l++;
-                for (; li < l; li++) {
-                    total = li == 0 ? acc : __fadd_rn(total, acc);
-                    acc = 0.0f;
+                // up to 4 occurrences: their rows are loaded together (independent
+                // loads in flight), then folded strictly in position order
+                int64_t ps[4];
+                int cnt = 0;
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    if (hits) {
+                        ps[t] = base + (__ffs(hits) - 1);
+                        hits &= hits - 1;
+                        cnt = t + 1;
+                    } else {
+                        ps[t] = ps[0];
+                    }
                 }
-                if (f < d) acc = __fadd_rn(acc, __ldg(g + pos * d + f));
+                float v[4][NF];
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+#pragma unroll
+                    for (int k = 0; k < NF; k++) {
+                        const int f = lane + 32 * k;
+                        v[t][k] = (t < cnt && f < d) ? __ldg(g + ps[t] * d + f) : 0.0f;
+                    }
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    if (t < cnt) {
+                        int l = 0;
+                        while (l + 1 < n_lists && ps[t] >= list_end.e[l]) l++;
+                        for (; li < l; li++) {
+#pragma unroll
+                            for (int k = 0; k < NF; k++) {
+                                total[k] = li == 0 ? acc[k] : __fadd_rn(total[k], acc[k]);
+                                acc[k] = 0.0f;
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < NF; k++)
+                            if (lane + 32 * k < d) acc[k] = __fadd_rn(acc[k], v[t][k]);
+                    }
+                }
             }
         }
-        for (; li < n_lists; li++) {
-            total = li == 0 ? acc : __fadd_rn(total, acc);
-            acc = 0.0f;
+    }
+    for (; li < n_lists; li++) {
+#pragma unroll
+        for (int k = 0; k < NF; k++) {
+            total[k] = li == 0 ? acc[k] : __fadd_rn(total[k], acc[k]);
+            acc[k] = 0.0f;
         }
-        if (f < d) out[(int64_t)row * d + f] = total;
+    }
+#pragma unroll
+    for (int k = 0; k < NF; k++) {
+        const int f = lane + 32 * k;
+        if (f < d) out[(int64_t)row * d + f] = total[k];
     }
 }
 
@@ -233,9 +287,19 @@ extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *i
     for (int i = 0; i < kMaxScatterLists; i++) ends.e[i] = i < n_lists ? list_end[i] : m;
     const int64_t blocks = (m * 32 + 255) / 256;
     if (!order) {
-        if (m > 16384) return KGQ_ERR_INVALID_ARG;  // sort-free path is quadratic: sort first
-        scatter_rows_multi_nosort_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(idx, m, ends, n_lists,
-                                                                                      g, d, out);
+        if (m > 16384 || d > 128) return KGQ_ERR_INVALID_ARG;  // quadratic in m; <= 4 features per lane
+        const size_t smem = (size_t)m * sizeof(int32_t);
+        if (smem > 48 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                cudaError_t e = cudaFuncSetAttribute(scatter_rows_multi_nosort_kernel,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                if (e != cudaSuccess) return kgq_set_cuda_error(e);
+                attr = true;
+            }
+        }
+        scatter_rows_multi_nosort_kernel<<<(int)blocks, 256, smem, (cudaStream_t)stream>>>(idx, m, ends, n_lists,
+                                                                                         g, d, out);
         KGQ_LAUNCH_CHECK();
         return KGQ_OK;
     }

@@ -192,8 +192,11 @@ def bpr_forward(u: torch.Tensor, p: torch.Tensor, n: torch.Tensor, l2: float):
     u, p, n = u.contiguous(), p.contiguous(), n.contiguous()
     margins = torch.empty(batch, dtype=torch.float32, device=dev)
     loss = torch.empty((), dtype=torch.float32, device=dev)
-    st = _lib.load().kgq_bpr_forward_f32(u.data_ptr(), p.data_ptr(), n.data_ptr(), batch, d, float(l2),
-                                         margins.data_ptr(), loss.data_ptr(), _lib.stream_ptr(dev))
+    L = _lib.load()
+    ws_bytes = int(L.kgq_bpr_forward_workspace_bytes(batch))
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+    st = L.kgq_bpr_forward_f32(u.data_ptr(), p.data_ptr(), n.data_ptr(), batch, d, float(l2),
+                               margins.data_ptr(), loss.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev))
     _lib.check(st, "kgq_bpr_forward_f32")
     return loss, margins
 
@@ -233,7 +236,7 @@ def scatter_rows_multi(src_rows: int, idxs, gs) -> torch.Tensor:
         return out
     ends = np.ascontiguousarray(np.cumsum([i.numel() for i in idxs]), dtype=np.int64)   # host, by value
     order = None
-    if m > 16384:        # the sort-free kernel is quadratic in m
+    if m > 16384 or d > 128:     # the sort-free kernel is quadratic in m, <= 128 features
         key = idx.to(torch.int64) * m + torch.arange(m, device=dev, dtype=torch.int64)
         order = torch.sort(key).indices
     if len(idxs) > 8:
