@@ -185,6 +185,25 @@ class IndustryGraph:
             raise ValueError("row block has >= 2^31 nonzeros; use more ranks")
         return indptr.to(torch.int32), cols.to(torch.int32), vals
 
+    def referenced_by_others(self, lo: int, hi: int, cuts) -> torch.Tensor:
+        """For the row block [lo, hi): how many distinct local rows each rank
+        (by ``cuts``) references through its own CSR block -- the send side
+        of the halo exchange (HaloPlan.send_counts), from one streaming pass."""
+        dev = self.device
+        cuts_t = torch.as_tensor(np.asarray(cuts, dtype=np.int64), device=dev)
+        n_loc = hi - lo
+        keys = []
+        for a, b in self.edges():
+            for r, c in ((a, b), (b, a)):
+                sel = (c >= lo) & (c < hi) & ((r < lo) | (r >= hi))
+                if bool(sel.any()):
+                    q = torch.searchsorted(cuts_t, r[sel], right=True) - 1
+                    keys.append(torch.unique(q * n_loc + (c[sel] - lo)))
+        if not keys:
+            return torch.zeros(len(cuts) - 1, dtype=torch.int64, device=dev)
+        k = torch.unique(torch.cat(keys))
+        return torch.bincount(k // n_loc, minlength=len(cuts) - 1)
+
     # -- small shapes: the whole dataset (tests) ------------------------------
     def dataset(self) -> KgDataset:
         s = self.shape

@@ -109,6 +109,23 @@ class Comm:
         out[sel] = local[idx[sel] - lo]
         return self.all_reduce_sum(out)
 
+    def all_to_all_v(self, send: torch.Tensor, send_counts, recv_counts, out: torch.Tensor | None = None):
+        """Rows send[sum(send_counts[:r]) : +send_counts[r]] go to rank r; the
+        rows from rank r land at out[sum(recv_counts[:r]) : ...] (NCCL
+        all_to_all_single with split sizes; gloo on CPU tensors)."""
+        n_out = int(sum(recv_counts))
+        if out is None:
+            out = send.new_empty((n_out,) + tuple(send.shape[1:]))
+        if self.gloo and send.is_cuda:
+            o = torch.empty((n_out,) + tuple(send.shape[1:]), dtype=send.dtype)
+            self.dist.all_to_all_single(o, send.cpu(), output_split_sizes=[int(c) for c in recv_counts],
+                                        input_split_sizes=[int(c) for c in send_counts], group=self.group)
+            out.copy_(o)
+        else:
+            self.dist.all_to_all_single(out, send.contiguous(), output_split_sizes=[int(c) for c in recv_counts],
+                                        input_split_sizes=[int(c) for c in send_counts], group=self.group)
+        return out
+
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         if self.gloo and t.is_cuda:
             c = t.cpu()
@@ -134,6 +151,9 @@ class SoloComm:
 
     def gather_index_rows(self, local, lo, idx):
         return local[idx - lo]
+
+    def all_to_all_v(self, send, send_counts, recv_counts, out=None):
+        return send if out is None else out.copy_(send)
 
     def all_reduce_sum(self, t):
         return t
@@ -180,8 +200,84 @@ class SimulatedRankComm:
         out[sel] = local[idx[sel] - lo]
         return out
 
+    def all_to_all_v(self, send, send_counts, recv_counts, out=None):
+        """The received halo rows keep their stand-in values (filled once)."""
+        n_out = int(sum(recv_counts))
+        if out is not None:
+            if "halo_fill" not in self._bufs:
+                self._bufs["halo_fill"] = True
+                g = torch.Generator(device=out.device).manual_seed(self.seed + 17)
+                out.normal_(0.0, self.fill_std, generator=g).abs_()
+            return out
+        return self._buf(("a2a", n_out), (n_out,) + tuple(send.shape[1:]), send)
+
     def all_reduce_sum(self, t):
         return t
+
+
+class HaloPlan:
+    """Boundary ("halo") exchange of one rank of a row partition: instead of
+    all-gathering every row, the rank receives only the remote rows its CSR
+    block references and sends the local rows the other ranks reference
+    (one all_to_all_v per exchange).  Local CSR columns are remapped once to
+    a compact space: [0, n_local) the rank's own rows, [n_local, n_local +
+    n_halo) the halo rows in (owner, global id) order.  Same values in the
+    same per-row column order -> the SpMM is bit-identical to the full
+    all-gather."""
+
+    def __init__(self, part, remote_ids: torch.Tensor, recv_counts, send_counts, send_idx: torch.Tensor):
+        self.part = part
+        self.n_local = part.hi - part.lo
+        self.remote_ids = remote_ids            # int64, sorted, device
+        self.n_halo = int(remote_ids.numel())
+        self.recv_counts = [int(c) for c in recv_counts]
+        self.send_counts = [int(c) for c in send_counts]
+        self.send_idx = send_idx                # int64 local row ids, grouped by destination rank
+
+    @classmethod
+    def build(cls, part, cols: torch.Tensor, comm) -> "HaloPlan":
+        """cols: the block's global column ids (any order).  Collective: every
+        rank of the partition calls it (counts, then the requested ids, are
+        exchanged with all_to_all_v)."""
+        dev = cols.device
+        lo, hi = part.lo, part.hi
+        u = torch.unique(cols.to(torch.int64))
+        remote = u[(u < lo) | (u >= hi)]
+        cuts = torch.as_tensor(np.asarray(part.cuts, dtype=np.int64), device=dev)
+        owner = torch.searchsorted(cuts, remote, right=True) - 1
+        recv_counts = torch.bincount(owner, minlength=part.world).to(torch.int64)
+        ones = [1] * part.world
+        send_counts = comm.all_to_all_v(recv_counts.reshape(-1, 1), ones, ones).reshape(-1)
+        rc, sc = recv_counts.cpu().tolist(), send_counts.cpu().tolist()
+        requested = comm.all_to_all_v(remote.reshape(-1, 1), rc, sc).reshape(-1)
+        return cls(part, remote, rc, sc, (requested - lo).to(torch.int64))
+
+    def remap(self, cols: torch.Tensor) -> torch.Tensor:
+        """Global column ids -> compact ids (int32)."""
+        c = cols.to(torch.int64)
+        lo, hi = self.part.lo, self.part.hi
+        local = (c >= lo) & (c < hi)
+        pos = torch.searchsorted(self.remote_ids, c)
+        return torch.where(local, c - lo, self.n_local + pos).to(torch.int32)
+
+    def exchange(self, x_local: torch.Tensor, comm, out: torch.Tensor | None = None) -> torch.Tensor:
+        """[own rows | halo rows] for the SpMM: one all_to_all_v of the rows
+        the other ranks reference."""
+        if self.n_halo == 0 and sum(self.send_counts) == 0:
+            return x_local
+        d = x_local.shape[1]
+        if out is None:
+            out = x_local.new_empty((self.n_local + self.n_halo, d))
+        out[:self.n_local].copy_(x_local)
+        send = x_local.index_select(0, self.send_idx)
+        comm.all_to_all_v(send, self.send_counts, self.recv_counts, out=out[self.n_local:])
+        return out
+
+    def recv_bytes(self, d: int) -> int:
+        return self.n_halo * d * 4
+
+    def send_bytes(self, d: int) -> int:
+        return int(sum(self.send_counts)) * d * 4
 
 
 class GpuOps:
@@ -251,7 +347,7 @@ class RowPartition:
 
 def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas, users, pos, neg,
                      l2: float, cfg: QuantConfig, stream: RandomStream, comm, ops=GpuOps,
-                     padded: bool = False, layout: str | None = None):
+                     padded: bool = False, layout: str | None = None, halo: "HaloPlan | None" = None):
     """One forward+backward of the KGNN backbone + BPR head on this rank's
     rows.  Returns (loss tensor, dE0 for the local rows, [dtheta_i] summed
     over ranks).  Mirrors tape.py:193-253's routing order.
@@ -261,18 +357,24 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     layout, ``GpuOps.local_adjacency(..., part=part)``: one
     all_gather_into_tensor, no copy; best for equal-row blocks) or "global"
     (all-gather-v by per-source broadcasts into the global layout: exact
-    bytes for uneven equal-nnz blocks, global column ids, no copy).
-    ``padded=True`` is shorthand for layout="padded".  The BPR head only
+    bytes for uneven equal-nnz blocks, global column ids, no copy) or "halo"
+    (only the rows the block references, ``HaloPlan``; ``a_local`` columns
+    remapped by ``HaloPlan.remap``).  ``padded=True`` is shorthand for
+    layout="padded".  The BPR head only
     needs the 3*B batch rows of the readout: they are exchanged by index
     (``gather_index_rows``), never the whole readout."""
     lo, counts = part.lo, part.counts
     m = part.block
 
-    layout = layout or ("padded" if padded else "concat")
-    if layout not in ("concat", "padded", "global"):
+    layout = layout or ("halo" if halo is not None else "padded" if padded else "concat")
+    if layout not in ("concat", "padded", "global", "halo"):
         raise ValueError(f"unknown exchange layout {layout!r}")
+    if layout == "halo" and halo is None:
+        raise ValueError("layout='halo' needs a HaloPlan (a_local remapped with HaloPlan.remap)")
 
     def gather(x):
+        if layout == "halo":
+            return halo.exchange(x, comm)
         if layout == "padded":
             return comm.all_gather_padded(x, m)
         if layout == "global":

@@ -100,3 +100,27 @@ def test_reference_datasets_match_survey_counts():
     assert len(ds.train) == 579759
     ip, _, _ = D.adjacency_arrays(ds)
     assert int(ip[-1]) == 6425569
+
+
+def test_industry_referenced_by_others_matches_blocks():
+    """The halo send side from one streaming pass equals, for each other rank,
+    the distinct local rows that rank's CSR block references."""
+    import torch
+    from paper_2212_04540_b200.industry import IndustryGraph, IndustryShape
+    sh = IndustryShape(users=2000, items=800, entities=6000, relations=5, groups=11,
+                       interactions_per_user=12.0, attr_links_per_item=5.0, user_chunk=500, item_chunk=200)
+    g = IndustryGraph(sh, seed=2, device="cpu")
+    deg = g.degrees()
+    W = 3
+    cuts = g.partition(deg, W)
+    blocks = [g.row_block(int(cuts[r]), int(cuts[r + 1]), deg) for r in range(W)]
+    for R in range(W):
+        lo, hi = int(cuts[R]), int(cuts[R + 1])
+        got = g.referenced_by_others(lo, hi, cuts).tolist()
+        for q in range(W):
+            if q == R:
+                assert got[q] == 0
+                continue
+            cols = blocks[q][1].long()
+            want = torch.unique(cols[(cols >= lo) & (cols < hi)]).numel()
+            assert got[q] == want, (R, q)

@@ -129,11 +129,17 @@ def _run(world, rank, comm, layout="concat"):
     z, n, e0, thetas, (users, pos, neg) = _problem()
     part = RowPartition.build(z["indptr"], world, rank)
     ip, ix, vv = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
+    halo = None
     if layout == "padded":           # columns index the padded gather buffer
         ix = part.padded_cols(ix).astype(np.int32)
+    elif layout == "halo":           # columns index [own rows | halo rows]
+        from paper_2212_04540_b200.parallel import HaloPlan
+        halo = HaloPlan.build(part, torch.from_numpy(ix.astype(np.int64)), comm)
+        ix = halo.remap(torch.from_numpy(ix.astype(np.int64))).numpy()
     cfg = QuantConfig(bits=2)
     loss, de0, dth = partitioned_step(part, (ip, ix, vv), e0[part.lo:part.hi], thetas, users, pos, neg,
-                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps, layout=layout)
+                                      1e-5, cfg, RandomStream(21), comm, ops=OracleOps, layout=layout,
+                                      halo=halo)
     return part, loss, de0, dth
 
 
@@ -149,12 +155,12 @@ def _worker(rank, world, port, out_q, layout="concat"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["concat", "padded", "global"])
+@pytest.mark.parametrize("layout", ["concat", "padded", "global", "halo"])
 def test_partitioned_step_world2_gloo_matches_world1(layout):
     part1, loss1, de1, dth1 = _run(1, 0, SoloComm())
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000) + 7 * ["concat", "padded", "global"].index(layout)
+    port = 29500 + (os.getpid() % 1000) + 7 * ["concat", "padded", "global", "halo"].index(layout)
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q, layout)) for r in range(2)]
     for p in procs:
         p.start()
@@ -215,3 +221,13 @@ def test_simulated_rank_comm_shapes_and_local_rows():
     assert padded.shape == (21, 2) and torch.equal(padded[7:14], local)
     t = torch.ones(3)
     assert comm.all_reduce_sum(t) is t
+
+
+def test_halo_plan_world1_is_identity():
+    from paper_2212_04540_b200.parallel import HaloPlan
+    z, n, e0, thetas, idx = _problem()
+    part = RowPartition.build(z["indptr"], 1, 0)
+    plan = HaloPlan.build(part, torch.from_numpy(z["indices"].astype(np.int64)), SoloComm())
+    assert plan.n_halo == 0 and plan.send_counts == [0]
+    assert torch.equal(plan.remap(torch.from_numpy(z["indices"].astype(np.int64))),
+                       torch.from_numpy(z["indices"].astype(np.int32)))
