@@ -200,7 +200,7 @@ reduce_partials_bwd_kernel(const float *__restrict__ partial, int nparts, int dd
 using namespace kgq;
 
 // d = 64: the tcgen05 kernel (kgq_backward_tc.cu) by default; KGQ_BWD_TC=0
-// selects the FFMA kernel below (read once).  Amazon shape: 73 us vs 110 us.
+// selects the FFMA kernel below (read once).  Amazon shape: 62 us vs 110 us.
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t bits, const float *theta, float *dh,

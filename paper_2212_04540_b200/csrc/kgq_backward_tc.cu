@@ -111,6 +111,13 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
         // ---- 1. stage g_j and Hhat (hi/lo, three layouts) from the prefetched registers ----
         {
             const float rg = prg, zz = pzz;
+            // b <= 2: the row's 2^b reconstruction values once (IEEE, lut_entry),
+            // then a select per element instead of the division sequence
+            float lut[BITS <= 2 ? (1 << BITS) : 1];
+            if (BITS <= 2) {
+#pragma unroll
+                for (int c = 0; c < (1 << BITS); c++) lut[c] = lut_entry<BITS>(rg, zz, c);
+            }
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const float av[4] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w}, ev[4] = {pe[j].x, pe[j].y, pe[j].z, pe[j].w};
@@ -124,7 +131,12 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
                     const float gj = __fmul_rn(g, ((mw >> (c & 31)) & 1u) ? 1.0f : 0.0f);
                     const int bp = c * BITS;
                     const uint32_t code = (pcw[bp >> 5] >> (bp & 31)) & CM;
-                    const float hv = ok ? lut_entry<BITS>(rg, zz, (int)code) : 0.0f;
+                    float hv;
+                    if (BITS == 1) hv = code ? lut[BITS <= 2 ? 1 : 0] : lut[0];
+                    else if (BITS == 2) hv = (code & 2u) ? ((code & 1u) ? lut[BITS == 2 ? 3 : 0] : lut[BITS == 2 ? 2 : 0])
+                                                     : ((code & 1u) ? lut[BITS <= 2 ? 1 : 0] : lut[0]);
+                    else hv = lut_entry<BITS>(rg, zz, (int)code);
+                    hv = ok ? hv : 0.0f;
                     float hh, hl;
                     tc::split_tf32(gj, gh[q], gl[q]);
                     tc::split_tf32(hv, hh, hl);
