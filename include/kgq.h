@@ -3,10 +3,14 @@
  *
  * Every entry point takes plain device pointers, element counts and a CUDA
  * stream (as void*, i.e. a cudaStream_t / CUstream; NULL = legacy default
- * stream).  The caller allocates every buffer; no function allocates device
- * memory, keeps global state, synchronises the stream, or throws.  Every
- * function is stream-ordered and CUDA-graph capturable.  Return value is a
- * kgq_status (0 = OK).
+ * stream).  The caller allocates every buffer: the device entry points never
+ * allocate device memory, synchronise the stream, or throw, and keep no state
+ * between calls beyond once-per-process kernel setup (dynamic shared-memory
+ * opt-ins; the KGQ_BWD_TC A/B switch, read at first use).  They are
+ * stream-ordered and CUDA-graph capturable.  The host-buffer entry points
+ * (kgq_*_host_f32) block like the numpy calls they replace and create a
+ * workspace and streams themselves when the caller passes none.  Return
+ * value is a kgq_status (0 = OK).
  *
  * The reference (kgact, pure numpy) has no FFI; each entry point below names
  * the reference function whose semantics it replaces.  The Python host layer
