@@ -180,6 +180,8 @@ KGQ_API int kgq_rowmm_f32(const float *a, int64_t rows, int32_t d, const float *
  *   g_j = (g_read + g_e) * mask;  dh = g_j . theta^T;  dtheta (+)= Hhat^T . g_j
  * with Hhat = dequantize(codes, ranges, offsets) never materialized.  g_read
  * or g_e may be NULL (not both).  workspace: kgq_layer_backward_workspace_bytes.
+ * d = 64 runs on tcgen05 (3xTF32 MMAs, TMEM accumulators; KGQ_BWD_TC=0 selects
+ * the FFMA kernel), d = 32 / 128 on FFMA; dtheta is reduced in a fixed order.
  * Other d -> KGQ_ERR_INVALID_ARG (the host falls back to the unfused ops). */
 KGQ_API size_t kgq_layer_backward_workspace_bytes(int64_t rows, int32_t d);
 KGQ_API int kgq_layer_backward_f32(const float *g_read, const float *g_e, const uint8_t *mask,
