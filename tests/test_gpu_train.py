@@ -531,3 +531,24 @@ print("ok")
     env = dict(os.environ, KGQ_BWD_TC="0")
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_scatter_rows_multi_edge_cases():
+    """Empty lists, rows owned elsewhere (-1, skipped), a single list, d = 1
+    and d = 128: bit-identical to the numpy reference sums."""
+    _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(11)
+    for d in (1, 64, 128):
+        rows = 40
+        idxs = [rng.integers(-1, rows, size=k).astype(np.int32) for k in (0, 77, 5)]
+        gs = [rng.standard_normal((len(i), d), dtype=np.float32) for i in idxs]
+        ref = None
+        for i, g in zip(idxs, gs):
+            s = np.zeros((rows, d), np.float32)
+            keep = i >= 0
+            np.add.at(s, i[keep], g[keep])
+            ref = s if ref is None else ref + s
+        out = F.scatter_rows_multi(rows, [torch.from_numpy(i).cuda() for i in idxs],
+                                   [torch.from_numpy(g).cuda() for g in gs])
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32)), d
