@@ -339,7 +339,7 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
     return out
 
 
-def quality_bench(args):
+def quality_bench(args, shape=None):
     """Recall@20 / NDCG@20 after ``--quality-epochs`` full epochs from the
     reference's initial state (same params, batches, negatives: train_run,
     train.py:175-227) at INT2 (fast and compat noise) and FP32, next to the
@@ -349,9 +349,10 @@ def quality_bench(args):
     import paper_2212_04540_b200 as kgq
     from paper_2212_04540_b200.model import ModelConfig
     from paper_2212_04540_b200.train import TrainConfig, train_run
-    ds = D.reference_dataset(args.train_shape)
+    shape = shape or args.train_shape
+    ds = D.reference_dataset(shape)
     adj = D.build_adjacency(ds)
-    out = {"epochs": args.quality_epochs, "dataset": f"{args.train_shape}_seed0 (reference generator)"}
+    out = {"epochs": args.quality_epochs, "dataset": f"{shape}_seed0 (reference generator)"}
     for name, bits, rng in (("int2_fast", 2, "fast"), ("int2_compat", 2, "compat"), ("fp32", 32, "fast")):
         q = kgq.QuantConfig(bits=bits, rng=rng)
         _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q),
@@ -361,7 +362,7 @@ def quality_bench(args):
                      "loss_curve": [round(v, 6) for v in rep["loss_curve"]],
                      "epoch_s": [round(v, 3) for v in rep["timing"]["epoch_seconds"]],
                      "activation_bytes_peak": rep["memory"]["activation_bytes_peak"]}
-    ref_path = os.path.join(ROOT, "datasets", f"{args.train_shape}_seed0_reference_runs.json")
+    ref_path = os.path.join(ROOT, "datasets", f"{shape}_seed0_reference_runs.json")
     if os.path.exists(ref_path):
         with open(ref_path) as f:
             ref = json.load(f)
@@ -717,6 +718,13 @@ def run_ours(args):
                 train["quality"] = quality_bench(args)
             except Exception as exc:
                 train["quality"] = {"error": f"{type(exc).__name__}: {exc}"}
+            if args.train_shape == "amazon" and isinstance(train.get("lastfm"), dict) and \
+                    os.path.exists(os.path.join(ROOT, "datasets", "lastfm_seed0_reference_runs.json")):
+                torch.cuda.empty_cache()
+                try:      # configs[2] quality next to the reference's own Last-FM runs
+                    train["lastfm"]["quality"] = quality_bench(args, shape="lastfm")
+                except Exception as exc:
+                    train["lastfm"]["quality"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     industry = None
     if args.industry and world == 1:
