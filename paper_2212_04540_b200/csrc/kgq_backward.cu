@@ -44,7 +44,7 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
                       float *__restrict__ partial) {
     constexpr int NC = D / 32;                     // columns per lane
     constexpr int RB = D * BITS / 8;
-    constexpr uint32_t CM = (1u << BITS) - 1u;
+    constexpr uint32_t CM = BITS >= 32 ? 0xFFFFFFFFu : (1u << BITS) - 1u;
     constexpr int TS = D > 64 ? 8 : 4;             // dtheta register tile
     constexpr int TPD = D / TS;                    // tiles per dimension (TPD^2 <= 256)
     static_assert(TPD * TPD <= 256, "dtheta tiles exceed the CTA");
@@ -74,8 +74,8 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
         for (int rr = 0; rr < 4; rr++) {
             const int64_t row = ch * kBwdRows + warp * 4 + rr;
             const bool ok = row < rows;
-            pr[rr] = ok ? __ldg(ranges + row) : 0.f;
-            pz[rr] = ok ? __ldg(offsets + row) : 0.f;
+            pr[rr] = (ok && BITS != 32) ? __ldg(ranges + row) : 0.f;
+            pz[rr] = (ok && BITS != 32) ? __ldg(offsets + row) : 0.f;
 #pragma unroll
             for (int c = 0; c < NC; c++) {
                 const int col = lane + 32 * c;
@@ -83,7 +83,10 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
                 pe[rr][c] = (ok && g_e) ? __ldg(g_e + row * D + col) : 0.f;
                 pm[rr][c] = ok ? __ldg(mask + row * (D / 32) + c) : 0u;
                 const int b = col * BITS;
-                pc[rr][c] = ok ? __ldg(codes + row * RB + (b >> 3)) : 0u;
+                if (BITS == 32)        // pass-through context: codes holds the fp32 H
+                    pc[rr][c] = ok ? __float_as_uint(__ldg(reinterpret_cast<const float *>(codes) + row * D + col)) : 0u;
+                else
+                    pc[rr][c] = ok ? __ldg(codes + row * RB + (b >> 3)) : 0u;
             }
         }
     };
@@ -104,10 +107,10 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
                 const float g = (g_read && g_e) ? __fadd_rn(pg[rr][c], pe[rr][c]) : (g_read ? pg[rr][c] : pe[rr][c]);
                 const float gj = __fmul_rn(g, ((pm[rr][c] >> lane) & 1u) ? 1.0f : 0.0f);
                 const int b = col * BITS;
-                const uint32_t code = (pc[rr][c] >> (b & 7)) & CM;
+                const uint32_t code = BITS == 32 ? 0u : (pc[rr][c] >> (b & 7)) & CM;
                 gs[lr][col] = gj;
                 gk[warp][col][rr] = gj;
-                hs[lr][col] = lut_entry<BITS>(pr[rr], pz[rr], (int)code);
+                hs[lr][col] = BITS == 32 ? __uint_as_float(pc[rr][c]) : lut_entry<BITS <= 8 ? BITS : 8>(pr[rr], pz[rr], (int)code);
             }
         }
         if (ch + gridDim.x < n_chunks) load(ch + gridDim.x);
@@ -225,7 +228,7 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
                                       const float *theta, float *dh, float *dtheta,
                                       void *workspace, size_t workspace_bytes, int32_t accumulate,
                                       void *stream) {
-    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8 || bits == 32)) return KGQ_ERR_UNSUPPORTED_BITS;
     if (d != 32 && d != 64 && d != 128) return KGQ_ERR_INVALID_ARG;   // caller falls back (unfused)
     if (rows < 0) return KGQ_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
@@ -236,8 +239,8 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
         }
         return KGQ_OK;
     }
-    if ((!g_read && !g_e) || !mask || !codes || !ranges || !offsets || !theta || !dh || !dtheta)
-        return KGQ_ERR_INVALID_ARG;
+    if ((!g_read && !g_e) || !mask || !codes || !theta || !dh || !dtheta) return KGQ_ERR_INVALID_ARG;
+    if (bits != 32 && (!ranges || !offsets)) return KGQ_ERR_INVALID_ARG;
     if (((uintptr_t)mask) & 3u) return KGQ_ERR_MISALIGNED;
     if (!workspace || workspace_bytes < kgq_layer_backward_workspace_bytes(rows, d))
         return KGQ_ERR_INVALID_ARG;
@@ -245,7 +248,7 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     float *partial = reinterpret_cast<float *>(workspace);
     const uint32_t *m32 = reinterpret_cast<const uint32_t *>(mask);
     const bool aligned16 = ((((uintptr_t)g_read) | ((uintptr_t)g_e) | ((uintptr_t)dh)) & 15u) == 0 &&
-                           ((uintptr_t)codes & 3u) == 0;
+                           ((uintptr_t)codes & (bits == 32 ? 15u : 3u)) == 0;
     if (d == 64 && aligned16 && use_tc_backward()) {
         const int64_t tiles = (rows + 127) / 128;
         grid = (int)(tiles < kSMs ? tiles : kSMs);
@@ -269,13 +272,16 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     } while (0)
     if (d == 128) {
         switch (bits) { case 1: KGQ_BWD(128, 1); break; case 2: KGQ_BWD(128, 2); break;
-                        case 4: KGQ_BWD(128, 4); break; default: KGQ_BWD(128, 8); break; }
+                        case 4: KGQ_BWD(128, 4); break; case 8: KGQ_BWD(128, 8); break;
+                        default: KGQ_BWD(128, 32); break; }
     } else if (d == 64) {
         switch (bits) { case 1: KGQ_BWD(64, 1); break; case 2: KGQ_BWD(64, 2); break;
-                        case 4: KGQ_BWD(64, 4); break; default: KGQ_BWD(64, 8); break; }
+                        case 4: KGQ_BWD(64, 4); break; case 8: KGQ_BWD(64, 8); break;
+                        default: KGQ_BWD(64, 32); break; }
     } else {
         switch (bits) { case 1: KGQ_BWD(32, 1); break; case 2: KGQ_BWD(32, 2); break;
-                        case 4: KGQ_BWD(32, 4); break; default: KGQ_BWD(32, 8); break; }
+                        case 4: KGQ_BWD(32, 4); break; case 8: KGQ_BWD(32, 8); break;
+                        default: KGQ_BWD(32, 32); break; }
     }
 #undef KGQ_BWD
     const int dd = d * d;

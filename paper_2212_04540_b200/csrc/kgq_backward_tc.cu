@@ -51,7 +51,8 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
                          int64_t rows, const float *__restrict__ theta, float *__restrict__ dh,
                          float *__restrict__ partial) {
     constexpr int M = kTcRows, D = kTcD, RB = D * BITS / 8;
-    constexpr uint32_t CM = (1u << BITS) - 1u;
+    constexpr uint32_t CM = BITS >= 32 ? 0xFFFFFFFFu : (1u << BITS) - 1u;
+    constexpr int NCW = BITS >= 32 ? 1 : 2 * BITS;      // code words per row held in registers
     extern __shared__ __align__(128) float tsm[];
     float *th_hi = tsm, *th_lo = tsm + BwdTcSmem::TH;
     float *ag_hi = tsm + 2 * BwdTcSmem::TH, *ag_lo = ag_hi + BwdTcSmem::AG;
@@ -85,17 +86,24 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
     // tile's MMAs run, so the loads overlap the tensor-core work)
     float4 pa[4], pe[4];
     float prg = 0.f, pzz = 0.f;
-    uint32_t pm0 = 0u, pm1 = 0u, pcw[2 * BITS];
+    uint32_t pm0 = 0u, pm1 = 0u, pcw[NCW];
+    float4 ph[BITS == 32 ? 4 : 1];                       // pass-through: the fp32 H quads
     auto load = [&](int64_t tl) {
         const int64_t row = tl * M + r;
         const bool ok = tl < n_tiles && row < rows;
-        prg = ok ? __ldg(ranges + row) : 0.f;
-        pzz = ok ? __ldg(offsets + row) : 0.f;
+        prg = (ok && BITS != 32) ? __ldg(ranges + row) : 0.f;
+        pzz = (ok && BITS != 32) ? __ldg(offsets + row) : 0.f;
         pm0 = ok ? __ldg(mask + row * 2) : 0u;
         pm1 = ok ? __ldg(mask + row * 2 + 1) : 0u;
-        const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB);
+        if (BITS == 32) {
+            const float4 *h4 = reinterpret_cast<const float4 *>(codes) + row * (D / 4);
 #pragma unroll
-        for (int w = 0; w < 2 * BITS; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
+            for (int j = 0; j < (BITS == 32 ? 4 : 1); j++) ph[j] = ok ? __ldg(h4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB);
+#pragma unroll
+            for (int w = 0; w < NCW; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
+        }
         const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D);
         const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D);
 #pragma unroll
@@ -114,7 +122,7 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
             // b <= 2: the row's 2^b reconstruction values once (IEEE, lut_entry),
             // then a select per element instead of the division sequence
             float lut[BITS <= 2 ? (1 << BITS) : 1];
-            if (BITS <= 2) {
+            if constexpr (BITS <= 2) {
 #pragma unroll
                 for (int c = 0; c < (1 << BITS); c++) lut[c] = lut_entry<BITS>(rg, zz, c);
             }
@@ -130,12 +138,15 @@ layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restri
                     const uint32_t mw = c < 32 ? pm0 : pm1;
                     const float gj = __fmul_rn(g, ((mw >> (c & 31)) & 1u) ? 1.0f : 0.0f);
                     const int bp = c * BITS;
-                    const uint32_t code = (pcw[bp >> 5] >> (bp & 31)) & CM;
+                    const uint32_t code = BITS == 32 ? 0u : (pcw[(bp >> 5) % NCW] >> (bp & 31)) & CM;
                     float hv;
-                    if (BITS == 1) hv = code ? lut[BITS <= 2 ? 1 : 0] : lut[0];
+                    if (BITS == 32) {
+                        const float4 hq = ph[BITS == 32 ? j : 0];
+                        hv = q == 0 ? hq.x : q == 1 ? hq.y : q == 2 ? hq.z : hq.w;
+                    } else if (BITS == 1) hv = code ? lut[BITS <= 2 ? 1 : 0] : lut[0];
                     else if (BITS == 2) hv = (code & 2u) ? ((code & 1u) ? lut[BITS == 2 ? 3 : 0] : lut[BITS == 2 ? 2 : 0])
                                                      : ((code & 1u) ? lut[BITS <= 2 ? 1 : 0] : lut[0]);
-                    else hv = lut_entry<BITS>(rg, zz, (int)code);
+                    else hv = lut_entry<BITS <= 8 ? BITS : 8>(rg, zz, (int)code);
                     hv = ok ? hv : 0.0f;
                     float hh, hl;
                     tc::split_tf32(gj, gh[q], gl[q]);
@@ -242,7 +253,7 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t bits, const float *theta, float *dh,
                                  float *partial, int grid, cudaStream_t s) {
-    static bool attr[9] = {false};
+    static bool attr[33] = {false};
 #define KGQ_BTC(B) do {                                                                            \
         if (!attr[B]) {                                                                            \
             cudaError_t e = cudaFuncSetAttribute(layer_backward_tc_kernel<B>,                        \
@@ -258,7 +269,8 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
         case 1: KGQ_BTC(1); break;
         case 2: KGQ_BTC(2); break;
         case 4: KGQ_BTC(4); break;
-        default: KGQ_BTC(8); break;
+        case 8: KGQ_BTC(8); break;
+        default: KGQ_BTC(32); break;
     }
 #undef KGQ_BTC
     return KGQ_OK;

@@ -635,6 +635,7 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
             float4 h[2] = {nh[0], nh[1]};
             if (pass + 1 < NP) fetch(tile, pass + 1);
             else fetch(tile + gridDim.x, 0);
+            if constexpr (BITS != 32)   // b = 32: pass-through context (H itself), nothing to quantize
             light_row_quantize<D, BITS, MODE>(h, active, active ? row : 0, gl, fk, seed, tid, row_offset,
                                               codes, ranges, offsets);
             const float hv[8] = {h[0].x, h[0].y, h[0].z, h[0].w, h[1].x, h[1].y, h[1].z, h[1].w};
@@ -854,10 +855,11 @@ extern "C" int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d,
                                       const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
                                       float *ranges, float *offsets, float *e_next, uint8_t *mask,
                                       void *stream) {
-    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8 || bits == 32)) return KGQ_ERR_UNSUPPORTED_BITS;
     if (n_rows < 0 || row_offset < 0 || rounding < 0 || rounding > 2) return KGQ_ERR_INVALID_ARG;
     if (n_rows == 0) return KGQ_OK;
-    if (!h || !theta || !codes || !ranges || !offsets || !e_next || !mask) return KGQ_ERR_INVALID_ARG;
+    if (!h || !theta || !e_next || !mask) return KGQ_ERR_INVALID_ARG;
+    if (bits != 32 && (!codes || !ranges || !offsets)) return KGQ_ERR_INVALID_ARG;
     if (((uintptr_t)mask & 3u) || ((uintptr_t)codes & 3u) || ((uintptr_t)h & 15u) ||
         ((uintptr_t)e_next & 15u) || ((uintptr_t)theta & 15u))
         return KGQ_ERR_MISALIGNED;
@@ -866,7 +868,8 @@ extern "C" int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d,
 #define KGQ_EPI(D, B) launch_epilogue<D, B>(rounding, h, n_rows, theta, seed, tensor_id, tid_base, row_offset, \
                                             codes, ranges, offsets, e_next, m32, s)
 #define KGQ_EPI_BITS(D) switch (bits) { case 1: return KGQ_EPI(D, 1); case 2: return KGQ_EPI(D, 2); \
-                                        case 4: return KGQ_EPI(D, 4); default: return KGQ_EPI(D, 8); }
+                                        case 4: return KGQ_EPI(D, 4); case 8: return KGQ_EPI(D, 8); \
+                                        default: return KGQ_EPI(D, 32); }
     switch (d) {
         case 32: KGQ_EPI_BITS(32)
         case 64: KGQ_EPI_BITS(64)

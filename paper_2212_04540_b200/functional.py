@@ -25,7 +25,7 @@ FUSED_DIMS = (32, 64, 128)
 
 
 def can_fuse(cfg: QuantConfig, d: int) -> bool:
-    return (not cfg.passthrough) and d in FUSED_DIMS and (cfg.group is None or cfg.group == d)
+    return d in FUSED_DIMS and (cfg.passthrough or cfg.group is None or cfg.group == d)
 
 
 # None = by the size of the gathered table: split while E fits in L2 (Amazon
@@ -54,7 +54,11 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     """
     n_rows, d = adj.shape[0], e.shape[1]
     if not can_fuse(cfg, d):
-        raise ValueError("graph_conv_forward needs bits < 32, d in (32, 64, 128), group == d")
+        raise ValueError("graph_conv_forward needs d in (32, 64, 128) and group == d")
+    if cfg.passthrough:
+        # b = 32 (quantize.py:182-183): the context is H itself, no tensor id is
+        # drawn; H comes from the SpMM kernel, the epilogue does J, relu, mask
+        return _graph_conv_passthrough(adj, e, theta, row_offset, want_h)
     if cfg.rounding == "stochastic":
         if stream is None:
             raise ValueError("stochastic rounding needs a RandomStream")
@@ -120,6 +124,26 @@ def layer_forward_unfused(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Q
     return e_next, mask, q, h
 
 
+def _graph_conv_passthrough(adj: CSR, e: torch.Tensor, theta: torch.Tensor, row_offset: int, want_h: bool):
+    n_rows, d = adj.shape[0], e.shape[1]
+    dev = e.device
+    e = e.contiguous()
+    theta = theta.contiguous()
+    h = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
+    e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
+    mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
+    L = _lib.load()
+    st = L.kgq_spmm_csr_f32(adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows,
+                            *adj.schedule(), e.data_ptr(), d, h.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_spmm_csr_f32")
+    st = L.kgq_layer_epilogue_f32(h.data_ptr(), n_rows, d, theta.data_ptr(), PASSTHROUGH_BITS, 0, 0, 0, None,
+                                  row_offset, None, None, None, e_next.data_ptr(), mask.data_ptr(),
+                                  _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_layer_epilogue_f32")
+    q = QuantizedTensor(n_rows, d, PASSTHROUGH_BITS, None, None, None, raw=h)
+    return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, (h if want_h else None)
+
+
 def dequant_gemm_tn(q: QuantizedTensor, g: torch.Tensor, out: torch.Tensor | None = None,
                     accumulate: bool = False) -> torch.Tensor:
     """dtheta (+)= dequantize(q)^T @ g without materializing the dequantized H."""
@@ -162,7 +186,8 @@ def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.
     from .tensorops import mask_apply, mm_theta
     src = g_read if g_read is not None else g_e
     d = src.shape[1]
-    if q.bits == PASSTHROUGH_BITS or d not in (32, 64, 128) or q.group_size != d:
+    passthrough = q.bits == PASSTHROUGH_BITS
+    if d not in (32, 64, 128) or (not passthrough and q.group_size != d) or (passthrough and q.raw is None):
         g = g_read if g_e is None else (g_e if g_read is None else g_read + g_e)
         g_j = mask_apply(g, mask)
         return dequant_gemm_tn(q, g_j), mm_theta(g_j, theta, transpose=True)
@@ -175,8 +200,9 @@ def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.
     ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
     gr = None if g_read is None else g_read.contiguous()
     ge = None if g_e is None else g_e.contiguous()
+    codes_ptr = q.raw.contiguous().data_ptr() if passthrough else q.codes.data_ptr()   # b=32: fp32 H
     st = L.kgq_layer_backward_f32(_lib.ptr(gr), _lib.ptr(ge), mask.packed.data_ptr(),
-                                  q.codes.data_ptr(), q.ranges.data_ptr(), q.offsets.data_ptr(), rows,
+                                  codes_ptr, _lib.ptr(q.ranges), _lib.ptr(q.offsets), rows,
                                   d, q.bits, theta.contiguous().data_ptr(), dh.data_ptr(),
                                   dth.data_ptr(), ws.data_ptr(), ws_bytes, 0, _lib.stream_ptr(dev))
     _lib.check(st, "kgq_layer_backward_f32")

@@ -552,3 +552,35 @@ def test_scatter_rows_multi_edge_cases():
         out = F.scatter_rows_multi(rows, [torch.from_numpy(i).cuda() for i in idxs],
                                    [torch.from_numpy(g).cuda() for g in gs])
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32)), d
+
+
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_passthrough_layer_fused_forward_and_backward(d):
+    """b = 32 (quantize.py:182-183: the context is H itself, no tensor id):
+    the split layer keeps the SpMM output as the raw context (bit-exact SpMM),
+    E' = relu(H theta) to fp32 rounding, and the fused backward reads raw H
+    (FFMA d = 32/128, tcgen05 d = 64) -- vs float64."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(d + 1)
+    n = 3000
+    a = _hub_graph(n, d)
+    A = kgq.CSR.from_scipy(a)
+    e_np = rng.standard_normal((n, d), dtype=np.float32)
+    e = torch.from_numpy(e_np).cuda()
+    th = torch.from_numpy((rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
+    cfg = kgq.QuantConfig(bits=32)
+    st = kgq.RandomStream(3)
+    e_next, mask, q, h = F.graph_conv_forward(A, e, th, cfg, st, want_h=True)
+    assert st._next_tensor_id == 0 and q.bits == 32 and q.raw is not None
+    h_ref = orc.spmm_csr(a.indptr, a.indices, a.data, e_np)
+    assert np.array_equal(q.raw.cpu().numpy().view(np.uint32), h_ref.view(np.uint32))
+    j = h_ref.astype(np.float64) @ th.double().cpu().numpy()
+    np.testing.assert_allclose(e_next.cpu().numpy(), np.maximum(j, 0), rtol=1e-4, atol=1e-5)
+    gr = torch.from_numpy(rng.standard_normal((n, d), dtype=np.float32)).cuda()
+    ge = torch.from_numpy(rng.standard_normal((n, d), dtype=np.float32)).cuda()
+    dth, dh = F.layer_backward(gr, ge, mask, q, th)
+    gj = ((gr + ge) * mask.to_bool().reshape(n, d)).double()
+    np.testing.assert_allclose(dh.cpu().numpy(), (gj @ th.double().t()).cpu().numpy(), rtol=1e-4, atol=1e-5)
+    ref_dth = (torch.from_numpy(h_ref).double().cuda().t() @ gj).cpu().numpy()
+    np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(n))
