@@ -424,3 +424,72 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
         g_e = ops.spmm(a_local, gather(dh_local))
     dth = comm.all_reduce_sum(torch.stack(dthetas))
     return loss, g_e, list(dth.unbind(0))
+
+
+class PartitionedStepGraph:
+    """One rank's partitioned training step (``partitioned_step`` + Adam on the
+    rank's E0 rows and the thetas) captured once as a CUDA graph and replayed
+    per batch, with the same device-side counters as the single-GPU
+    ``train._StepGraph``: tensor ids advance on the device (``base``), Adam's
+    step and bias corrections come from ``step_rel`` / ``c12``.  The step has
+    fixed shapes and no host synchronisation, so the collectives (NCCL) are
+    captured with it; a replay equals the eager step bit for bit."""
+
+    def __init__(self, part: RowPartition, a_local, params: dict, state, cfg, stream: RandomStream, comm,
+                 n_layers: int, batch: int, capacity: int, layout: str = "global", halo=None, ops=GpuOps):
+        from .train import AdamState  # noqa: F401  (state is a train.AdamState)
+        dev = params["E0"].device
+        self.B, self.capacity, self.n_layers = batch, capacity, n_layers
+        sr = cfg.quant.rounding == "stochastic" and not cfg.quant.passthrough
+        self.n_tids = (n_layers + 3) if sr else 0
+        self.idx = torch.zeros((3, batch), dtype=torch.int64, device=dev)     # users, pos, neg node ids
+        self.base = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.step_rel = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.c12 = torch.ones(2 * (capacity + 1), dtype=torch.float32, device=dev)
+        host_tid = stream._next_tensor_id
+        stream.bind_device_base(self.base)
+        stream._next_tensor_id = 0
+        from . import _lib
+        self.graph = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(self.graph):
+                self.step_rel.add_(1)
+                thetas = [params[f"theta{i}"] for i in range(n_layers)]
+                loss, de0, dth = partitioned_step(part, a_local, params["E0"], thetas, self.idx[0], self.idx[1],
+                                                  self.idx[2], cfg.l2, cfg.quant, stream, comm, ops=ops,
+                                                  layout=layout, halo=halo)
+                grads = {"E0": de0}
+                grads.update({f"theta{i}": t for i, t in enumerate(dth)})
+                L = _lib.load()
+                for name, g in grads.items():
+                    p = params[name]
+                    st = L.kgq_adam_step_dev_f32(p.data_ptr(), g.contiguous().data_ptr(), state.m[name].data_ptr(),
+                                                 state.v[name].data_ptr(), p.numel(), cfg.lr, state.beta1,
+                                                 state.beta2, state.eps, self.c12.data_ptr(),
+                                                 self.step_rel.data_ptr(), _lib.stream_ptr(dev))
+                    _lib.check(st, "kgq_adam_step_dev_f32")
+                self.base.add_(self.n_tids)
+                self.loss = loss
+        finally:
+            stream.bind_device_base(None)
+            stream._next_tensor_id = host_tid
+
+    def run(self, batches, stream: RandomStream, state):
+        """Replay once per (users, pos, neg) node-id batch; returns the losses."""
+        from .train import _bias_rows
+        n = len(batches)
+        if n > self.capacity:
+            raise ValueError("graph capacity exceeded")
+        self.base.fill_(stream._next_tensor_id)
+        self.step_rel.zero_()
+        self.c12.copy_(torch.from_numpy(_bias_rows(state, state.step, self.capacity)))
+        losses = []
+        for u, p, ng in batches:
+            self.idx[0].copy_(u)
+            self.idx[1].copy_(p)
+            self.idx[2].copy_(ng)
+            self.graph.replay()
+            losses.append(self.loss.clone())
+        stream._next_tensor_id += n * self.n_tids
+        state.step += n
+        return losses

@@ -584,3 +584,56 @@ def test_passthrough_layer_fused_forward_and_backward(d):
     np.testing.assert_allclose(dh.cpu().numpy(), (gj @ th.double().t()).cpu().numpy(), rtol=1e-4, atol=1e-5)
     ref_dth = (torch.from_numpy(h_ref).double().cuda().t() @ gj).cpu().numpy()
     np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(n))
+
+
+def test_partitioned_step_graph_equals_eager():
+    """parallel.PartitionedStepGraph (the partitioned step + Adam captured as
+    one CUDA graph) replays bit-identically to the eager partitioned steps
+    (world size 1, SoloComm): tensor ids, Adam step and every parameter."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig, init_params
+    from paper_2212_04540_b200.parallel import (GpuOps, PartitionedStepGraph, RowPartition, SoloComm,
+                                                partitioned_step)
+    from paper_2212_04540_b200.train import AdamState, TrainConfig, adam_step
+    ds = D.synth_kg(D.SynthShape(600, 400, 1500, relations=5, interactions_per_user=20.0), seed=3)
+    ip, ix, vv = D.adjacency_arrays(ds)
+    part = RowPartition.build(ip, 1, 0)
+    a_local = GpuOps.local_adjacency(ip, ix, vv, 0, ds.num_nodes, ds.num_nodes, "cuda")
+    q = kgq.QuantConfig(bits=2)
+    mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), TrainConfig(quant=q, batch_size=256)
+    trip = torch.from_numpy(D.sample_negatives(ds, np.random.default_rng(0))).cuda().long()
+    U = ds.num_users
+    batches = [(trip[k * 256:(k + 1) * 256, 0], U + trip[k * 256:(k + 1) * 256, 1],
+                U + trip[k * 256:(k + 1) * 256, 2]) for k in range(5)]
+    outs = []
+    for graphs in (False, True):
+        p0 = init_params(ds.num_nodes, mcfg, 0)
+        local = {"E0": p0.entity_embeddings.clone()}
+        local.update({f"theta{i}": t.clone() for i, t in enumerate(p0.layer_weights)})
+        state, st = AdamState(local), kgq.RandomStream(0)
+        if graphs:
+            sg = PartitionedStepGraph(part, a_local, local, state, cfg, st, SoloComm(), 3, 256, 8)
+            # capture recorded nothing real: restore the initial parameters / state
+            local["E0"].copy_(p0.entity_embeddings)
+            for i, t in enumerate(p0.layer_weights):
+                local[f"theta{i}"].copy_(t)
+            for k in local:
+                state.m[k].zero_()
+                state.v[k].zero_()
+            losses = [float(x) for x in sg.run(batches, st, state)]
+        else:
+            losses = []
+            for u, pp, nn in batches:
+                th = [local[f"theta{i}"] for i in range(3)]
+                loss, de0, dth = partitioned_step(part, a_local, local["E0"], th, u, pp, nn, cfg.l2, q, st,
+                                                  SoloComm(), layout="global")
+                grads = {"E0": de0}
+                grads.update({f"theta{i}": g for i, g in enumerate(dth)})
+                adam_step(local, grads, state, cfg.lr)
+                losses.append(float(loss))
+        outs.append((losses, {k: v.clone() for k, v in local.items()}, st._next_tensor_id, state.step))
+    (l0, p0_, t0, s0), (l1, p1_, t1, s1) = outs
+    assert t0 == t1 and s0 == s1 and l0 == l1
+    for k in p0_:
+        assert torch.equal(p0_[k], p1_[k]), k
