@@ -242,6 +242,13 @@ KGQ_API int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx,
                                const int64_t *list_end, int32_t n_lists, const float *g,
                                int32_t d, float *out, void *stream);
 
+/* Rows idx of a sum of n_terms (<= 8) row-major n x d tensors, summed in
+ * order ((t_0 + t_1) + ...): the gather of the KGNN sum readout (model.py:86-88
+ * + tape.py:143-152) without materializing the sum.  terms: HOST array of
+ * device pointers (passed by value, graph-capturable); idx: device int64. */
+KGQ_API int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
+                            int64_t n_idx, int32_t d, float *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -308,3 +308,41 @@ extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *i
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Gather of a lazily-summed readout (tape.LazySumWire): out[i] =
+// ((t_0[idx[i]] + t_1[idx[i]]) + ...) in the terms' order -- the rows of
+// the materialized sum, bit for bit, in one launch instead of one gather per
+// term plus the adds.
+// ---------------------------------------------------------------------------
+constexpr int kMaxSumTerms = 8;
+struct SumTerms { const float *t[kMaxSumTerms]; };
+
+__global__ void gather_rows_sum_kernel(SumTerms terms, int n_terms, const int64_t *__restrict__ idx, int64_t n_idx,
+                                       int d, float *__restrict__ out) {
+    const int64_t total = n_idx * d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / d;
+        const int f = (int)(e - i * d);
+        const int64_t r = __ldg(idx + i);
+        float acc = __ldg(terms.t[0] + r * d + f);
+        for (int k = 1; k < n_terms; k++) acc = __fadd_rn(acc, __ldg(terms.t[k] + r * d + f));
+        out[e] = acc;
+    }
+}
+
+extern "C" int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
+                                       int64_t n_idx, int32_t d, float *out, void *stream) {
+    if (n_terms < 1 || n_terms > kMaxSumTerms || n_idx < 0 || d < 1 || !terms) return KGQ_ERR_INVALID_ARG;
+    if (n_idx == 0) return KGQ_OK;
+    if (!idx || !out) return KGQ_ERR_INVALID_ARG;
+    SumTerms t;                                     // host array of device pointers -> kernel parameter
+    for (int k = 0; k < kMaxSumTerms; k++) t.t[k] = k < n_terms ? terms[k] : nullptr;
+    for (int k = 0; k < n_terms; k++) if (!t.t[k]) return KGQ_ERR_INVALID_ARG;
+    const int64_t total = n_idx * d;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)kSMs * 8) blocks = (int64_t)kSMs * 8;
+    gather_rows_sum_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(t, n_terms, idx, n_idx, d, out);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -11,6 +11,7 @@ Each op is one (or two) libkgq launches on the current CUDA stream:
   :233-244) on torch ops in the reference's op order.
 """
 
+import ctypes
 import os
 
 import numpy as np
@@ -270,4 +271,18 @@ def scatter_rows_multi(src_rows: int, idxs, gs) -> torch.Tensor:
     st = _lib.load().kgq_scatter_rows_multi_f32(_lib.ptr(order), idx.data_ptr(), m, ends.ctypes.data, len(idxs),
                                                 g.data_ptr(), d, out.data_ptr(), _lib.stream_ptr(dev))
     _lib.check(st, "kgq_scatter_rows_multi_f32")
+    return out
+
+def gather_rows_sum(terms, idx64: torch.Tensor) -> torch.Tensor:
+    """((terms[0][idx] + terms[1][idx]) + ...) in one kernel
+    (kgq_gather_rows_sum_f32): the rows of the sum readout, bit-identical to
+    gathering the materialized sum."""
+    t0 = terms[0]
+    d = t0.shape[1]
+    out = torch.empty((idx64.shape[0], d), dtype=torch.float32, device=t0.device)
+    ptrs = (ctypes.c_void_p * len(terms))(*[t.data_ptr() for t in terms])
+    st = _lib.load().kgq_gather_rows_sum_f32(ctypes.cast(ptrs, ctypes.c_void_p), len(terms),
+                                             idx64.contiguous().data_ptr(), idx64.shape[0], d, out.data_ptr(),
+                                             _lib.stream_ptr(t0.device))
+    _lib.check(st, "kgq_gather_rows_sum_f32")
     return out

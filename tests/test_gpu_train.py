@@ -637,3 +637,16 @@ def test_partitioned_step_graph_equals_eager():
     assert t0 == t1 and s0 == s1 and l0 == l1
     for k in p0_:
         assert torch.equal(p0_[k], p1_[k]), k
+
+
+def test_gather_rows_sum_equals_gather_of_sum():
+    """kgq_gather_rows_sum_f32 == the rows of ((t0 + t1) + t2), bitwise."""
+    _kgq()
+    from paper_2212_04540_b200 import functional as F
+    g = torch.Generator(device="cuda").manual_seed(4)
+    ts = [torch.randn(5000, 64, device="cuda", generator=g) for _ in range(3)]
+    idx = torch.randint(0, 5000, (3072,), device="cuda", generator=g)
+    ref = ((ts[0] + ts[1]) + ts[2]).index_select(0, idx)
+    out = F.gather_rows_sum(ts, idx)
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    assert torch.equal(F.gather_rows_sum(ts[:1], idx), ts[0].index_select(0, idx))
