@@ -747,6 +747,31 @@ def run_ours(args):
                 except Exception as exc:
                     train["lastfm"]["quality"] = {"error": f"{type(exc).__name__}: {exc}"}
 
+    verification = None
+    if world == 1 and not args.skip_verification:
+        # SURVEY 8(a) a18 at the reference's full scale (quantize.py:358-412:
+        # 100 rows x d=64 x 1e5 draws x 4 widths), every draw through K1
+        torch.cuda.empty_cache()
+        try:
+            from paper_2212_04540_b200 import verification as V
+            verification = {"scale": "100 rows x d=64 x 1e5 draws x bits 1/2/4/8, seed 0 (the reference's sweep)",
+                            "reference_seconds": 25.3,
+                            "reference_source": "pkg/test_output.txt:10 (SURVEY.md 8(a) a18)",
+                            "note": "criterion (a) is a fixed-seed 4-sigma test over 6,400 elements per width; "
+                                    "over seeds 0-11 it trips in 3/48 (fast) and 5/48 (compat = numpy's "
+                                    "Philox4x64-10) cells (profiles/r1_verification_seeds.json)"}
+            for rng_name in ("fast", "compat"):
+                t0 = time.perf_counter()
+                rep = V.quantizer_verification(bits_list=(1, 2, 4, 8), n_rows=100, dim=64, trials=100000,
+                                               seed=0, rng=rng_name)
+                torch.cuda.synchronize()
+                verification[rng_name] = {
+                    "passed": rep["passed"], "seconds": round(time.perf_counter() - t0, 2),
+                    "bits": {str(b): {k: round(v, 4) if isinstance(v, float) else v for k, v in e.items()}
+                             for b, e in rep["bits"].items()}}
+        except Exception as exc:
+            verification = {"error": f"{type(exc).__name__}: {exc}"}
+
     industry = None
     if args.industry and world == 1:
         torch.cuda.empty_cache()
@@ -794,6 +819,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "train": train,
             **({"industry": industry} if industry is not None else {}),
+            **({"verification": verification} if verification is not None else {}),
             "native_lib": os.path.relpath(_lib.LIB_PATH, ROOT),
         }
         print(json.dumps(line), flush=True)
@@ -824,6 +850,7 @@ def main():
     ap.add_argument("--skip-train", action="store_true")
     ap.add_argument("--skip-quality", action="store_true")
     ap.add_argument("--skip-lastfm", action="store_true")
+    ap.add_argument("--skip-verification", action="store_true")
     ap.add_argument("--industry", action="store_true", help="configs[4] per-rank shard measurement")
     ap.add_argument("--industry-world", type=int, default=8)
     ap.add_argument("--industry-ranks", default="0")
