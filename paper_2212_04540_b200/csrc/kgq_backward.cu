@@ -36,7 +36,10 @@ struct BwdSmem {
 #define KGQ_BWD_MINB 1
 #endif
 template <int D, int BITS>
-__global__ void __launch_bounds__(256, D > 64 ? 1 : KGQ_BWD_MINB)
+#ifndef KGQ_BWD128_MINB
+#define KGQ_BWD128_MINB 1
+#endif
+__global__ void __launch_bounds__(256, D > 64 ? KGQ_BWD128_MINB : KGQ_BWD_MINB)
 layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
                       const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
                       const float *__restrict__ ranges, const float *__restrict__ offsets,
