@@ -24,6 +24,7 @@ from kgact.data import parse_synth_spec, synth_generate  # noqa: E402
 from paper_2212_04540_b200 import data as D  # noqa: E402
 
 SPECS = {
+    "default": "default",     # the reference's acceptance-test dataset (test_acceptance.py:44-45)
     "amazon": "default,users=70679,items=24915,entities=88572,relations=39,"
               "interactions_per_user=12,attr_links_per_item=101.7",
     "lastfm": "default,users=23566,items=48123,entities=58266,relations=9,"

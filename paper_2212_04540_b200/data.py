@@ -181,7 +181,7 @@ def load_compact(path) -> KgDataset:
         return unpack_dataset(z)
 
 
-REFERENCE_DATASETS = ("amazon", "lastfm")
+REFERENCE_DATASETS = ("amazon", "lastfm", "default")
 
 
 def reference_dataset(name: str) -> KgDataset:

@@ -650,3 +650,49 @@ def test_gather_rows_sum_equals_gather_of_sum():
     out = F.gather_rows_sum(ts, idx)
     assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
     assert torch.equal(F.gather_rows_sum(ts[:1], idx), ts[0].index_select(0, idx))
+
+
+def test_acceptance_criterion_4_memory_accounting():
+    """The reference's acceptance criterion 4 (test_acceptance.py:169-189) on
+    its default dataset: stored-bytes formula exact, 3-layer d=64 INT2
+    compression ratio in [6, 11], bytes strictly monotone over b in
+    {8, 4, 2, 1}, b=32 ratio 1."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig
+    from paper_2212_04540_b200.train import TrainConfig, bench_memory
+    st = kgq.RandomStream(0)
+    q = kgq.quantize_tensor(torch.zeros((1000, 64), device="cuda"), kgq.QuantConfig(bits=2), st)
+    assert kgq.stored_bytes(q) == 24000
+    q1 = kgq.quantize_tensor(torch.zeros((7, 5), device="cuda"), kgq.QuantConfig(bits=1), st)
+    assert kgq.stored_bytes(q1) == 7 * ((5 + 7) // 8 + 8)
+    ds = D.reference_dataset("default")
+    rows = bench_memory(ds, ModelConfig(layers=3, dim=64), TrainConfig(batch_size=1024, epochs=1, seed=0))
+    by = {r["bits"]: r for r in rows}
+    assert 6.0 <= by[2]["compression_ratio"] <= 11.0
+    sizes = [by[b]["activation_bytes_peak"] for b in (8, 4, 2, 1)]
+    assert all(a > b for a, b in zip(sizes, sizes[1:]))
+    assert by[32]["compression_ratio"] == 1.0
+
+
+def test_acceptance_criterion_5_accuracy_parity():
+    """The reference's acceptance criterion 5 (test_acceptance.py:192-213):
+    Recall@20 averaged over 5 seeds on the default dataset (batch 256, 20
+    epochs): INT8/FP32 >= 0.98 and INT2/FP32 >= 0.95."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.model import ModelConfig
+    from paper_2212_04540_b200.train import TrainConfig, train_run
+    ds = D.reference_dataset("default")
+    adj = D.build_adjacency(ds)
+    means = {}
+    for bits in (32, 8, 2):
+        rec = []
+        for seed in range(5):
+            q = kgq.QuantConfig(bits=bits)
+            cfg = TrainConfig(seed=seed, quant=q, batch_size=256, epochs=20, lr=1e-3, l2=1e-5)
+            _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q), cfg, adjacency=adj, graphs=True)
+            rec.append(rep["metrics"]["recall_at_20"])
+        means[bits] = float(np.mean(rec))
+    assert means[8] / means[32] >= 0.98, means
+    assert means[2] / means[32] >= 0.95, means
