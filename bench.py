@@ -324,6 +324,32 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
                                "kind": "port",
                                "sample": "2 fp32 steps of oracle.dense_step (numpy/scipy restatement of "
                                          "the reference Tape step, no quantization) on the same graph"}
+    if world == 1 and shape in ("amazon", "lastfm"):
+        # the step's dominant kernel (K4 SpMM, ~60 % of the step): its L2
+        # random-row gather rate against the ceiling measured by
+        # tools/tc_probe/l2_gather.cu on this pool (profiles/r1_l2_gather_ceiling.json)
+        from paper_2212_04540_b200 import tensorops as TO
+        adj = D.build_adjacency(ds)
+        x = torch.randn(ds.num_nodes, 64, device="cuda")
+        TO.spmm(adj, x)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        a.record(cur)
+        for _ in range(20):
+            TO.spmm(adj, x)
+        b.record(cur)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / 20 * 1e3
+        gbs = adj.nnz * (64 * 4 + 8) / us / 1e3
+        ceil_path = os.path.join(ROOT, "profiles", "r1_l2_gather_ceiling.json")
+        ceiling = json.load(open(ceil_path))["GBps"] if os.path.exists(ceil_path) else None
+        out["roofline_spmm"] = {"kernel": "spmm_kernel (K4, bit-exact ordered CSR SpMM)", "bound": "l2-gather",
+                                "us": round(us, 1), "achieved": round(gbs, 1), "unit": "GB/s",
+                                "peak": ceiling, "frac": round(gbs / ceiling, 4) if ceiling else None,
+                                "peak_source": "measured L2 random-row gather ceiling (tools/tc_probe/l2_gather.cu)",
+                                "bytes_per_nnz": 64 * 4 + 8}
+        del x
     if mem2 is not None:
         mb = lambda v: round(v / 1e6, 3)
         out["activation_MB"] = {
