@@ -556,10 +556,103 @@ static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_gr
     return false;
 }
 
+// K2 for wide groups (G = 128 / 256): a warp per group, lane l owns float4
+// l + 32h (h < G/128), so every store instruction writes 512 contiguous bytes
+// (the 4-lanes-per-group kernel scatters 64-byte pieces 1 KB apart at G = 256
+// and stalls on the store queue).  The group's code words are loaded once
+// (coalesced u32) and each lane takes its 4*BITS bits with one shuffle; the
+// 2^b reconstruction values (b <= 4) come from a per-warp smem table built
+// with the same IEEE lut_entry; b = 8 divides per element exactly as K2 does.
+template <int G, int BITS>
+__global__ void __launch_bounds__(kThreads)
+dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
+                       const float *__restrict__ offsets, int64_t n_groups, float *__restrict__ out) {
+    constexpr int GB = G * BITS / 8;                     // code bytes per group
+    constexpr int NW = GB / 4;                           // code words per group
+    constexpr int WPL = (NW + 31) / 32;                  // words per lane
+    constexpr int H = G / 128;                           // float4 per lane
+    constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    __shared__ float lut[kWarps][NL];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t stride = (int64_t)gridDim.x * kWarps;
+    int64_t g = (int64_t)blockIdx.x * kWarps + warp;
+    uint32_t cw[WPL];
+    float rn = 0.f, zn = 0.f;
+    auto fetch = [&](int64_t gg) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(codes + gg * GB);
+#pragma unroll
+        for (int k = 0; k < WPL; k++)
+            cw[k] = (lane + 32 * k < NW) ? __ldg(src + lane + 32 * k) : 0u;
+        rn = __ldg(ranges + gg);
+        zn = __ldg(offsets + gg);
+    };
+    if (g < n_groups) fetch(g);
+    for (; g < n_groups; g += stride) {
+        uint32_t w[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; k++) w[k] = cw[k];
+        const float r = rn, z = zn;
+        if (NL > 1) {
+            if (lane < NL) lut[warp][lane] = lut_entry<BITS>(r, z, lane);
+            __syncwarp();
+        }
+        if (g + stride < n_groups) fetch(g + stride);
+        DivR dB;
+        if (BITS == 8) dB = make_div(Bf);
+        const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
+        float4 *dst = reinterpret_cast<float4 *>(out) + g * (G / 4);
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+            const int e0 = 4 * (lane + 32 * h);          // first element of my float4
+            const int bit = e0 * BITS;                   // 4*BITS bits, inside one word
+            const int wi = bit >> 5;                     // < 32 except b = 8 (then = lane + 32h)
+            const uint32_t word = __shfl_sync(0xffffffffu, w[BITS == 8 ? (h < WPL ? h : 0) : 0], wi & 31);
+            const uint32_t piece = word >> (bit & 31);
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t c = (piece >> (BITS * e)) & PackInfo<BITS>::B;
+                if (NL > 1) {
+                    o[e] = lut[warp][c];
+                } else if (r == 0.0f) {
+                    o[e] = z;
+                } else {
+                    const float t = __fmul_rn(r, __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f));
+                    float qv;
+                    if (rfast) {
+                        const float q0 = __fmul_rn(t, dB.y);
+                        const float er = __fmaf_rn(-Bf, q0, t);
+                        qv = __fmaf_rn(dB.y, er, q0);
+                    } else {
+                        qv = __fdiv_rn(t, Bf);
+                    }
+                    o[e] = __fadd_rn(qv, z);
+                }
+            }
+            stg_stream(dst + lane + 32 * h, make_float4(o[0], o[1], o[2], o[3]));
+        }
+        if (NL > 1) __syncwarp();
+    }
+}
+
 template <int G>
 static bool dispatch_dequant_bits(int bits, const uint8_t *codes, const float *ranges,
                                   const float *offsets, int64_t n_groups, float *out,
                                   cudaStream_t s) {
+#ifndef KGQ_DQ_WIDE
+#define KGQ_DQ_WIDE 1
+#endif
+    if (KGQ_DQ_WIDE && G >= 128) {
+        const int grid = grid_for(n_groups, kWarps, 8);
+        switch (bits) {
+            case 1: dequantize_wide_kernel<G, 1><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+            case 2: dequantize_wide_kernel<G, 2><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+            case 4: dequantize_wide_kernel<G, 4><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+            case 8: dequantize_wide_kernel<G, 8><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        }
+        return false;
+    }
     const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
     const int grid = grid_for(tiles, kWarps, 8);
     switch (bits) {
