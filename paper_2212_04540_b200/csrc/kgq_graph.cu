@@ -587,8 +587,11 @@ struct EpiTile {
     static constexpr size_t smem = ((size_t)D * D + (size_t)D * RS) * sizeof(float);
 };
 
+#ifndef KGQ_EPI_MINB
+#define KGQ_EPI_MINB 1
+#endif
 template <int D, int BITS, int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, KGQ_EPI_MINB)
 layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
                       uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
                       int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
