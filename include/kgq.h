@@ -249,6 +249,15 @@ KGQ_API int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx,
 KGQ_API int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
                             int64_t n_idx, int32_t d, float *out, void *stream);
 
+/* Per-row Top-K of an evaluation score block (replaces train.py:141-143:
+ * s[train positives] = -inf; np.argsort(-s, kind="stable")[:k]): for each of
+ * n_rows rows (row stride ld floats) the indices of the k best of n_cols
+ * scores, best first; descending score, ties by ascending index, -0.0 == +0.0,
+ * -inf after every finite score, NaN last; -1 past n_cols.  1 <= k <= 64;
+ * out_idx: n_rows x k int32.  Reads the block once, no workspace. */
+KGQ_API int kgq_topk_rows_f32(const float *scores, int64_t n_rows, int64_t n_cols, int64_t ld, int32_t k,
+                      int32_t *out_idx, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

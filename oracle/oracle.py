@@ -263,3 +263,43 @@ def adam_step(params: dict, grads: dict, m: dict, v: dict, t: int, lr: float,
         m_hat = mm / (1 - b1 ** t)
         v_hat = vv / (1 - b2 ** t)
         params[name] -= lr * m_hat / (np.sqrt(v_hat) + eps)
+
+
+# ---------------------------------------------------------------------------
+# Evaluation (kgact/train.py:108-160), restated in numpy
+# ---------------------------------------------------------------------------
+
+def topk_stable(scores: np.ndarray, k: int) -> np.ndarray:
+    """train.py:143: ``np.argsort(-s, kind="stable")[:k]`` per row (float64)."""
+    s = np.asarray(scores, dtype=np.float64)
+    return np.argsort(-s, axis=1, kind="stable")[:, :k]
+
+
+def evaluate(num_users: int, num_items: int, train: np.ndarray, test: np.ndarray,
+             readout: np.ndarray, k: int):
+    """train.py:119-160: mean Recall@k / NDCG@k over the users with test
+    pairs; train positives set to -inf before the stable ranking; readout
+    scores in float32 (readout[u] @ item_emb.T), ranked in float64."""
+    test_pos: dict[int, list[int]] = {}
+    for u, i in np.asarray(test):
+        test_pos.setdefault(int(u), []).append(int(i))
+    train_pos: dict[int, set] = {}
+    for u, i in np.asarray(train):
+        train_pos.setdefault(int(u), set()).add(int(i))
+    users = sorted(test_pos)
+    if not users:
+        raise ValueError("test split is empty")
+    item_emb = readout[num_users:num_users + num_items]
+    recalls, ndcgs = [], []
+    for u in users:
+        s = np.asarray(readout[u] @ item_emb.T, dtype=np.float64)
+        held = sorted(train_pos.get(u, ()))
+        if held:
+            s[held] = -np.inf
+        top = topk_stable(s[None, :], k)[0]
+        pos = set(test_pos[u])
+        hits = [r for r, item in enumerate(top, start=1) if int(item) in pos]
+        recalls.append(len(hits) / len(pos))
+        idcg = sum(1.0 / np.log2(r + 1) for r in range(1, min(len(pos), k) + 1))
+        ndcgs.append(sum(1.0 / np.log2(r + 1) for r in hits) / idcg)
+    return float(np.mean(recalls)), float(np.mean(ndcgs))

@@ -286,3 +286,20 @@ def gather_rows_sum(terms, idx64: torch.Tensor) -> torch.Tensor:
                                              _lib.stream_ptr(t0.device))
     _lib.check(st, "kgq_gather_rows_sum_f32")
     return out
+
+
+def topk_rows(scores: torch.Tensor, k: int) -> torch.Tensor:
+    """Indices of the k best entries of every row of a fp32 score block, best
+    first, ties by ascending column (kgq_topk_rows_f32; the stable
+    ``np.argsort(-s, kind="stable")[:k]`` of train.py:141-143); int32, -1
+    past the row length.  1 <= k <= 64."""
+    if scores.dtype != torch.float32 or scores.dim() != 2 or not scores.is_cuda:
+        raise TypeError("topk_rows: expected a 2-D fp32 CUDA tensor")
+    if scores.stride(1) != 1:
+        scores = scores.contiguous()
+    n, m = scores.shape
+    out = torch.empty((n, k), dtype=torch.int32, device=scores.device)
+    st = _lib.load().kgq_topk_rows_f32(scores.data_ptr(), n, m, scores.stride(0), k, out.data_ptr(),
+                                       _lib.stream_ptr(scores.device))
+    _lib.check(st, "kgq_topk_rows_f32")
+    return out

@@ -146,3 +146,19 @@ def test_fast_stream_is_philox4x32_7():
             call = 4 * (k >> 5) + ((k >> 2) & 3)
             w = _philox4x32_py([call, g, 0, tid & 0xFFFFFFFF], key, 7)[k & 3]
             assert int(u[g, k]) == (w >> (16 * ((k >> 4) & 1))) & 0xFFFF
+
+
+@pytest.mark.parametrize("name", ["int", "gauss"])
+def test_oracle_evaluate_matches_reference(name):
+    """oracle.evaluate (train.py:119-160 restated) == kgact.train.evaluate on
+    the fixture (tests/golden/make_eval_golden.py)."""
+    z = golden_io.load("eval")
+    for k, want in zip(z["ks"], z[f"metrics_{name}"]):
+        got = orc.evaluate(int(z["num_users"]), int(z["num_items"]), z["train"], z["test"],
+                           z[f"readout_{name}"], int(k))
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-15)
+
+
+def test_oracle_topk_stable_order():
+    s = np.array([[1.0, 3.0, 3.0, -np.inf, 0.0, -0.0, np.nan, 3.0]])
+    assert orc.topk_stable(s, 8)[0].tolist() == [1, 2, 7, 0, 4, 5, 3, 6]
