@@ -8,11 +8,12 @@
 //   hi = order-preserving bits of the score (NaN -> 0), lo = ~index,
 // so "larger key" == "ranks earlier" and all keys of a row are distinct.
 //
-// One warp per row: lane l scans items l, l+32, ... keeping its own best KM
-// keys in registers (sorted, fully unrolled insertion; an item only enters
-// when it beats both the lane's KM-th key and the warp-wide threshold), then
-// k rounds of a warp argmax over the lane heads pop the row's top-k in order.  The score block is read
-// once, coalesced; nothing is written but k indices per row.
+// One warp per row streams the row as float4 (scalar head/tail around the
+// 16-byte boundaries) and keeps the row's exact running top-k as a sorted list
+// distributed over the lanes (entry i in lane i % 32).  A key enters only if
+// it beats entry k-1 (a ballot per loaded element; after the first few passes
+// almost nothing does), by one ballot-count + shuffle-up.  The score block is
+// read once, coalesced; nothing is written but k indices per row.
 #include "kgq_common.cuh"
 
 namespace kgq {
@@ -25,59 +26,102 @@ __device__ __forceinline__ uint64_t rank_key(float s, uint32_t idx) {
     return ((uint64_t)o << 32) | (uint64_t)(0xFFFFFFFFu - idx);
 }
 
-template <int KM>
+// The row's running top-k, distributed over the warp: entry i lives in lane
+// i % 32 of register i / 32 (NR registers, k <= 32 * NR), descending; 0 = empty.
+template <int NR>
+struct WarpList {
+    uint64_t e[NR];
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int r = 0; r < NR; r++) e[r] = 0ull;
+    }
+    // entry j (warp-uniform j), broadcast to every lane
+    __device__ __forceinline__ uint64_t at(int j) const {
+        uint64_t v = e[0];
+#pragma unroll
+        for (int r = 1; r < NR; r++)
+            if ((j >> 5) == r) v = e[r];
+        return __shfl_sync(0xffffffffu, v, j & 31);
+    }
+    // insert a key larger than entry k-1 (warp-uniform x; keys are distinct)
+    __device__ __forceinline__ void insert(uint64_t x, int lane) {
+        int pos = 0;
+#pragma unroll
+        for (int r = 0; r < NR; r++) pos += __popc(__ballot_sync(0xffffffffu, e[r] > x));
+        uint64_t carry = 0ull;                       // entry 32r - 1 of the old list
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            const uint64_t up = __shfl_up_sync(0xffffffffu, e[r], 1);
+            const uint64_t last = __shfl_sync(0xffffffffu, e[r], 31);
+            const int j = 32 * r + lane;
+            const uint64_t shifted = lane == 0 ? carry : up;
+            e[r] = j < pos ? e[r] : (j == pos ? x : shifted);
+            carry = last;
+        }
+    }
+};
+
+template <int NR>
 __global__ void __launch_bounds__(256)
 topk_rows_kernel(const float *__restrict__ scores, int64_t n_rows, int64_t n_cols, int64_t ld, int k,
                  int32_t *__restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (row >= n_rows) return;
+    if (row >= n_rows) return;                       // warp-uniform
     const float *s = scores + row * ld;
-    uint64_t L[KM];                     // descending; 0 = empty (below every real key)
-#pragma unroll
-    for (int j = 0; j < KM; j++) L[j] = 0ull;
-    // thr = max over lanes of their KM-th best: that lane holds KM keys >= thr,
-    // so no key below it can reach the row's top KM >= k (warp-shared pruning)
-    uint64_t thr = 0ull;
-    auto insert = [&](uint64_t x) {
-        if (x <= thr || x <= L[KM - 1]) return;
-#pragma unroll
-        for (int j = KM - 1; j > 0; j--) {
-            if (x > L[j - 1]) L[j] = L[j - 1];
-            else if (x > L[j]) L[j] = x;
+    WarpList<NR> L;
+    L.clear();
+    uint64_t thr = 0ull;                             // entry k-1: the bar a key must clear
+    // one candidate key per lane: every lane whose key clears the bar joins,
+    // in lane order, re-checked against the bar as it rises
+    auto offer = [&](uint64_t key, bool valid) {
+        uint32_t m = __ballot_sync(0xffffffffu, valid && key > thr);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const uint64_t x = __shfl_sync(0xffffffffu, key, src);
+            if (x > thr) {
+                L.insert(x, lane);
+                thr = L.at(k - 1);
+            }
         }
-        if (x > L[0]) L[0] = x;
     };
-    int64_t c = lane;
-    for (; c + 96 < n_cols; c += 128) {             // 4 loads in flight per lane
-        const float v0 = __ldg(s + c), v1 = __ldg(s + c + 32), v2 = __ldg(s + c + 64), v3 = __ldg(s + c + 96);
-        insert(rank_key(v0, (uint32_t)c));
-        insert(rank_key(v1, (uint32_t)(c + 32)));
-        insert(rank_key(v2, (uint32_t)(c + 64)));
-        insert(rank_key(v3, (uint32_t)(c + 96)));
-        uint64_t t = L[KM - 1];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, t, o);
-            t = other > t ? other : t;
-        }
-        thr = t;
+    // head: scalar items up to the first 16-byte boundary of the row
+    const int64_t h0 = (int64_t)((4u - (((uintptr_t)s >> 2) & 3u)) & 3u);
+    const int64_t head = h0 < n_cols ? h0 : n_cols;
+    offer(lane < head ? rank_key(__ldg(s + lane), (uint32_t)lane) : 0ull, lane < head);
+    // body: float4 per lane, two per pass (256 items per warp per pass), the
+    // next pass's two loaded before this one is ranked; warp-uniform trips
+    const float4 *s4 = reinterpret_cast<const float4 *>(s + head);
+    const int64_t n4 = (n_cols - head) >> 2;
+    const float4 none = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 na = lane < n4 ? __ldg(s4 + lane) : none;
+    float4 nb = lane + 32 < n4 ? __ldg(s4 + lane + 32) : none;
+    for (int64_t base = 0; base < n4; base += 64) {
+        const int64_t fa = base + lane, fb = fa + 32;
+        const float4 a = na, b = nb;
+        na = fa + 64 < n4 ? __ldg(s4 + fa + 64) : none;
+        nb = fb + 64 < n4 ? __ldg(s4 + fb + 64) : none;
+        const uint32_t ia = (uint32_t)(head + 4 * fa), ib = (uint32_t)(head + 4 * fb);
+        const bool va = fa < n4, vb = fb < n4;
+        offer(rank_key(a.x, ia), va);
+        offer(rank_key(a.y, ia + 1), va);
+        offer(rank_key(a.z, ia + 2), va);
+        offer(rank_key(a.w, ia + 3), va);
+        offer(rank_key(b.x, ib), vb);
+        offer(rank_key(b.y, ib + 1), vb);
+        offer(rank_key(b.z, ib + 2), vb);
+        offer(rank_key(b.w, ib + 3), vb);
     }
-    for (; c < n_cols; c += 32) insert(rank_key(__ldg(s + c), (uint32_t)c));
-    // k rounds: warp max over the lane heads; the winning lane pops its head
-    for (int r = 0; r < k; r++) {
-        uint64_t best = L[0];
+    // tail: the last (n_cols - head) % 4 items
+    const int64_t t0 = head + 4 * n4;
+    const bool vt = lane < n_cols - t0;
+    offer(vt ? rank_key(__ldg(s + t0 + lane), (uint32_t)(t0 + lane)) : 0ull, vt);
+    // entries 0..k-1 are the answer, best first
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, best, o);
-            best = other > best ? other : best;
-        }
-        if (lane == 0) out[row * k + r] = best ? (int32_t)(0xFFFFFFFFu - (uint32_t)best) : -1;
-        if (best != 0ull && L[0] == best) {          // keys are distinct: exactly one lane
-#pragma unroll
-            for (int j = 0; j < KM - 1; j++) L[j] = L[j + 1];
-            L[KM - 1] = 0ull;
-        }
+    for (int r = 0; r < NR; r++) {
+        const int j = 32 * r + lane;
+        if (j < k) out[row * k + j] = L.e[r] ? (int32_t)(0xFFFFFFFFu - (uint32_t)L.e[r]) : -1;
     }
 }
 
@@ -94,9 +138,8 @@ extern "C" int kgq_topk_rows_f32(const float *scores, int64_t n_rows, int64_t n_
     const int64_t blocks = (n_rows + 7) / 8;
     if (blocks > 0x7fffffff) return KGQ_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (k <= 16) topk_rows_kernel<16><<<(int)blocks, 256, 0, st>>>(scores, n_rows, n_cols, ld, k, out_idx);
-    else if (k <= 32) topk_rows_kernel<32><<<(int)blocks, 256, 0, st>>>(scores, n_rows, n_cols, ld, k, out_idx);
-    else topk_rows_kernel<64><<<(int)blocks, 256, 0, st>>>(scores, n_rows, n_cols, ld, k, out_idx);
+    if (k <= 32) topk_rows_kernel<1><<<(int)blocks, 256, 0, st>>>(scores, n_rows, n_cols, ld, k, out_idx);
+    else topk_rows_kernel<2><<<(int)blocks, 256, 0, st>>>(scores, n_rows, n_cols, ld, k, out_idx);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
