@@ -78,3 +78,20 @@ def test_evaluate_matches_reference_golden(name):
     for k, want in zip(z["ks"], z[f"metrics_{name}"]):
         got = evaluate(ds, r, int(k))
         np.testing.assert_allclose(got, want, rtol=0, atol=1e-12)
+
+
+def test_evaluate_duplicate_test_pairs_and_chunking():
+    """Duplicate test pairs count once (the reference's ``set(test_pos[u])``)
+    and the user chunking does not change the result (oracle.evaluate)."""
+    from paper_2212_04540_b200.data import KgDataset
+    from paper_2212_04540_b200.train import evaluate
+    z = golden_io.load("eval")
+    nu, ni = int(z["num_users"]), int(z["num_items"])
+    readout = z["readout_int"]
+    test = np.concatenate([z["test"], z["test"][::4]], 0)
+    ds = KgDataset(nu, ni, readout.shape[0] - nu, z["train"], np.zeros((0, 2), np.int32), test,
+                   np.zeros((0, 3), np.int32), 1)
+    want = orc.evaluate(nu, ni, z["train"], test, readout, 20)
+    r = torch.from_numpy(readout).cuda()
+    for chunk in (None, 7, 64):
+        np.testing.assert_allclose(evaluate(ds, r, 20, chunk=chunk), want, rtol=0, atol=1e-12)
