@@ -587,15 +587,18 @@ struct EpiTile {
     static constexpr size_t smem = ((size_t)D * D + (size_t)D * RS) * sizeof(float);
 };
 
-// Min CTAs/SM at d <= 64 (fast/nearest modes).  5 (<= 51 registers, no
-// spills) is 67 -> 60 us in the warm layer loop of tools/spmm_ab.py but no
-// faster inside the captured training step (1.345 vs 1.332 ms) and slower
-// cold under ncu (55.7 vs 50.9 us), so the default stays 1.
-#ifndef KGQ_EPI_MINB
-#define KGQ_EPI_MINB 1
+// Occupancy: plain __launch_bounds__(256) gives 64 registers (4 CTAs/SM).
+// -DKGQ_EPI_MINB=n asks for n CTAs/SM at d <= 64 (fast/nearest modes): 5 is
+// faster in the warm layer loop of tools/spmm_ab.py (60 vs 67 us) but not
+// inside the captured training step (1.345 vs 1.332 ms); an explicit 1 lets
+// ptxas take 91 registers (2 CTAs/SM) and costs the step ~3 % (1.368 ms).
+#ifdef KGQ_EPI_MINB
+#define KGQ_EPI_BOUNDS __launch_bounds__(256, (D <= 64 && MODE != KGQ_ROUND_SR_COMPAT) ? KGQ_EPI_MINB : 1)
+#else
+#define KGQ_EPI_BOUNDS __launch_bounds__(256)
 #endif
 template <int D, int BITS, int MODE>
-__global__ void __launch_bounds__(256, (D <= 64 && MODE != KGQ_ROUND_SR_COMPAT) ? KGQ_EPI_MINB : 1)
+__global__ void KGQ_EPI_BOUNDS
 layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
                       uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
                       int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
