@@ -387,6 +387,7 @@ def quality_bench(args, shape=None):
         out[name] = {"recall_at_20": round(m["recall_at_20"], 5), "ndcg_at_20": round(m["ndcg_at_20"], 5),
                      "loss_curve": [round(v, 6) for v in rep["loss_curve"]],
                      "epoch_s": [round(v, 3) for v in rep["timing"]["epoch_seconds"]],
+                     "eval_s": round(rep["timing"]["eval_seconds"], 4),
                      "activation_bytes_peak": rep["memory"]["activation_bytes_peak"]}
     ref_path = os.path.join(ROOT, "datasets", f"{shape}_seed0_reference_runs.json")
     if os.path.exists(ref_path):
