@@ -497,9 +497,13 @@ static inline int grid_for(int64_t work_items, int per_block, int max_blocks_per
     return (int)b;
 }
 
-// T = threads per group: 2 for G <= 64 (less per-group overhead), 4 above
-// (keeps registers and the prefetch ring small).
+// T = threads per group: 4 (registers and the prefetch ring stay small;
+// -DKGQ_T64_2 builds the 2-thread variant for G = 64: measured 58 % vs 81 %
+// of the HBM peak on configs[1], so 4 stays).
 template <int G> struct PickT { static constexpr int T = 4; };
+#ifdef KGQ_T64_2   // A/B switch: 2 threads per 64-element group
+template <> struct PickT<64> { static constexpr int T = 2; };
+#endif
 
 template <int G, int BITS, int MODE>
 static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, float *ranges,
