@@ -512,7 +512,10 @@ static void launch_quant_t4(const float *x, int64_t n_groups, uint8_t *codes, fl
     constexpr int T = PickT<G>::T;
     using GE = Geo<G, T>;
     const int64_t tiles = (n_groups + GE::GPW - 1) / GE::GPW;
-    const int grid = grid_for(tiles, kWarps, 8);
+#ifndef KGQ_QGRID_PER_SM
+#define KGQ_QGRID_PER_SM 8   // 3 / 6: -1..-3 %; 12 / 16 / 32: within noise of 8 (configs[1])
+#endif
+    const int grid = grid_for(tiles, kWarps, KGQ_QGRID_PER_SM);
     const size_t smem = GE::S > 1 ? (size_t)kWarps * GE::S * GE::NF * 32 * sizeof(float4) : 0;
     if (smem > 0) {   // dynamic + static smem may exceed the 48 KB default
         static unsigned attr_set = 0;   // per template instance, bit per device
