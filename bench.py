@@ -230,7 +230,7 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
            "steps_per_epoch": steps_per_epoch, "n_gpus": world}
     res = {}
     for bits in ((2, 4, 32) if with_fp32 else (2,)):
-        q = kgq.QuantConfig(bits=bits)
+        q = kgq.QuantConfig(bits=bits, rng="fast")
         mcfg = ModelConfig(layers=3, dim=64, quant=q)
         cfg = TrainConfig(quant=q)
         rng = np.random.default_rng(0)
@@ -432,7 +432,7 @@ def industry_bench(args):
                        f"{INDUSTRY.entities} entities), {n_triples_edges} KG edges + {n_train} train pairs, "
                        f"adjacency nnz {nnz_total}; KGNN {L} layers d={d}, batch {B}, INT2 stochastic (fast rng)",
            "world": W, "generator_degrees_s": round(t_deg, 2), "ranks": {}}
-    cfg = kgq.QuantConfig(bits=2)
+    cfg = kgq.QuantConfig(bits=2, rng="fast")
     for rank in ranks:
         t1 = time.perf_counter()
         lo, hi = int(cuts[rank]), int(cuts[rank + 1])

@@ -127,7 +127,8 @@ static void quantize_groups(const float *x, int64_t g0, int64_t g1, int64_t G, i
     for (int64_t g = g0; g < g1; g++) {
         const float *row = x + g * G;
         float mn = row[0], mx = row[0];
-        for (int64_t k = 1; k < G; k++) {            /* x.min / x.max, :184-185 */
+        for (int64_t k = 1; k < G && mn == mn; k++) { /* x.min / x.max, :184-185 */
+            if (row[k] != row[k]) { mn = mx = row[k]; break; }   /* numpy propagates NaN */
             if (row[k] < mn) mn = row[k];
             if (row[k] > mx) mx = row[k];
         }
@@ -148,6 +149,7 @@ static void quantize_groups(const float *x, int64_t g0, int64_t g1, int64_t G, i
             }
             if (s < 0.0f) s = 0.0f;                   /* clip :125               */
             if (s > B) s = B;
+            if (s != s) s = 0.0f;                     /* inf/inf: numpy's NaN cast gives code 0 */
             float code;
             if (mode == KGQ_MODE_NEAREST) {
                 code = rintf(s);                      /* np.rint, half-even :130 */

@@ -74,7 +74,10 @@ __device__ __forceinline__ void quant_pieces(const float4 (&v)[Geo<G, T>::NF], f
                 for (int e = 0; e < 4; e++) {
                     const float a = __fsub_rn(xs[e], z);
                     const float qv = GUARD ? div_a(dv, a) : div_a_unguarded(dv, a);
-                    const float s = __fmul_rn(qv, Bf);
+                    float s = __fmul_rn(qv, Bf);
+                    // R = inf (an inf in the group, or a range that overflows):
+                    // inf/inf scales to NaN, which numpy casts to code 0
+                    if (GUARD && !(s == s)) s = 0.0f;
                     const float uf = h ? u16_carrier_hi(rw[e], kc) : u16_carrier_lo(rw[e], kc);
                     acc += code_bits<MODE>(s, uf, cw[e] >> 11) << (BITS * e);
                 }
@@ -148,17 +151,17 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
                 for (int qq = 0; qq < Q; qq++) v[i * Q + qq] = ldg_stream(src + 4 * i + qq);
         }
 
-        float mn = fminf(fminf(v[0].x, v[0].y), fminf(v[0].z, v[0].w));
-        float mx = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
+        float mn = fmin_nan(fmin_nan(v[0].x, v[0].y), fmin_nan(v[0].z, v[0].w));
+        float mx = fmax_nan(fmax_nan(v[0].x, v[0].y), fmax_nan(v[0].z, v[0].w));
 #pragma unroll
         for (int f = 1; f < NF; f++) {
-            mn = fminf(mn, fminf(fminf(v[f].x, v[f].y), fminf(v[f].z, v[f].w)));
-            mx = fmaxf(mx, fmaxf(fmaxf(v[f].x, v[f].y), fmaxf(v[f].z, v[f].w)));
+            mn = fmin_nan(mn, fmin_nan(fmin_nan(v[f].x, v[f].y), fmin_nan(v[f].z, v[f].w)));
+            mx = fmax_nan(mx, fmax_nan(fmax_nan(v[f].x, v[f].y), fmax_nan(v[f].z, v[f].w)));
         }
 #pragma unroll
         for (int o = 1; o < T; o <<= 1) {
-            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
         const float z = mn;
         const float r = __fsub_rn(mx, mn);
@@ -245,8 +248,8 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
         const float *row = x + g * (int64_t)G;
         float mn = INFINITY, mx = -INFINITY;
         for (int k = lane; k < G; k += 32) {
-            mn = fminf(mn, row[k]);
-            mx = fmaxf(mx, row[k]);
+            mn = fmin_nan(mn, row[k]);
+            mx = fmax_nan(mx, row[k]);
         }
         mn = warp_min(mn, 32);
         mx = warp_max(mx, 32);
@@ -261,7 +264,7 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
                 uint32_t code = 0;
                 if (r > 0.0f) {
                     float s = __fmul_rn(__fdiv_rn(__fsub_rn(row[k], z), r), Bf);
-                    s = fminf(fmaxf(s, 0.0f), Bf);
+                    s = fminf(fmaxf(s, 0.0f), Bf);     // NaN (inf/inf) -> 0, numpy's cast
                     if (mode == KGQ_ROUND_NEAREST) {
                         code = (uint32_t)rintf(s);
                     } else {

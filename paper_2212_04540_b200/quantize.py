@@ -15,10 +15,12 @@ reference's behaviour where it is defined:
 * ``QuantConfig.group``: quantization group size G.  ``None`` means one group
   per row (the reference, quantize.py:184-186); otherwise groups are the rows
   of the ``(-1, G)`` view of the row-major tensor.
-* ``QuantConfig.rng``: ``"compat"`` draws the reference's numpy
-  Philox4x64-10 stream bit-for-bit (quantize.py:61-102); ``"fast"`` (default)
-  draws Philox4x32-7 16-bit uniforms and is checked bit-exact
-  against the reference through the exported-noise route.
+* ``QuantConfig.rng``: ``"compat"`` (default) draws the reference's numpy
+  Philox4x64-10 stream bit-for-bit (quantize.py:61-102), so the same
+  ``RandomStream(seed)`` gives the same codes as kgact; ``"fast"`` (opt-in,
+  the throughput configuration) draws Philox4x32-7 16-bit uniforms
+   and is checked bit-exact against the reference through the
+  exported-noise route.
 """
 
 import math
@@ -47,7 +49,7 @@ class QuantConfig:
     bits: int = PASSTHROUGH_BITS
     rounding: str = ROUND_STOCHASTIC
     group: int | None = None
-    rng: str = RNG_FAST
+    rng: str = RNG_COMPAT
 
     def __post_init__(self):
         if self.bits not in SUPPORTED_BITS:

@@ -97,7 +97,7 @@ def half_fraction_row(bins: int, dim: int) -> np.ndarray:
 
 def quantizer_verification(bits_list=(1, 2, 4, 8), n_rows: int = 100, dim: int = 64,
                            trials: int = 100000, seed: int = 0, variance_slack: float = 1.05,
-                           tightness_window: float = 0.02, rng: str = "fast") -> dict:
+                           tightness_window: float = 0.02, rng: str = "compat") -> dict:
     """quantize.py:358-412: per bit width, (a) per-element |mean dev| <=
     4 sqrt(R^2 / (4 B^2) / trials), (b) per-row variance <= slack * d * R^2 /
     (4 B^2), (c) at half fractions the per-element variance within the window

@@ -20,6 +20,11 @@ Fixtures:
 * spmm.npz    -- build_adjacency (data.py:230-266) on a tiny synthetic KG,
                  spmm / spmm_t (tensorops.py:37-50), relu + BitMask
                  (tensorops.py:57-92).
+* quant_special.npz -- quantize_tensor / dequantize_tensor on rows holding
+                 IEEE special values (mixed +-0.0, subnormals, +-inf, NaN,
+                 ranges that overflow to inf), G = 64 and 32, all widths and
+                 roundings: pins R/Z bits (sign of zero) and the code of a
+                 NaN-scaled element (numpy casts NaN to code 0).
 * tape.npz    -- Tape forward_all + gathers + BPR (tape.py, model.py) on a
                  toy model: b=32 pass-through and b=2 with fast noise; loss,
                  gradients, packed context codes, ledger counters.
@@ -95,6 +100,75 @@ def quant_cases():
     cases.append(dict(x=x, group=64, bits=2, mode="compat", seed=2**64 - 1, tid=2**63 + 5))
     cases.append(dict(x=x, group=64, bits=2, mode="fast", seed=2**64 - 1, tid=2**63 + 5))
     return cases
+
+
+def special_matrix(seed=0):
+    """64-column rows of IEEE special values (quantize.py:184-186 min/max,
+    :116-125 scaling, :128-132 rounding, :199-210 dequantize)."""
+    rng = np.random.default_rng(seed)
+    f = np.float32
+    rows = []
+    base = lambda: rng.standard_normal(64).astype(f)            # noqa: E731
+    z = np.zeros(64, f)
+    r = z.copy(); r[1::3] = -0.0; rows.append(r)                # mixed +0/-0 (min sign: numpy SIMD order)
+    rows.append(np.full(64, -0.0, f))                           # all -0
+    rows.append(np.zeros(64, f))                                # all +0
+    r = np.abs(base()); r[::4] = -0.0; rows.append(r)           # -0 min with positives (post-ReLU-like)
+    r = np.abs(base()); r[::4] = 0.0; rows.append(r)            # +0 min with positives
+    r = -np.abs(base()); r[::5] = -0.0; rows.append(r)          # -0 max with negatives
+    rows.append((base() * f(1e-39)).astype(f))                  # subnormal values only
+    r = (np.abs(base()) * f(1e-40)).astype(f); r[::3] = 0.0; rows.append(r)   # subnormals + zeros
+    r = base(); r[7] = f(1e-41); rows.append(r)                 # one subnormal among normals
+    r = (base() * f(1e-37)).astype(f); rows.append(r)           # near the normal boundary
+    rows.append(np.full(64, f(1.4e-45)))                        # constant min-subnormal
+    r = base(); r[5] = np.inf; rows.append(r)                   # +inf -> R = inf
+    r = base(); r[9] = -np.inf; rows.append(r)                  # -inf -> Z = -inf
+    r = base(); r[2] = np.inf; r[3] = -np.inf; rows.append(r)   # both -> R = inf
+    rows.append(np.full(64, np.inf, f))                         # all +inf (R = nan)
+    rows.append(np.full(64, -np.inf, f))                        # all -inf
+    r = base(); r[0] = f(3e38); r[1] = f(-3e38); rows.append(r)  # range overflows to inf
+    r = base(); r[63] = f(3.4e38); rows.append(r)               # huge max, finite range
+    r = base(); r[11] = np.nan; rows.append(r)                  # NaN -> R = Z = nan
+    rows.append(np.full(64, f(-7.25)))                          # constant negative
+    for _ in range(4):
+        rows.append(base())                                     # plain rows around them
+    return np.stack(rows).astype(f)
+
+
+SPECIAL_NAN_ROWS = (18,)   # rows whose R/Z are NaN (payload is platform-defined)
+
+
+def special_cases():
+    x = special_matrix()
+    cases = []
+    for g in (64, 32):
+        for bits in (1, 2, 4, 8):
+            for mode in ("compat", "fast", "nearest"):
+                cases.append(dict(x=x, group=g, bits=bits, mode=mode, seed=31 + g, tid=bits))
+    return cases
+
+
+def make_special():
+    import warnings
+    out = {}
+    cases = special_cases()
+    for i, cs in enumerate(cases):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")   # numpy warns on inf-inf, inf/inf and NaN casts
+            q, deq = run_quant_case(cs)
+        p = f"c{i}_"
+        out[p + "x"] = cs["x"]
+        out[p + "meta"] = np.array([cs["group"], cs["bits"],
+                                    {"nearest": 0, "fast": 1, "compat": 2}[cs["mode"]]],
+                                   dtype=np.int64)
+        out[p + "seed_tid"] = np.array([cs["seed"], cs["tid"]], dtype=np.uint64)
+        out[p + "codes"] = q.codes
+        out[p + "ranges"] = q.ranges
+        out[p + "offsets"] = q.offsets
+        out[p + "deq"] = deq
+        out[p + "stored_bytes"] = np.array(kq.stored_bytes(q))
+    out["n_cases"] = np.array(len(cases))
+    return out
 
 
 def run_quant_case(cs):
@@ -271,9 +345,13 @@ def make_c1():
 
 
 def main():
+    if sys.argv[1:] == ["special"]:
+        np.savez_compressed(os.path.join(HERE, "quant_special.npz"), **make_special())
+        return
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **make_c1())
     np.savez_compressed(os.path.join(HERE, "philox.npz"), **make_philox())
     np.savez_compressed(os.path.join(HERE, "quant.npz"), **make_quant())
+    np.savez_compressed(os.path.join(HERE, "quant_special.npz"), **make_special())
     np.savez_compressed(os.path.join(HERE, "spmm.npz"), **make_spmm())
     np.savez_compressed(os.path.join(HERE, "tape.npz"), **make_tape())
     for f in sorted(os.listdir(HERE)):

@@ -65,6 +65,6 @@ def test_status_strings_and_version():
 def test_host_path_without_gpu_raises_not_falls_back():
     import paper_2212_04540_b200 as kgq
     x = torch.randn(64, 64)
-    cfg = kgq.QuantConfig(bits=2)
+    cfg = kgq.QuantConfig(bits=2, rng="fast")
     with pytest.raises(Exception):
         kgq.quantize_tensor(x, cfg, kgq.RandomStream(1), tensor_id=0)

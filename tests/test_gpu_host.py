@@ -69,7 +69,7 @@ def test_host_chunking_is_byte_identical(n_streams):
                                  ctypes.cast(arr, ctypes.c_void_p), n_streams,
                                  torch.cuda.current_stream().cuda_stream)
     assert st == 0
-    cfg = kgq.QuantConfig(bits=bits, group=group)
+    cfg = kgq.QuantConfig(bits=bits, group=group, rng="fast")
     qd = _dev_q(kgq, x, cfg, 9, 4, goff)
     assert _same(codes, qd.codes) and _same(r, qd.ranges) and _same(z, qd.offsets)
     out = torch.empty(rows, cols).pin_memory()
@@ -105,7 +105,7 @@ def test_host_errors():
     L = _lib.load()
     x = torch.randn(8, 64)
     with pytest.raises(ValueError):
-        kgq.quantize_tensor(x, kgq.QuantConfig(bits=2), kgq.RandomStream(1), tensor_id=0,
+        kgq.quantize_tensor(x, kgq.QuantConfig(bits=2, rng="fast"), kgq.RandomStream(1), tensor_id=0,
                             noise=torch.zeros(8 * 64, dtype=torch.float64, device="cuda"))
     assert L.kgq_quantize_host_f32(x.data_ptr(), 8, 64, 2, _lib.ROUND_SR_NOISE, 0, 0, 0, None, None, None,
                                    None, 0, None, 0, None) == _lib.KGQ_ERR_INVALID_ARG
@@ -115,7 +115,7 @@ def test_host_errors():
         == _lib.KGQ_ERR_INVALID_ARG
     # empty input is a no-op
     e = torch.empty(0, 64)
-    q = kgq.quantize_tensor(e, kgq.QuantConfig(bits=2), kgq.RandomStream(1), tensor_id=0)
+    q = kgq.quantize_tensor(e, kgq.QuantConfig(bits=2, rng="fast"), kgq.RandomStream(1), tensor_id=0)
     assert q.codes.shape[0] == 0 and kgq.dequantize_tensor(q).shape == (0, 64)
 
 

@@ -5,6 +5,8 @@ Bit-exact against (a) golden fixtures produced by the reference itself and
 Full-size (BASELINE configs[1]) behaviour is checked through size-independent
 properties.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -70,7 +72,7 @@ def test_exported_noise_route(case):
     assert np.array_equal(u16.cpu().numpy(),
                           orc.fast_noise_u16(case["seed"], case["tid"], x.shape[0], x.shape[1]))
     noise = u16.to(torch.float64) / 65536.0
-    q = kgq.quantize_tensor(_to_dev(x), kgq.QuantConfig(bits=case["bits"]), noise=noise)
+    q = kgq.quantize_tensor(_to_dev(x), kgq.QuantConfig(bits=case["bits"], rng="fast"), noise=noise)
     _assert_q_equal(q, case["codes"], case["ranges"], case["offsets"])
 
 
@@ -160,32 +162,32 @@ def test_pack_unpack_known_answers_and_errors():
 def test_errors_match_reference_classes():
     kgq = _kgq()
     with pytest.raises(ValueError):
-        kgq.QuantConfig(bits=3)
+        kgq.QuantConfig(bits=3, rng="fast")
     with pytest.raises(ValueError):
-        kgq.QuantConfig(rounding="up")
+        kgq.QuantConfig(rounding="up", rng="fast")
     x = torch.zeros((4, 8), device="cuda")
     with pytest.raises(ValueError):   # SR without a stream, quantize.py:189-190
-        kgq.quantize_tensor(x, kgq.QuantConfig(bits=2))
-    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=32))
+        kgq.quantize_tensor(x, kgq.QuantConfig(bits=2, rng="fast"))
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=32, rng="fast"))
     assert kgq.dequantize_tensor(q) is x      # pass-through is the raw tensor
     with pytest.raises(ValueError):
-        kgq.quantize_tensor(torch.zeros((3, 8), device="cuda"), kgq.QuantConfig(bits=2, group=16),
+        kgq.quantize_tensor(torch.zeros((3, 8), device="cuda"), kgq.QuantConfig(bits=2, group=16, rng="fast"),
                             kgq.RandomStream(0))
     # a host tensor takes the host-buffer path (computed on the GPU, context in host memory)
-    qh = kgq.quantize_tensor(torch.zeros((3, 8)), kgq.QuantConfig(bits=2), kgq.RandomStream(0), tensor_id=0)
+    qh = kgq.quantize_tensor(torch.zeros((3, 8)), kgq.QuantConfig(bits=2, rng="fast"), kgq.RandomStream(0), tensor_id=0)
     assert qh.codes.device.type == "cpu"
     with pytest.raises(TypeError):
-        kgq.quantize_tensor(torch.zeros((3, 8), dtype=torch.float64, device="cuda"), kgq.QuantConfig(bits=2),
+        kgq.quantize_tensor(torch.zeros((3, 8), dtype=torch.float64, device="cuda"), kgq.QuantConfig(bits=2, rng="fast"),
                             kgq.RandomStream(0))
 
 
 def test_empty_and_tiny_inputs():
     kgq = _kgq()
     st = kgq.RandomStream(1)
-    q = kgq.quantize_tensor(torch.zeros((0, 64), device="cuda"), kgq.QuantConfig(bits=2), st)
+    q = kgq.quantize_tensor(torch.zeros((0, 64), device="cuda"), kgq.QuantConfig(bits=2, rng="fast"), st)
     assert q.codes.shape == (0, 16) and kgq.dequantize_tensor(q).shape == (0, 64)
     x = torch.tensor([[4.2, 4.2, 4.2]], device="cuda")
-    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=2), st)
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=2, rng="fast"), st)
     assert q.codes.cpu().tolist() == [[0]] and float(q.ranges[0]) == 0.0
     assert torch.equal(kgq.dequantize_tensor(q), x)
 
@@ -199,7 +201,7 @@ def test_full_size_properties(bits):
     rows, cols = (64 << 20, 128) if free > 100e9 else (16 << 20, 128)
     g = torch.Generator(device="cuda").manual_seed(bits)
     x = torch.randn((rows, cols), device="cuda", generator=g)
-    cfg = kgq.QuantConfig(bits=bits, group=64)
+    cfg = kgq.QuantConfig(bits=bits, group=64, rng="fast")
     st = kgq.RandomStream(11)
     q = kgq.quantize_tensor(x, cfg, st, tensor_id=3)
     q2 = kgq.quantize_tensor(x, cfg, st, tensor_id=3)
@@ -229,3 +231,84 @@ def test_full_size_properties(bits):
     # unbiased SR: mean normalized error ~ 0 (sigma <= 1/(2B sqrt(n)))
     n = rows * cols
     assert abs(err_sum / n) < 6.0 / (2 * B * np.sqrt(n))
+
+
+@pytest.mark.parametrize("misalign", [False, True], ids=["fast", "generic"])
+@pytest.mark.parametrize("case", list(golden_io.special_cases()), ids=lambda c: f"s{c['idx']}")
+def test_special_values_match_reference_golden(case, misalign):
+    """Rows of +-0, subnormals, +-inf, NaN and overflowing ranges, run through
+    the reference (quant_special.npz): codes bit-exact; R, Z and the
+    dequantized fp32 bit-exact up to NaN payloads and the sign of a zero
+    extreme in groups that hold both +0 and -0 (numpy's SIMD reduction order
+    picks that sign; golden_io.mixed_zero_groups)."""
+    kgq = _kgq()
+    g = case["group"]
+    x = case["x"].reshape(-1, g)
+    q = kgq.quantize_tensor(_to_dev(x, misalign), _cfg(kgq, g, case["bits"], case["mode"], True),
+                            kgq.RandomStream(case["seed"]), tensor_id=case["tid"])
+    free = golden_io.mixed_zero_groups(x, g)
+    assert np.array_equal(q.codes.cpu().numpy(), case["codes"])
+    assert golden_io.same_bits(q.ranges.cpu().numpy(), case["ranges"], free)
+    assert golden_io.same_bits(q.offsets.cpu().numpy(), case["offsets"], free)
+    deq = kgq.dequantize_tensor(q).cpu().numpy()
+    assert golden_io.same_bits(deq, case["deq"].reshape(deq.shape), free)
+
+
+def test_default_stream_is_the_reference_stream():
+    """QuantConfig() draws kgact's numpy Philox4x64-10 stream: the same
+    RandomStream(seed) gives the reference's codes with no extra argument."""
+    kgq = _kgq()
+    assert kgq.QuantConfig(bits=2).rng == "compat"
+    n = 0
+    for case in golden_io.quant_cases():
+        if case["mode"] != 2 or case["group"] != case["x"].shape[1]:
+            continue
+        q = kgq.quantize_tensor(_to_dev(case["x"]), kgq.QuantConfig(bits=case["bits"]),
+                                kgq.RandomStream(case["seed"]), tensor_id=case["tid"])
+        _assert_q_equal(q, case["codes"], case["ranges"], case["offsets"])
+        n += 1
+    assert n >= 20
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs[1] whole-tensor parity: every code, R, Z and dequantized
+# value of 1M x 64 and 4M x 128 fp32 tensors against the threaded C oracle.
+# ---------------------------------------------------------------------------
+_WHOLE = {}
+
+
+def _whole_input(rows, cols):
+    """configs[1] input: N(0,1) from default_rng(0), every
+    97th row constant (R = 0), every 89th row scaled by 1e-30."""
+    key = (rows, cols)
+    if key not in _WHOLE:
+        _WHOLE.clear()
+        x = np.random.default_rng(0).standard_normal((rows, cols), dtype=np.float32)
+        x[::97] = x[::97, :1]
+        x[::89] *= np.float32(1e-30)
+        _WHOLE[key] = (x, torch.from_numpy(x).cuda())
+    return _WHOLE[key]
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2], ids=["nearest", "fast", "compat"])
+@pytest.mark.parametrize("group", [64, 256])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("rows,cols", [(1 << 20, 64), (4 << 20, 128)], ids=["1Mx64", "4Mx128"])
+def test_configs1_whole_tensor_bit_exact(rows, cols, bits, group, mode):
+    kgq = _kgq()
+    x, xt = _whole_input(rows, cols)
+    cfg = kgq.QuantConfig(bits=bits, rounding="nearest" if mode == 0 else "stochastic", group=group,
+                          rng=RNG_OF_MODE[mode])
+    seed, tid = 1, 0                                   # SURVEY.md 8(d): seed=1, tensor_id=0
+    q = kgq.quantize_tensor(xt, cfg, kgq.RandomStream(seed), tensor_id=tid)
+    threads = os.cpu_count() or 8
+    codes, ranges, offsets = orc.quantize(x.reshape(-1, group), group, bits, mode, seed, tid,
+                                          threads=threads)
+    gc = q.codes.cpu().numpy()
+    mism = int((gc != codes).any(1).sum())
+    assert mism == 0, f"{mism} of {codes.shape[0]} groups differ"
+    _assert_q_equal(q, codes, ranges, offsets)
+    del gc
+    deq = kgq.dequantize_tensor(q).cpu().numpy().reshape(-1, group)
+    ref = orc.dequantize(codes, ranges, offsets, group, bits, threads=threads)
+    assert np.array_equal(deq.view(np.uint32), ref.view(np.uint32))

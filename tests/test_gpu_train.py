@@ -47,7 +47,7 @@ def _params(kgq, z, d, layers):
 def test_tape_b32_matches_reference(d, layers, fused):
     kgq, z, adj = _tiny()
     from paper_2212_04540_b200.tape import Tape
-    tape = Tape(kgq.QuantConfig(bits=32), kgq.RandomStream(21))
+    tape = Tape(kgq.QuantConfig(bits=32, rng="fast"), kgq.RandomStream(21))
     _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, fused)
     pre = f"d{d}_b32_"
     assert tape.peak_context_bytes == int(z[pre + "peak_ctx"])
@@ -59,17 +59,24 @@ def test_tape_b32_matches_reference(d, layers, fused):
         np.testing.assert_allclose(g.cpu().numpy(), z[pre + "grad_" + name], rtol=2e-4, atol=2e-7)
 
 
+# Observed on B200 (round 2, bits 2/4/8 x fused/split): every code of every
+# context identical to the reference's; gradients within 6.4e-7 of max|grad|.
+MAX_CODE_MISMATCH = 0.0
+MAX_GRAD_REL = 2e-6
+
+
 @pytest.mark.parametrize("bits", [2, 4, 8])
 @pytest.mark.parametrize("fused", [True, False])
 def test_tape_quantized_matches_reference(bits, fused):
-    """Same noise (fast stream == reference fed the exported noise): layer-0
-    context codes are bit-exact; deeper contexts see H through an fp32 GEMM
-    whose summation order differs from OpenBLAS, so a few codes may flip;
-    gradients agree within a tolerance set by one code step."""
+    """Same noise (fast stream == reference fed the exported noise): the codes
+    of all six contexts (3 layers + u/p/n) are bit-exact with the reference's
+    (deeper layers see H through an fp32 GEMM whose summation order differs
+    from OpenBLAS, yet no code flips at this size); gradients agree to
+    fp32-reordering level (max 6.4e-7 of max|grad| observed, bound 2e-6)."""
     kgq, z, adj = _tiny()
     from paper_2212_04540_b200.tape import Tape
     d, layers = 64, 3
-    tape = Tape(kgq.QuantConfig(bits=bits), kgq.RandomStream(21))
+    tape = Tape(kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(21))
     _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, fused)
     pre = f"d{d}_b{bits}_"
     assert tape.peak_context_bytes == int(z[pre + "peak_ctx"])
@@ -79,20 +86,27 @@ def test_tape_quantized_matches_reference(bits, fused):
     qs += [bpr["qu"], bpr["qp"], bpr["qn"]]
     assert np.array_equal(qs[0].codes.cpu().numpy(), z[pre + "q0_codes"])
     assert np.array_equal(qs[0].ranges.cpu().numpy(), z[pre + "q0_ranges"])
+    mism, gerr = [], {}
     for k, q in enumerate(qs):
         ours = q.codes.cpu().numpy()
         ref = z[pre + f"q{k}_codes"]
         assert ours.shape == ref.shape
-        assert np.mean(ours != ref) < 0.02, k
+        # packed bytes -> per-element code mismatch rate
+        ou = kgq.unpack_codes(q.codes, bits, q.cols).cpu().numpy()
+        ru = kgq.unpack_codes(torch.from_numpy(ref).cuda(), bits, q.cols).cpu().numpy()
+        mism.append(float(np.mean(ou != ru)))
         np.testing.assert_allclose(q.ranges.cpu().numpy(), z[pre + f"q{k}_ranges"], rtol=1e-4, atol=1e-6)
     grads = tape.backward()
     assert tape.current_context_bytes == 0
     assert tape.loss() == pytest.approx(float(z[pre + "loss"]), rel=1e-5)
     for name, g in grads.items():
         ref = z[pre + "grad_" + name]
-        scale = np.abs(ref).max()
-        err = np.abs(g.cpu().numpy() - ref).max()
-        assert err <= 0.05 * scale + 1e-7, (name, err, scale)
+        gerr[name] = float(np.abs(g.cpu().numpy() - ref).max() / np.abs(ref).max())
+    print(f"TAPE b{bits} fused={fused} code_mismatch={[f'{m:.2e}' for m in mism]} "
+          f"grad_rel={ {k: float(f'{v:.2e}') for k, v in gerr.items()} }")
+    # bounds: the observed maxima over bits 2/4/8 x fused/split, ~3x slack on grads
+    assert max(mism) <= MAX_CODE_MISMATCH, mism
+    assert max(gerr.values()) <= MAX_GRAD_REL, gerr
 
 
 def _hub_graph(n, seed):
@@ -192,7 +206,7 @@ def test_dequant_gemm_matches_dequantize_then_matmul():
             x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
             g = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
             for bits in (1, 2, 4, 8):
-                q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(2), tensor_id=1)
+                q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(2), tensor_id=1)
                 hh = kgq.dequantize_tensor(q).double()
                 ref = (hh.t() @ g.double()).cpu().numpy()
                 out = F.dequant_gemm_tn(q, g).double().cpu().numpy()
@@ -209,7 +223,7 @@ def test_autograd_kgnn_equals_tape():
     from paper_2212_04540_b200.tape import Tape
     d, layers = 64, 3
     for bits in (32, 2):
-        cfg = kgq.QuantConfig(bits=bits)
+        cfg = kgq.QuantConfig(bits=bits, rng="fast")
         tape = Tape(cfg, kgq.RandomStream(21))
         _record(kgq, tape, _params(kgq, z, d, layers), adj, z, layers, d, True)
         tg = tape.backward()
@@ -245,7 +259,7 @@ def test_training_c1_matches_reference_run(bits, graphs):
     ds = D.KgDataset(int(z["num_users"]), int(z["num_items"]), int(z["num_entities"]), z["train"],
                      z["val"], z["test"], z["triples"], int(z["num_relations"]))
     epochs = int(z["run_epochs"])
-    q = kgq.QuantConfig(bits=bits)
+    q = kgq.QuantConfig(bits=bits, rng="fast")
     _, rep = train_run(ds, ModelConfig(layers=2, dim=64, quant=q), TrainConfig(epochs=epochs, seed=0, quant=q),
                        graphs=graphs)
     pre = f"run_b{bits}_"
@@ -268,7 +282,7 @@ def test_row_block_fused_layer_is_bit_identical_to_full():
     rng = np.random.default_rng(3)
     e = torch.from_numpy(rng.standard_normal((5000, 64), dtype=np.float32)).cuda()
     th = torch.from_numpy((rng.standard_normal((64, 64)) / 8).astype(np.float32)).cuda()
-    cfg = kgq.QuantConfig(bits=2)
+    cfg = kgq.QuantConfig(bits=2, rng="fast")
     full = F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(1), 4)
     for w in (2, 4, 8):
         cuts = D.partition_rows(a.indptr, w)
@@ -287,7 +301,7 @@ def test_partitioned_step_gpu_world1_matches_tape():
     from paper_2212_04540_b200.parallel import GpuOps, RowPartition, SoloComm, partitioned_step
     from paper_2212_04540_b200.tape import Tape
     n = int(z["n"])
-    cfg = kgq.QuantConfig(bits=2)
+    cfg = kgq.QuantConfig(bits=2, rng="fast")
     p = _params(kgq, z, 64, 3)
     tape = Tape(cfg, kgq.RandomStream(21))
     _record(kgq, tape, p, adj, z, 3, 64, True)
@@ -335,7 +349,7 @@ def test_cuda_graph_epoch_equals_eager_epoch():
     from paper_2212_04540_b200.train import AdamState, TrainConfig, train_epoch
     ds = D.synth_kg(D.SynthShape(600, 400, 1500, relations=5, interactions_per_user=20.0), seed=3)
     adj = D.build_adjacency(ds)
-    q = kgq.QuantConfig(bits=2)
+    q = kgq.QuantConfig(bits=2, rng="fast")
     mcfg = ModelConfig(layers=3, dim=64, quant=q)
     cfg = TrainConfig(batch_size=256, quant=q)
     outs = []
@@ -365,7 +379,7 @@ def test_fused_layer_backward_matches_fp64(d, bits, terms):
     rng = np.random.default_rng(d * 10 + bits)
     rows = 10007
     x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
-    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(1), tensor_id=2)
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(1), tensor_id=2)
     j = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
     _, mask = kgq.relu(j)
     gr = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
@@ -513,7 +527,7 @@ rng = np.random.default_rng(5)
 for bits in (1, 2, 4, 8):
     rows, d = 10007, 64
     x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
-    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits), kgq.RandomStream(1), tensor_id=2)
+    q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(1), tensor_id=2)
     j = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
     _, mask = kgq.relu(j)
     gr = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
@@ -569,7 +583,7 @@ def test_passthrough_layer_fused_forward_and_backward(d):
     e_np = rng.standard_normal((n, d), dtype=np.float32)
     e = torch.from_numpy(e_np).cuda()
     th = torch.from_numpy((rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
-    cfg = kgq.QuantConfig(bits=32)
+    cfg = kgq.QuantConfig(bits=32, rng="fast")
     st = kgq.RandomStream(3)
     e_next, mask, q, h = F.graph_conv_forward(A, e, th, cfg, st, want_h=True)
     assert st._next_tensor_id == 0 and q.bits == 32 and q.raw is not None
@@ -600,7 +614,7 @@ def test_partitioned_step_graph_equals_eager():
     ip, ix, vv = D.adjacency_arrays(ds)
     part = RowPartition.build(ip, 1, 0)
     a_local = GpuOps.local_adjacency(ip, ix, vv, 0, ds.num_nodes, ds.num_nodes, "cuda")
-    q = kgq.QuantConfig(bits=2)
+    q = kgq.QuantConfig(bits=2, rng="fast")
     mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), TrainConfig(quant=q, batch_size=256)
     trip = torch.from_numpy(D.sample_negatives(ds, np.random.default_rng(0))).cuda().long()
     U = ds.num_users
@@ -662,9 +676,9 @@ def test_acceptance_criterion_4_memory_accounting():
     from paper_2212_04540_b200.model import ModelConfig
     from paper_2212_04540_b200.train import TrainConfig, bench_memory
     st = kgq.RandomStream(0)
-    q = kgq.quantize_tensor(torch.zeros((1000, 64), device="cuda"), kgq.QuantConfig(bits=2), st)
+    q = kgq.quantize_tensor(torch.zeros((1000, 64), device="cuda"), kgq.QuantConfig(bits=2, rng="fast"), st)
     assert kgq.stored_bytes(q) == 24000
-    q1 = kgq.quantize_tensor(torch.zeros((7, 5), device="cuda"), kgq.QuantConfig(bits=1), st)
+    q1 = kgq.quantize_tensor(torch.zeros((7, 5), device="cuda"), kgq.QuantConfig(bits=1, rng="fast"), st)
     assert kgq.stored_bytes(q1) == 7 * ((5 + 7) // 8 + 8)
     ds = D.reference_dataset("default")
     rows = bench_memory(ds, ModelConfig(layers=3, dim=64), TrainConfig(batch_size=1024, epochs=1, seed=0))
@@ -689,7 +703,7 @@ def test_acceptance_criterion_5_accuracy_parity():
     for bits in (32, 8, 2):
         rec = []
         for seed in range(5):
-            q = kgq.QuantConfig(bits=bits)
+            q = kgq.QuantConfig(bits=bits, rng="fast")
             cfg = TrainConfig(seed=seed, quant=q, batch_size=256, epochs=20, lr=1e-3, l2=1e-5)
             _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q), cfg, adjacency=adj, graphs=True)
             rec.append(rep["metrics"]["recall_at_20"])
@@ -702,7 +716,7 @@ def _toy_step_grads(ds, adj, params, mcfg, bits, stream, batch):
     import paper_2212_04540_b200 as kgq
     from paper_2212_04540_b200.model import forward_all
     from paper_2212_04540_b200.tape import Tape
-    tape = Tape(kgq.QuantConfig(bits=bits), stream)
+    tape = Tape(kgq.QuantConfig(bits=bits, rng="fast"), stream)
     readout = forward_all(tape, params, adj, mcfg)
     u = tape.record_gather(readout, batch[:, 0])
     p = tape.record_gather(readout, ds.num_users + batch[:, 1])
@@ -791,7 +805,7 @@ def test_acceptance_criterion_8_determinism_and_lifecycle():
     ds = D.reference_dataset("default")
     reports, retained = [], []
     for _ in range(2):
-        cfg = TrainConfig(batch_size=256, epochs=2, seed=1, quant=kgq.QuantConfig(bits=2))
+        cfg = TrainConfig(batch_size=256, epochs=2, seed=1, quant=kgq.QuantConfig(bits=2, rng="fast"))
         _, rep = train_run(ds, ModelConfig(layers=3, dim=64), cfg, graphs=True)
         retained.append(rep["memory"]["retained_context_bytes"])
         rep = dict(rep)
@@ -830,3 +844,76 @@ def test_lastfm_one_epoch_matches_reference_run(bits, rng_mode):
     assert rep["loss_curve"][0] == pytest.approx(ref["loss_curve"][0], rel=1e-2)
     assert abs(rep["metrics"]["recall_at_20"] - ref["recall_at_20"]) <= 0.005
     assert abs(rep["metrics"]["ndcg_at_20"] - ref["ndcg_at_20"]) <= 0.005
+
+
+def _ulp_rel(a, b):
+    """max |a - b| over max |b| (0 when both are 0)."""
+    s = float(np.abs(b).max())
+    return float(np.abs(a.astype(np.float64) - b.astype(np.float64)).max()) / s if s else 0.0
+
+
+@pytest.mark.parametrize("bits", [32, 2])
+def test_lastfm_step_level_pin(bits):
+    """BASELINE configs[2] step by step against the reference's own loop
+    (tests/golden/lastfm_steps.npz, datasets/record_reference_steps.py): same
+    init, batches and (bits 2) the reference's noise stream.  Step 1's loss
+    and gradients agree to fp32 reordering level; the parameters then drift
+    only as far as the recorded bounds allow, so the epoch-level gap of
+    test_lastfm_one_epoch_matches_reference_run starts as last-bit noise, not
+    a logic difference."""
+    import os
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import train as T
+    from paper_2212_04540_b200.model import ModelConfig, init_params
+    path = os.path.join(golden_io.GOLDEN, "lastfm_steps.npz")
+    if not os.path.exists(path):
+        pytest.skip("lastfm_steps.npz not recorded")
+    z = np.load(path)
+    pre = f"b{bits}_"
+    n_steps = int(z["n_steps"])
+    rows = z[pre + "rows"]
+    ds = D.reference_dataset("lastfm")
+    q = kgq.QuantConfig(bits=bits)                         # default stream = the reference's
+    mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), T.TrainConfig(epochs=1, quant=q)
+    adj = D.build_adjacency(ds, "cuda")
+    rng = np.random.default_rng(cfg.seed)
+    stream = kgq.RandomStream(cfg.seed)
+    params = init_params(ds.num_nodes, mcfg, cfg.seed, "cuda")
+    state = T.AdamState(params.as_dict())
+    snaps, grad1 = {}, {}
+    orig = T.adam_step
+
+    def rec(param_dict, grads, st, lr):
+        if st.step == 0:
+            for k, g in grads.items():
+                grad1[k] = (g[torch.from_numpy(rows).cuda()] if k == "E0" else g).cpu().numpy()
+        orig(param_dict, grads, st, lr)
+        if st.step in tuple(int(c) for c in z["checkpoints"]):
+            snaps[st.step] = {k: p.cpu().numpy().copy() for k, p in param_dict.items()}
+
+    T.adam_step = rec
+    try:
+        stats = T.train_epoch(ds, adj, params, mcfg, cfg, state, stream, rng, max_steps=n_steps)
+    finally:
+        T.adam_step = orig
+    losses = np.array(stats["losses"])
+    ref_losses = z[pre + "losses"]
+    assert len(losses) == len(ref_losses) == n_steps
+    loss_gap = np.abs(losses - ref_losses)
+    g_rel = {k: _ulp_rel(v, z[pre + f"grad1_{k}"]) for k, v in grad1.items()}
+    report = {"loss_gap_step1": float(loss_gap[0]), "loss_gap_step10": float(loss_gap[9]),
+              "loss_gap_max": float(loss_gap.max()), "grad1_rel": max(g_rel.values())}
+    for c in (int(c) for c in z["checkpoints"]):
+        th = max(_ulp_rel(snaps[c][f"theta{i}"], z[pre + f"s{c}_theta{i}"]) for i in range(3))
+        e = snaps[c]["E0"]
+        er = e[rows] - z[pre + f"s{c}_E0_rows"]
+        report[f"s{c}_theta_rel"] = th
+        report[f"s{c}_E0rows_maxabs"] = float(np.abs(er).max())
+        report[f"s{c}_E0rows_frac_gt_1e-6"] = float(np.mean(np.abs(er) > 1e-6))
+        report[f"s{c}_E0_sum_gap"] = float(abs(e.astype(np.float64).sum() - z[pre + f"s{c}_E0_sum"][0]))
+    print(f"PIN b{bits}", {k: float(f"{v:.3g}") for k, v in report.items()})
+    # step 1: the same batch and init; fp32 reordering only
+    assert report["loss_gap_step1"] <= 1e-6
+    assert report["grad1_rel"] <= 1e-4
+    assert report["loss_gap_max"] <= 5e-3

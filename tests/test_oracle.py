@@ -162,3 +162,17 @@ def test_oracle_evaluate_matches_reference(name):
 def test_oracle_topk_stable_order():
     s = np.array([[1.0, 3.0, 3.0, -np.inf, 0.0, -0.0, np.nan, 3.0]])
     assert orc.topk_stable(s, 8)[0].tolist() == [1, 2, 7, 0, 4, 5, 3, 6]
+
+
+@pytest.mark.parametrize("case", list(golden_io.special_cases()), ids=lambda c: f"s{c['idx']}")
+def test_oracle_special_values_match_reference(case):
+    """+-0, subnormals, +-inf, NaN (quant_special.npz, written by the reference)."""
+    g = case["group"]
+    codes, ranges, offsets = orc.quantize(case["x"].reshape(-1, g), g, case["bits"], case["mode"],
+                                          case["seed"], case["tid"])
+    free = golden_io.mixed_zero_groups(case["x"], g)
+    assert np.array_equal(codes, case["codes"])
+    assert golden_io.same_bits(ranges, case["ranges"], free)
+    assert golden_io.same_bits(offsets, case["offsets"], free)
+    deq = orc.dequantize(codes, ranges, offsets, g, case["bits"])
+    assert golden_io.same_bits(deq, case["deq"].reshape(deq.shape), free)

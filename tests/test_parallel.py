@@ -136,7 +136,7 @@ def _run(world, rank, comm, layout="concat"):
         from paper_2212_04540_b200.parallel import HaloPlan
         halo = HaloPlan.build(part, torch.from_numpy(ix.astype(np.int64)), comm)
         ix = halo.remap(torch.from_numpy(ix.astype(np.int64))).numpy()
-    cfg = QuantConfig(bits=2)
+    cfg = QuantConfig(bits=2, rng="fast")
     loss, de0, dth = partitioned_step(part, (ip, ix, vv), e0[part.lo:part.hi], thetas, users, pos, neg,
                                       1e-5, cfg, RandomStream(21), comm, ops=OracleOps, layout=layout,
                                       halo=halo)
@@ -179,13 +179,14 @@ def test_partitioned_step_world2_gloo_matches_world1(layout):
 
 def test_partitioned_world1_matches_reference_tape():
     """W=1 partitioned step vs the reference Tape fed the same (fast) noise
-    (golden tape.npz, b=2): same loss, gradients within one code step."""
+    (golden tape.npz, b=2): same loss, gradients equal (0 difference observed;
+    bound 1e-6 of max|grad| for BLAS summation-order differences across hosts)."""
     z, n, e0, thetas, (users, pos, neg) = _problem()
     part, loss, de0, dth = _run(1, 0, SoloComm())
     assert float(loss) == pytest.approx(float(z["d64_b2_loss"]), rel=1e-5)
     for name, g in [("E0", de0)] + [(f"theta{i}", t) for i, t in enumerate(dth)]:
         ref = z["d64_b2_grad_" + name]
-        assert np.abs(g.numpy() - ref).max() <= 0.05 * np.abs(ref).max() + 1e-7, name
+        assert np.abs(g.numpy() - ref).max() <= 1e-6 * np.abs(ref).max(), name
 
 
 def test_padded_cols_layout():

@@ -7,7 +7,7 @@ from paper_2212_04540_b200.train import AdamState, TrainConfig, evaluate, train_
 for shape in ("amazon", "lastfm"):
     ds = D.reference_dataset(shape); adj = D.build_adjacency(ds)
     for fused in (True, False):
-        q = kgq.QuantConfig(bits=32)
+        q = kgq.QuantConfig(bits=32, rng="fast")
         mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), TrainConfig(quant=q)
         params = init_params(ds.num_nodes, mcfg, 0); state = AdamState(params.as_dict())
         st = train_epoch(ds, adj, params, mcfg, cfg, state, kgq.RandomStream(0), np.random.default_rng(0), fused=fused, graphs=True)

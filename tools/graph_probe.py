@@ -8,7 +8,7 @@ from paper_2212_04540_b200.model import ModelConfig, init_params
 
 ds = D.synth_kg(D.SHAPES["amazon"], seed=0)
 adj = D.build_adjacency(ds)
-q = kgq.QuantConfig(bits=2)
+q = kgq.QuantConfig(bits=2, rng="fast")
 mcfg = ModelConfig(layers=3, dim=64, quant=q)
 cfg = T.TrainConfig(quant=q)
 params = init_params(ds.num_nodes, mcfg, 0)

@@ -6,7 +6,7 @@ import paper_2212_04540_b200 as kgq
 
 rows = 8 << 20
 x = torch.randn(rows, 128).pin_memory()
-cfg = kgq.QuantConfig(bits=2, group=64)
+cfg = kgq.QuantConfig(bits=2, group=64, rng="fast")
 st = kgq.RandomStream(1)
 def t(f, n=3):
     f(); torch.cuda.synchronize()

@@ -17,7 +17,7 @@ for rows in (1 << 20, 4 << 20, 16 << 20, 64 << 20):
         x = torch.randn(rows, cols, device="cuda")
         for bits in (2, 4, 8):
             for group in (64, 256):
-                cfg = kgq.QuantConfig(bits=bits, group=group)
+                cfg = kgq.QuantConfig(bits=bits, group=group, rng="fast")
                 st = kgq.RandomStream(1)
                 q = kgq.quantize_tensor(x, cfg, st, tensor_id=0)
                 out = kgq.dequantize_tensor(q)

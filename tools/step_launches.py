@@ -11,7 +11,7 @@ from paper_2212_04540_b200.train import TrainConfig, AdamState, train_epoch
 
 ds = D.reference_dataset(sys.argv[1] if len(sys.argv) > 1 else "amazon")
 adj = D.build_adjacency(ds)
-q = kgq.QuantConfig(bits=2)
+q = kgq.QuantConfig(bits=2, rng="fast")
 mcfg, cfg = ModelConfig(layers=3, dim=64, quant=q), TrainConfig(quant=q)
 params = init_params(ds.num_nodes, mcfg, 0)
 state = AdamState(params.as_dict())

@@ -15,7 +15,7 @@ ds = D.reference_dataset(shape) if shape in D.REFERENCE_DATASETS else D.synth_kg
 t1 = time.time()
 adj = D.build_adjacency(ds)
 print(f"gen {t1-t0:.1f}s adj {time.time()-t1:.1f}s nodes {ds.num_nodes} nnz {adj.nnz} train {len(ds.train)} triples {len(ds.triples)}", flush=True)
-q = kgq.QuantConfig(bits=bits)
+q = kgq.QuantConfig(bits=bits, rng="fast")
 mcfg = ModelConfig(layers=3, dim=64, quant=q)
 cfg = TrainConfig(quant=q)
 params = init_params(ds.num_nodes, mcfg, 0)
