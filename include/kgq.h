@@ -157,17 +157,33 @@ KGQ_API int kgq_dequant_gemm_tn_f32(const uint8_t *codes, const float *ranges, c
 /* Adam step, train.py:42-59, fused into one pass with the reference's numpy
  * float32 op order (scalars rounded to float32, true divisions, separate
  * roundings) -- bit-identical to the numpy update.  step >= 1 is the
- * post-increment step count t. */
+ * post-increment step count t.  status (nullable, device int64[4] of
+ * kgq_check_finite_f32): when status[0] != 0 the update is skipped, so a
+ * failed step leaves parameters and moments as they were (train.py:91-93
+ * raises before adam_step). */
 KGQ_API int kgq_adam_step_f32(float *param, const float *grad, float *m, float *v, int64_t n,
                       double lr, double beta1, double beta2, double eps, int64_t step,
-                      void *stream);
+                      const int64_t *status, void *stream);
 
 /* Same update for CUDA-graph replay: i = *step_ptr (device int64) indexes a
  * host-built float32 table c12[2i], c12[2i+1] = 1 - beta1^t, 1 - beta2^t of
  * the steps t the replays run.  n % 4 == 0 and 16-byte alignment. */
 KGQ_API int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, float *v, int64_t n,
                           double lr, double beta1, double beta2, double eps,
-                          const float *c12, const int64_t *step_ptr, void *stream);
+                          const float *c12, const int64_t *step_ptr, const int64_t *status,
+                          void *stream);
+
+/* Per-step health check replacing the reference's host checks
+ * (train.py:91-92 non-finite loss -> FloatingPointError; tape.py:256-264
+ * non-finite gradient -> ValueError) without a host sync.  tensors[k] (device
+ * fp32, sizes[k] elements, k < count <= 8; host arrays read at launch) are
+ * scanned; if any holds inf/NaN and status[0] == 0, status[0] = code0 + the
+ * first failing k and status[1] = step_host + (*step_dev if step_dev).  The
+ * latch is sticky; status[2..3] are scratch the launch resets itself
+ * (CUDA-graph replayable).  status: device int64[4], zeroed by the caller. */
+KGQ_API int kgq_check_finite_f32(const float *const *tensors, const int64_t *sizes, int32_t count,
+                         int32_t code0, const int64_t *step_dev, int64_t step_host,
+                         int64_t *status, void *stream);
 
 /* out[rows][d] = a[rows][d] . theta (transpose_theta = 0) or . theta^T (1) on
  * the tcgen05 tensor cores (kind::tf32, 3xTF32 split: fp32-level accuracy),

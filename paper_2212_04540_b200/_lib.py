@@ -50,9 +50,10 @@ SIGNATURES = {
     "kgq_dequant_gemm_workspace_bytes": (_SZ, [_I64, _I32]),
     "kgq_dequant_gemm_tn_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _I32, _P]),
     "kgq_adam_step_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.c_double, ctypes.c_double,
-                                         ctypes.c_double, ctypes.c_double, _I64, _P]),
+                                         ctypes.c_double, ctypes.c_double, _I64, _P, _P]),
     "kgq_adam_step_dev_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.c_double, ctypes.c_double,
-                                             ctypes.c_double, ctypes.c_double, _P, _P, _P]),
+                                             ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
+    "kgq_check_finite_f32": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _I64, _P, _P]),
     "kgq_rowmm_f32": (ctypes.c_int, [_P, _I64, _I32, _P, _I32, _P, _P]),
     "kgq_layer_backward_workspace_bytes": (_SZ, [_I64, _I32]),
     "kgq_layer_backward_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _P,

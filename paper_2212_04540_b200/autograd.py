@@ -19,7 +19,7 @@ backward has run.
 import torch
 
 from . import functional as F
-from .quantize import (QuantConfig, RandomStream, dequantize_tensor, fp32_equivalent_bytes,
+from .quantize import (row_group_offset, QuantConfig, RandomStream, dequantize_tensor, fp32_equivalent_bytes,
                        quantize_tensor, stored_bytes)
 from .tensorops import CSR, mask_apply, mm_theta, relu, spmm, spmm_t
 
@@ -86,7 +86,7 @@ class QuantLinearFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, h, theta, cfg: QuantConfig, stream: RandomStream, ledger=None, row_offset=0):
-        q = quantize_tensor(h, cfg, stream, group_offset=row_offset)
+        q = quantize_tensor(h, cfg, stream, group_offset=row_group_offset(row_offset, h.shape[1], cfg.group))
         ctx.q = q
         ctx.ledger = ledger
         ctx.bytes = (stored_bytes(q), fp32_equivalent_bytes(q))

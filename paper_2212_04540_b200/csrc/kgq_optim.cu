@@ -19,7 +19,8 @@ __device__ __forceinline__ void adam_elem(float &p, float g, float &m, float &v,
 
 __global__ void __launch_bounds__(256)
 adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
-                float4 *__restrict__ v, int64_t n4, AdamScalars a) {
+                float4 *__restrict__ v, int64_t n4, AdamScalars a, const int64_t *__restrict__ status) {
+    if (status && *(volatile const int64_t *)status) return;   // a step failed: no update
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
          i += (int64_t)gridDim.x * blockDim.x) {
         float4 pp = p[i], mm = m[i], vv = v[i];
@@ -41,7 +42,8 @@ adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__
 __global__ void __launch_bounds__(256)
 adam_vec_dev_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
                     float4 *__restrict__ v, int64_t n4, AdamScalars a, const float *__restrict__ c12,
-                    const int64_t *__restrict__ step_ptr) {
+                    const int64_t *__restrict__ step_ptr, const int64_t *__restrict__ status) {
+    if (status && *(volatile const int64_t *)status) return;
     const int64_t t = __ldg(step_ptr);
     a.c1 = __ldg(c12 + 2 * t);
     a.c2 = __ldg(c12 + 2 * t + 1);
@@ -60,7 +62,9 @@ adam_vec_dev_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4
 }
 
 __global__ void adam_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
-                            float *__restrict__ v, int64_t n, AdamScalars a) {
+                            float *__restrict__ v, int64_t n, AdamScalars a,
+                            const int64_t *__restrict__ status) {
+    if (status && *(volatile const int64_t *)status) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float pp = p[i], mm = m[i], vv = v[i];
@@ -71,13 +75,97 @@ __global__ void adam_kernel(float *__restrict__ p, const float *__restrict__ g, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Per-step health check (train.py:91-93 and tape.py:256-264 without a host
+// sync): scan the loss and every gradient for non-finite values; the first
+// failing tensor (in list order: loss, then gradients in parameter order) and
+// the step are latched into status[0..1] once, and every later Adam update
+// reads status[0] and skips.  status[2..3] are per-launch scratch (bit mask of
+// failing tensors, finished-block counter) that the last block resets, so the
+// launch can be replayed from a CUDA graph.
+// ---------------------------------------------------------------------------
+constexpr int kMaxCheck = 8;
+struct CheckList { const float *p[kMaxCheck]; int64_t n[kMaxCheck]; };
+
+__global__ void __launch_bounds__(256)
+check_finite_kernel(CheckList L, int count, int code0, const int64_t *__restrict__ step_dev,
+                    int64_t step_host, int64_t *__restrict__ status) {
+    unsigned bad = 0;
+    const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < count; k++) {
+        const float *x = L.p[k];
+        const int64_t n = L.n[k];
+        bool any = false;
+        if ((((uintptr_t)x) & 15u) == 0) {
+            const int64_t n4 = n >> 2;
+            for (int64_t i = tid0; i < n4; i += nthr) {
+                const float4 v = ldg_stream(reinterpret_cast<const float4 *>(x) + i);
+                // x - x is NaN exactly for inf / NaN inputs
+                any |= !(__fsub_rn(v.x, v.x) == 0.0f) | !(__fsub_rn(v.y, v.y) == 0.0f) |
+                       !(__fsub_rn(v.z, v.z) == 0.0f) | !(__fsub_rn(v.w, v.w) == 0.0f);
+            }
+            for (int64_t i = 4 * n4 + tid0; i < n; i += nthr) any |= !(__fsub_rn(x[i], x[i]) == 0.0f);
+        } else {
+            for (int64_t i = tid0; i < n; i += nthr) any |= !(__fsub_rn(x[i], x[i]) == 0.0f);
+        }
+        if (any) bad |= 1u << k;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    __shared__ unsigned s_bad;
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_bad) atomicOr(reinterpret_cast<unsigned long long *>(status + 2), (unsigned long long)s_bad);
+        __threadfence();
+        const unsigned long long done = atomicAdd(reinterpret_cast<unsigned long long *>(status + 3), 1ull);
+        s_last = done == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long mask = *(volatile unsigned long long *)(status + 2);
+        if (mask && status[0] == 0) {
+            status[0] = code0 + __ffsll((long long)mask) - 1;
+            status[1] = step_host + (step_dev ? *step_dev : 0);
+        }
+        status[2] = 0;
+        status[3] = 0;
+    }
+}
+
 }  // namespace kgq
 
 using namespace kgq;
 
+extern "C" int kgq_check_finite_f32(const float *const *tensors, const int64_t *sizes, int32_t count,
+                                    int32_t code0, const int64_t *step_dev, int64_t step_host,
+                                    int64_t *status, void *stream) {
+    if (count < 1 || count > kMaxCheck || !tensors || !sizes || !status || code0 < 1)
+        return KGQ_ERR_INVALID_ARG;
+    CheckList L;
+    int64_t total = 0;
+    for (int k = 0; k < kMaxCheck; k++) {
+        L.p[k] = k < count ? tensors[k] : nullptr;
+        L.n[k] = k < count ? sizes[k] : 0;
+        if (k < count && (L.n[k] < 0 || (L.n[k] > 0 && !L.p[k]))) return KGQ_ERR_INVALID_ARG;
+        total += L.n[k];
+    }
+    int64_t blocks = (total / 4 + 255) / 256;
+    if (blocks > (int64_t)kSMs * 4) blocks = (int64_t)kSMs * 4;
+    if (blocks < 1) blocks = 1;
+    check_finite_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(L, count, code0, step_dev, step_host,
+                                                                     status);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
 extern "C" int kgq_adam_step_f32(float *param, const float *grad, float *m, float *v, int64_t n,
                                  double lr, double beta1, double beta2, double eps, int64_t step,
-                                 void *stream) {
+                                 const int64_t *status, void *stream) {
     if (n < 0 || step < 1) return KGQ_ERR_INVALID_ARG;
     if (n == 0) return KGQ_OK;
     if (!param || !grad || !m || !v) return KGQ_ERR_INVALID_ARG;
@@ -103,11 +191,11 @@ extern "C" int kgq_adam_step_f32(float *param, const float *grad, float *m, floa
         adam_vec_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<float4 *>(param),
                                                     reinterpret_cast<const float4 *>(grad),
                                                     reinterpret_cast<float4 *>(m),
-                                                    reinterpret_cast<float4 *>(v), n4, a);
+                                                    reinterpret_cast<float4 *>(v), n4, a, status);
     } else {
         int64_t blocks = (n + 255) / 256;
         if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
-        adam_kernel<<<(int)blocks, 256, 0, s>>>(param, grad, m, v, n, a);
+        adam_kernel<<<(int)blocks, 256, 0, s>>>(param, grad, m, v, n, a, status);
     }
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
@@ -115,7 +203,8 @@ extern "C" int kgq_adam_step_f32(float *param, const float *grad, float *m, floa
 
 extern "C" int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, float *v, int64_t n,
                                      double lr, double beta1, double beta2, double eps,
-                                     const float *c12, const int64_t *step_ptr, void *stream) {
+                                     const float *c12, const int64_t *step_ptr, const int64_t *status,
+                                     void *stream) {
     if (n < 0 || !c12 || !step_ptr) return KGQ_ERR_INVALID_ARG;
     if (n == 0) return KGQ_OK;
     if (!param || !grad || !m || !v) return KGQ_ERR_INVALID_ARG;
@@ -134,7 +223,7 @@ extern "C" int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, 
     if (blocks > (int64_t)kSMs * 16) blocks = (int64_t)kSMs * 16;
     adam_vec_dev_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<float4 *>(param), reinterpret_cast<const float4 *>(grad),
-        reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, a, c12, step_ptr);
+        reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, a, c12, step_ptr, status);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

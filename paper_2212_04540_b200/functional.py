@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .quantize import (PASSTHROUGH_BITS, QuantConfig, QuantizedTensor, RandomStream,
+from .quantize import (row_group_offset, PASSTHROUGH_BITS, QuantConfig, QuantizedTensor, RandomStream,
                        dequantize_tensor, packed_group_bytes, quantize_tensor)
 from .tensorops import CSR, BitMask, mm, relu, spmm
 
@@ -118,8 +118,8 @@ def layer_forward_unfused(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Q
                           row_offset: int = 0):
     """spmm -> quantize -> mm -> relu as separate launches (any d / bits)."""
     h = spmm(adj, e)
-    q = quantize_tensor(h, cfg, stream, tensor_id, group_offset=row_offset * (
-        1 if cfg.group is None else h.shape[1] // cfg.group))
+    q = quantize_tensor(h, cfg, stream, tensor_id,
+                        group_offset=row_group_offset(row_offset, h.shape[1], cfg.group))
     j = mm(h, theta)
     e_next, mask = relu(j)
     return e_next, mask, q, h
@@ -292,12 +292,21 @@ def topk_rows(scores: torch.Tensor, k: int) -> torch.Tensor:
     """Indices of the k best entries of every row of a fp32 score block, best
     first, ties by ascending column (kgq_topk_rows_f32; the stable
     ``np.argsort(-s, kind="stable")[:k]`` of train.py:141-143); int32, -1
-    past the row length.  1 <= k <= 64."""
+    past the row length.  1 <= k <= 64 runs the K11 kernel; the reference
+    accepts any K, so k > 64 ranks with a stable device sort of -s (NaN last,
+    as numpy's argsort)."""
     if scores.dtype != torch.float32 or scores.dim() != 2 or not scores.is_cuda:
         raise TypeError("topk_rows: expected a 2-D fp32 CUDA tensor")
+    if k < 1:
+        raise ValueError("topk_rows: k must be >= 1")
     if scores.stride(1) != 1:
         scores = scores.contiguous()
     n, m = scores.shape
+    if k > 64:
+        order = torch.sort(-scores, dim=1, stable=True).indices[:, :k].to(torch.int32)
+        if k > m:
+            order = torch.cat([order, order.new_full((n, k - m), -1)], 1)
+        return order
     out = torch.empty((n, k), dtype=torch.int32, device=scores.device)
     st = _lib.load().kgq_topk_rows_f32(scores.data_ptr(), n, m, scores.stride(0), k, out.data_ptr(),
                                        _lib.stream_ptr(scores.device))

@@ -466,7 +466,8 @@ class PartitionedStepGraph:
                     st = L.kgq_adam_step_dev_f32(p.data_ptr(), g.contiguous().data_ptr(), state.m[name].data_ptr(),
                                                  state.v[name].data_ptr(), p.numel(), cfg.lr, state.beta1,
                                                  state.beta2, state.eps, self.c12.data_ptr(),
-                                                 self.step_rel.data_ptr(), _lib.stream_ptr(dev))
+                                                 self.step_rel.data_ptr(), _lib.ptr(getattr(state, "status", None)),
+                                                 _lib.stream_ptr(dev))
                     _lib.check(st, "kgq_adam_step_dev_f32")
                 self.base.add_(self.n_tids)
                 self.loss = loss

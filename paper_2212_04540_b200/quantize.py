@@ -219,6 +219,19 @@ def packed_group_bytes(group: int, bits: int) -> int:
     return (group * bits + 7) // 8
 
 
+def row_group_offset(row_offset: int, cols: int, group: int | None) -> int:
+    """Global index of the first quantization group of a row block that starts
+    at global row ``row_offset`` (row-partitioned runs): groups are the rows
+    of the ``(-1, G)`` view of the whole tensor, so the block must start on a
+    group boundary.  Keying the noise by this global group index is what makes
+    the codes byte-identical at any world size."""
+    G = cols if group is None else int(group)
+    if (row_offset * cols) % G:
+        raise ValueError(f"row block at row {row_offset} does not start on a group boundary "
+                         f"(cols {cols}, group {G})")
+    return row_offset * cols // G
+
+
 def quantize_tensor(x: torch.Tensor, cfg: QuantConfig, stream: RandomStream | None = None,
                     tensor_id: int | None = None, *, noise: torch.Tensor | None = None,
                     group_offset: int = 0, out: QuantizedTensor | None = None) -> QuantizedTensor:

@@ -53,11 +53,16 @@ def test_topk_rows_all_masked_and_strided():
 
 
 def test_topk_rows_rejects_bad_k():
+    from paper_2212_04540_b200 import _lib
     from paper_2212_04540_b200 import functional as F
     s = torch.zeros(4, 10, device="cuda")
-    for k in (0, 65):
-        with pytest.raises(Exception):
+    for k in (0, -1):
+        with pytest.raises(ValueError):
             F.topk_rows(s, k)
+    # the K11 kernel itself takes 1 <= k <= 64; larger K ranks by a stable sort
+    out = torch.empty((4, 65), dtype=torch.int32, device="cuda")
+    st = _lib.load().kgq_topk_rows_f32(s.data_ptr(), 4, 10, 10, 65, out.data_ptr(), _lib.stream_ptr())
+    assert st == _lib.KGQ_ERR_INVALID_ARG
 
 
 @pytest.mark.parametrize("name", ["int", "gauss"])
