@@ -87,9 +87,172 @@ __device__ __forceinline__ void quant_pieces(const float4 (&v)[Geo<G, T>::NF], f
     }
 }
 
+// Unguarded groups (the common case) on packed fp32 pairs: the same IEEE
+// sequence as quant_pieces<..., false> -- a = x - Z, q0 = a*y, e = a - R*q0,
+// q = q0 + y*e, s = q*B, then the code -- two elements per FADD2 / FMUL2 /
+// FFMA2, so about half the FP issue slots (K1 is issue-bound).
+template <int G, int T, int BITS, int MODE>
+__device__ __forceinline__ void quant_pieces_x2(const float4 (&v)[Geo<G, T>::NF], float z, const DivR &dv,
+                                                const FastKey &fk, uint64_t gglob, int j,
+                                                uint64_t seed, uint64_t tid,
+                                                uint32_t (&piece)[Geo<G, T>::NF]) {
+    using GE = Geo<G, T>;
+    constexpr float Bf = (float)PackInfo<BITS>::B;
+    const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
+    const f32x2 mz = pk2(-z, -z), y2 = pk2(dv.y, dv.y), mr2 = pk2(-dv.r, -dv.r), B2 = pk2(Bf, Bf);
+    const f32x2 mu2 = pk2(-0x1p-16f, -0x1p-16f), mg2 = pk2(kMagic + 128.0f, kMagic + 128.0f);
+#pragma unroll
+    for (int p = 0; p < GE::NBLK / 2; p++) {
+#pragma unroll
+        for (int qq = 0; qq < GE::Q; qq++) {
+            const int q = j * GE::Q + qq;
+            uint4 rnd = make_uint4(0, 0, 0, 0);
+            if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)(4 * p + q));
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int i = 2 * p + h;
+                const int f = i * GE::Q + qq;
+                u64x4 r64 = {0, 0, 0, 0};
+                if (MODE == KGQ_ROUND_SR_COMPAT)
+                    r64 = philox4x64_10(gglob * (uint64_t)(G / 4) + (uint64_t)(4 * i + q) + 1ull,
+                                        0, 0, 0, seed, tid);
+                const f32x2 xv[2] = {pk2(v[f].x, v[f].y), pk2(v[f].z, v[f].w)};
+                const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+                const uint64_t cw[4] = {r64.x, r64.y, r64.z, r64.w};
+                uint32_t cb[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 2; e2++) {
+                    const f32x2 a = add2_rn(xv[e2], mz);
+                    const f32x2 q0 = mul2_rn(a, y2);
+                    const f32x2 er = fma2_rn(mr2, q0, a);
+                    const f32x2 qv = fma2_rn(y2, er, q0);
+                    const f32x2 sc = mul2_rn(qv, B2);
+                    if (MODE == KGQ_ROUND_NEAREST) {
+                        // scalar magic adds: ptxas contracts mul.rn.f32x2 + add.rn.f32x2
+                        // into one FFMA2 (a single rounding), which would change rint(s)
+                        uint32_t s0, s1;
+                        upk2u(sc, s0, s1);
+                        cb[2 * e2] = code_bits<MODE>(__uint_as_float(s0), 0.f, 0);
+                        cb[2 * e2 + 1] = code_bits<MODE>(__uint_as_float(s1), 0.f, 0);
+                    } else if (MODE == KGQ_ROUND_SR_FAST) {
+                        const uint32_t u0 = h ? __byte_perm(rw[2 * e2], kc, 0x7632) : __byte_perm(rw[2 * e2], kc, 0x7610);
+                        const uint32_t u1 = h ? __byte_perm(rw[2 * e2 + 1], kc, 0x7632)
+                                              : __byte_perm(rw[2 * e2 + 1], kc, 0x7610);
+                        const f32x2 x1 = fma2_ru(pk2u(u0, u1), mu2, sc);   // RU(s - 128 - u)
+                        upk2u(add2_ru(x1, mg2), cb[2 * e2], cb[2 * e2 + 1]);
+                    } else {
+                        uint32_t s0, s1;
+                        upk2u(sc, s0, s1);
+                        cb[2 * e2] = code_bits<MODE>(__uint_as_float(s0), 0.f, cw[2 * e2] >> 11);
+                        cb[2 * e2 + 1] = code_bits<MODE>(__uint_as_float(s1), 0.f, cw[2 * e2 + 1] >> 11);
+                    }
+                }
+                uint32_t acc = cb[0];
+#pragma unroll
+                for (int e = 1; e < 4; e++) acc += cb[e] << (BITS * e);
+                piece[f] = acc - magic_sum4<BITS>();
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K1: fast fused quantize + pack.
 // ---------------------------------------------------------------------------
+// One warp tile (GPW groups) from the NF float4 each lane holds: min / max,
+// the codes (packed, staged in shared memory, 16-byte coalesced stores) and
+// R, Z.  FULL tiles (all but at most one per launch) skip every bounds check.
+template <int G, int T, int BITS, int MODE, bool FULL>
+__device__ __forceinline__ void quant_tile(const float4 (&v)[Geo<G, T>::NF], int64_t tile, int64_t n_groups,
+                                           int lane, int j, int gw, uint8_t *st, const FastKey &fk,
+                                           uint64_t seed, uint64_t tid, int64_t group_offset,
+                                           uint8_t *__restrict__ codes, float *__restrict__ ranges,
+                                           float *__restrict__ offsets) {
+    using GE = Geo<G, T>;
+    constexpr int NF = GE::NF, Q = GE::Q, GPW = GE::GPW;
+    constexpr int GB = G * BITS / 8;              // packed bytes per group
+    constexpr int PW = 4 * BITS * Q;              // packed bits per thread per block
+    constexpr int TB = GPW * GB;                  // packed bytes per tile (multiple of 16)
+    const int64_t g = tile * GPW + gw;
+    float mn = fmin_nan(fmin_nan(v[0].x, v[0].y), fmin_nan(v[0].z, v[0].w));
+    float mx = fmax_nan(fmax_nan(v[0].x, v[0].y), fmax_nan(v[0].z, v[0].w));
+#pragma unroll
+    for (int f = 1; f < NF; f++) {
+        mn = fmin_nan(mn, fmin_nan(fmin_nan(v[f].x, v[f].y), fmin_nan(v[f].z, v[f].w)));
+        mx = fmax_nan(mx, fmax_nan(fmax_nan(v[f].x, v[f].y), fmax_nan(v[f].z, v[f].w)));
+    }
+#pragma unroll
+    for (int o = 1; o < T; o <<= 1) {
+        mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const float z = mn;
+    const float r = __fsub_rn(mx, mn);
+    const DivR dv = make_div(r);
+    const uint64_t gglob = (uint64_t)(group_offset + g);
+
+    uint32_t piece[NF];
+    if (r > 0.0f) {
+        if (group_div_unguarded(dv, z))
+#ifndef KGQ_NO_X2
+            quant_pieces_x2<G, T, BITS, MODE>(v, z, dv, fk, gglob, j, seed, tid, piece);
+#else
+            quant_pieces<G, T, BITS, MODE, false>(v, z, dv, fk, gglob, j, seed, tid, piece);
+#endif
+        else
+            quant_pieces<G, T, BITS, MODE, true>(v, z, dv, fk, gglob, j, seed, tid, piece);
+    } else {
+#pragma unroll
+        for (int f = 0; f < NF; f++) piece[f] = 0;   // R == 0 -> scaled 0 -> code 0
+    }
+
+    // stage the packed codes: the thread's Q float4 of block i are PW
+    // contiguous bits at byte (16i + 4jQ) * BITS / 8 of the group
+    uint8_t *gst = st + gw * GB;
+#pragma unroll
+    for (int i = 0; i < GE::NBLK; i++) {
+        const int off = (16 * i + 4 * j * Q) * BITS / 8;
+        if (PW == 64) {
+            *reinterpret_cast<uint2 *>(gst + off) = make_uint2(piece[i * Q], piece[i * Q + 1]);
+        } else {
+            uint32_t w = piece[i * Q];
+            if constexpr (Q == 2) w |= piece[i * Q + 1] << (4 * BITS);
+            if (PW == 32) *reinterpret_cast<uint32_t *>(gst + off) = w;
+            else if (PW == 16) *reinterpret_cast<uint16_t *>(gst + off) = (uint16_t)w;
+            else if (PW == 8) gst[off] = (uint8_t)w;
+            else {  // PW == 4 (T=4, BITS=1): pair lanes j, j^1 into one byte
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, w, 1);
+                if ((j & 1) == 0) gst[off] = (uint8_t)(w | (other << 4));
+            }
+        }
+    }
+    __syncwarp();
+    uint8_t *dst = codes + tile * TB;
+    if (FULL) {
+        constexpr int NCH = TB / 16;
+#pragma unroll
+        for (int k = 0; k < (NCH + 31) / 32; k++) {
+            const int c = lane + 32 * k;
+            if (NCH % 32 == 0 || c < NCH)
+                *reinterpret_cast<uint4 *>(dst + 16 * c) = *reinterpret_cast<const uint4 *>(st + 16 * c);
+        }
+        // R and Z: one store per lane (j = 0 -> R, j = 1 -> Z)
+        if (j < 2) (j ? offsets : ranges)[g] = j ? z : r;
+    } else {
+        const int nvalid = (int)imin64(GPW, n_groups - tile * GPW);
+        const int nbytes = nvalid * GB;
+        if ((nbytes & 15) == 0) {
+            for (int b = lane * 16; b < nbytes; b += 32 * 16)
+                *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
+        } else {
+            for (int b = lane * 4; b < nbytes; b += 32 * 4)
+                *reinterpret_cast<uint32_t *>(dst + b) = *reinterpret_cast<const uint32_t *>(st + b);
+        }
+        if (gw < nvalid && j < 2) (j ? offsets : ranges)[g] = j ? z : r;
+    }
+    __syncwarp();
+}
+
 template <int G, int T, int BITS, int MODE>
 __global__ void __launch_bounds__(kThreads)
 quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__restrict__ codes,
@@ -98,11 +261,10 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
     if (tid_base) tid += __ldg(tid_base);          // graph replays advance the key on device
     using GE = Geo<G, T>;
     constexpr int NF = GE::NF, Q = GE::Q, GPW = GE::GPW, S = GE::S;
-    constexpr int GB = G * BITS / 8;              // packed bytes per group
-    constexpr int PW = 4 * BITS * Q;              // packed bits per thread per block
+    constexpr int GB = G * BITS / 8;
     __shared__ __align__(16) uint8_t stage[kWarps][GPW * GB];
-    // cp.async ring: each lane streams its own float4s for the next S-1 tiles
-    // into private shared-memory slots (no cross-lane sharing -> no barriers).
+    // cp.async ring: each lane streams its own float4s for the next S-1 full
+    // tiles into private shared-memory slots (no cross-lane sharing -> no barriers).
     extern __shared__ __align__(16) float4 pf_raw[];   // [kWarps][S][NF][32]
     auto pf = reinterpret_cast<float4 (*)[S][NF][32]>(pf_raw);
 
@@ -111,31 +273,29 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
     uint8_t *st = stage[warp];
     const FastKey fk = make_fast_key(seed, tid);
 
-    const int64_t n_tiles = (n_groups + GPW - 1) / GPW;
+    const int64_t n_full = n_groups / GPW;             // full tiles
     const int64_t stride = (int64_t)gridDim.x * kWarps;
     const int64_t tile0 = (int64_t)blockIdx.x * kWarps + warp;
-    const float4 *xb = reinterpret_cast<const float4 *>(x) + j * Q;
-    const int64_t gstep = stride * GPW;
-    int64_t gnext = tile0 * GPW + gw;     // group of the next tile to prefetch
-    auto issue = [&](int s) {             // one commit group per tile (possibly empty)
-        if (gnext < n_groups) {
-            const float4 *src = xb + gnext * (G / 4);
+    const float4 *xb = reinterpret_cast<const float4 *>(x) + j * Q + gw * (G / 4);
+    int64_t pnext = tile0;                             // next full tile to prefetch
+    auto issue = [&](int s) {                          // one commit group per tile (possibly empty)
+        if (pnext < n_full) {
+            const float4 *src = xb + pnext * (GPW * G / 4);
 #pragma unroll
             for (int i = 0; i < GE::NBLK; i++)
 #pragma unroll
                 for (int qq = 0; qq < Q; qq++) cp_async16(&pf[warp][s][i * Q + qq][lane], src + 4 * i + qq);
         }
         cp_async_commit();
-        gnext += gstep;
+        pnext += stride;
     };
     if (S > 1) {
 #pragma unroll
         for (int k = 0; k < S - 1; k++) issue(k);
     }
     int cur = 0;
-    for (int64_t tile = tile0; tile < n_tiles; tile += stride) {
-        const int64_t g = tile * GPW + gw;
-        const bool valid = g < n_groups;   // invalid lanes compute on stale data, store nothing
+    int64_t tile = tile0;
+    for (; tile < n_full; tile += stride) {
         float4 v[NF];
         if (S > 1) {
             cp_async_wait<(S > 1 ? S - 2 : 0)>();
@@ -144,86 +304,30 @@ quantize_fast_kernel(const float *__restrict__ x, int64_t n_groups, uint8_t *__r
             issue(cur == 0 ? S - 1 : cur - 1);
             cur = (cur + 1 == S) ? 0 : cur + 1;
         } else {
-            const float4 *src = xb + (valid ? g : 0) * (G / 4);
+            const float4 *src = xb + tile * (GPW * G / 4);
 #pragma unroll
             for (int i = 0; i < GE::NBLK; i++)
 #pragma unroll
                 for (int qq = 0; qq < Q; qq++) v[i * Q + qq] = ldg_stream(src + 4 * i + qq);
         }
-
-        float mn = fmin_nan(fmin_nan(v[0].x, v[0].y), fmin_nan(v[0].z, v[0].w));
-        float mx = fmax_nan(fmax_nan(v[0].x, v[0].y), fmax_nan(v[0].z, v[0].w));
+        quant_tile<G, T, BITS, MODE, true>(v, tile, n_groups, lane, j, gw, st, fk, seed, tid, group_offset,
+                                          codes, ranges, offsets);
+    }
+    if (S > 1) cp_async_wait<0>();
+    // the partial last tile (at most one per launch): guarded direct loads;
+    // lanes past the end compute on zeros and store nothing
+    if (tile * GPW < n_groups) {
+        const int64_t g = tile * GPW + gw;
+        const bool valid = g < n_groups;
+        const float4 *src = xb + tile * (GPW * G / 4);
+        float4 v[NF];
 #pragma unroll
-        for (int f = 1; f < NF; f++) {
-            mn = fmin_nan(mn, fmin_nan(fmin_nan(v[f].x, v[f].y), fmin_nan(v[f].z, v[f].w)));
-            mx = fmax_nan(mx, fmax_nan(fmax_nan(v[f].x, v[f].y), fmax_nan(v[f].z, v[f].w)));
-        }
+        for (int i = 0; i < GE::NBLK; i++)
 #pragma unroll
-        for (int o = 1; o < T; o <<= 1) {
-            mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        const float z = mn;
-        const float r = __fsub_rn(mx, mn);
-        const DivR dv = make_div(r);
-        const uint64_t gglob = (uint64_t)(group_offset + g);
-
-        uint32_t piece[NF];
-        if (r > 0.0f) {
-            if (group_div_unguarded(dv, z))
-                quant_pieces<G, T, BITS, MODE, false>(v, z, dv, fk, gglob, j, seed, tid, piece);
-            else
-                quant_pieces<G, T, BITS, MODE, true>(v, z, dv, fk, gglob, j, seed, tid, piece);
-        } else {
-#pragma unroll
-            for (int f = 0; f < NF; f++) piece[f] = 0;   // R == 0 -> scaled 0 -> code 0
-        }
-
-        // stage the packed codes: the thread's Q float4 of block i are PW
-        // contiguous bits at byte (16i + 4jQ) * BITS / 8 of the group
-        uint8_t *gst = st + gw * GB;
-#pragma unroll
-        for (int i = 0; i < GE::NBLK; i++) {
-            const int off = (16 * i + 4 * j * Q) * BITS / 8;
-            if (PW == 64) {
-                *reinterpret_cast<uint2 *>(gst + off) = make_uint2(piece[i * Q], piece[i * Q + 1]);
-            } else {
-                uint32_t w = piece[i * Q];
-                if constexpr (Q == 2) w |= piece[i * Q + 1] << (4 * BITS);
-                if (PW == 32) *reinterpret_cast<uint32_t *>(gst + off) = w;
-                else if (PW == 16) *reinterpret_cast<uint16_t *>(gst + off) = (uint16_t)w;
-                else if (PW == 8) gst[off] = (uint8_t)w;
-                else {  // PW == 4 (T=4, BITS=1): pair lanes j, j^1 into one byte
-                    const uint32_t other = __shfl_xor_sync(0xffffffffu, w, 1);
-                    if ((j & 1) == 0) gst[off] = (uint8_t)(w | (other << 4));
-                }
-            }
-        }
-        __syncwarp();
-        const int64_t g0 = tile * GPW;
-        const int nvalid = (int)imin64(GPW, n_groups - g0);
-        uint8_t *dst = codes + g0 * GB;
-        const int nbytes = nvalid * GB;
-        if (nvalid == GPW) {   // full tile: GPW*GB bytes, a multiple of 16
-            constexpr int NCH = GPW * GB / 16;
-#pragma unroll
-            for (int k = 0; k < (NCH + 31) / 32; k++) {
-                const int c = lane + 32 * k;
-                if (NCH % 32 == 0 || c < NCH)
-                    *reinterpret_cast<uint4 *>(dst + 16 * c) = *reinterpret_cast<const uint4 *>(st + 16 * c);
-            }
-        } else if ((nbytes & 15) == 0) {
-            for (int b = lane * 16; b < nbytes; b += 32 * 16)
-                *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
-        } else {
-            for (int b = lane * 4; b < nbytes; b += 32 * 4)
-                *reinterpret_cast<uint32_t *>(dst + b) = *reinterpret_cast<const uint32_t *>(st + b);
-        }
-        if (valid && j == 0) {
-            ranges[g] = r;
-            offsets[g] = z;
-        }
-        __syncwarp();
+            for (int qq = 0; qq < Q; qq++)
+                v[i * Q + qq] = valid ? ldg_stream(src + 4 * i + qq) : make_float4(0.f, 0.f, 0.f, 0.f);
+        quant_tile<G, T, BITS, MODE, false>(v, tile, n_groups, lane, j, gw, st, fk, seed, tid, group_offset,
+                                           codes, ranges, offsets);
     }
 }
 
