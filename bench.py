@@ -143,16 +143,19 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_port_run(rows, cols, bits, group, threads, seed=1, tid=0, min_seconds=0.0, max_reps=1):
-    """The oracle port of the reference quantize/dequantize (compat stream) on
-    host cores.  Returns (GB/s, seconds, reps)."""
+def cpu_port_run(rows, cols, bits, group, threads, seed=1, tid=0, min_seconds=0.0, max_reps=1, rng="compat"):
+    """The oracle port of the reference quantize/dequantize on host cores, with
+    the reference's numpy Philox4x64-10 stream (rng="compat") or the fast
+    stream the GPU arm's headline uses (rng="fast": the reference's rounding
+    fed that noise, the exported-noise route).  Returns (GB/s, seconds, reps)."""
     from oracle import oracle as orc
+    mode = orc.MODE_SR_COMPAT if rng == "compat" else orc.MODE_SR_FAST
     x = np.random.default_rng(0).standard_normal((rows * cols // group, group), dtype=np.float32)
     orc.lib()
     t0 = time.perf_counter()
     reps = 0
     while True:
-        c, r, o = orc.quantize(x, group, bits, orc.MODE_SR_COMPAT, seed, tid + reps, threads=threads)
+        c, r, o = orc.quantize(x, group, bits, mode, seed, tid + reps, threads=threads)
         orc.dequantize(c, r, o, group, bits, threads=threads)
         reps += 1
         el = time.perf_counter() - t0
@@ -170,16 +173,22 @@ def run_reference(args):
         return 0
     threads = os.cpu_count() or 1
     rows = args.ref_rows
+    # the GPU arm's config, unchanged: same workload, widths, group and noise
+    # stream (the per-element CPU rate does not depend on the row count, so
+    # each step is a bounded row sample, stated in cpu_baseline.sample)
     cfg = workload_config(args)
-    cfg["sample"] = f"{rows}x{args.cols} fp32 per step (bounded sample of the workload)"
+    sample = f"{rows}x{args.cols} fp32 rows per step (bounded sample of the {args.rows}-row workload)"
     for _ in range(args.warmup):
-        cpu_port_run(rows, args.cols, args.bits, args.group, threads)
+        cpu_port_run(rows, args.cols, args.bits, args.group, threads, rng=args.rng)
     times = []
     for s in range(args.steps):
-        gbs, el, _ = cpu_port_run(rows, args.cols, args.bits, args.group, threads, tid=1000 + s)
+        gbs, el, _ = cpu_port_run(rows, args.cols, args.bits, args.group, threads, tid=1000 + s, rng=args.rng)
         times.append(el)
     total_gb = 2 * rows * args.cols * algo_bytes_per_elem(args.bits, args.group) * args.steps / 1e9
     value = total_gb / sum(times)
+    # beside it: the reference's own numpy Philox4x64-10 stream (rng="compat")
+    other = "compat" if args.rng != "compat" else "fast"
+    o_gbs, _, _ = cpu_port_run(rows, args.cols, args.bits, args.group, threads, tid=2000, rng=other)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -187,14 +196,60 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": cfg,
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": cfg["sample"] + "; oracle/kgq_oracle.c restatement of "
-                         "quantize_tensor/dequantize_tensor with the reference's numpy "
-                         "Philox4x64 stream, pthreads over groups"},
+                         "sample": sample + f"; oracle/kgq_oracle.c restatement of quantize_tensor/"
+                         f"dequantize_tensor (quantize.py:177-210), rng={args.rng} as in config, "
+                         "pthreads over groups",
+                         f"value_rng_{other}": round(o_gbs, 4)},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pcie_probe(h_in, h_out):
+    """Host<->device copy ceilings on the e2e leg's own pinned buffers, CUDA
+    events: H2D alone, D2H alone, and both directions at once on two streams
+    (the e2e step's traffic pattern).  GB/s per direction."""
+    import torch
+    n = h_in.numel()
+    d_in = torch.empty(n, dtype=torch.float32, device="cuda")
+    d_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    hi, ho = h_in.view(-1), h_out.view(-1)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1e3
+
+    def both():
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        for st, f in ((s1, lambda: d_in.copy_(hi, non_blocking=True)),
+                      (s2, lambda: ho.copy_(d_out, non_blocking=True))):
+            st.wait_event(ev)
+            with torch.cuda.stream(st):
+                f()
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    gb = n * 4 / 1e9
+    h2d = gb / timed(lambda: d_in.copy_(hi, non_blocking=True))
+    d2h = gb / timed(lambda: ho.copy_(d_out, non_blocking=True))
+    t_both = timed(both)
+    del d_in, d_out
+    return {"h2d_GBps": round(h2d, 2), "d2h_GBps": round(d2h, 2),
+            "both_h2d_GBps": round(gb / t_both, 2), "both_d2h_GBps": round(gb / t_both, 2),
+            "bytes_each_way": int(n * 4),
+            "note": "pinned copies of the e2e buffers; 'both' = H2D and D2H on two streams at once"}
 
 
 def workload_config(args):
@@ -228,7 +283,7 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
                        f"{ds.num_items} items, {ds.num_entities} entities, {len(ds.triples)} triples, "
                        f"{len(ds.train)} train pairs; KGNN 3 layers d=64, batch 1024, INT2 stochastic (fast rng)",
            "steps_per_epoch": steps_per_epoch, "n_gpus": world}
-    res = {}
+    res, hbm_peak = {}, {}
     for bits in ((2, 4, 32) if with_fp32 else (2,)):
         q = kgq.QuantConfig(bits=bits, rng="fast")
         mcfg = ModelConfig(layers=3, dim=64, quant=q)
@@ -251,6 +306,17 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
             #     outside the timed region), CUDA events on the launch stream
             trip = torch.from_numpy(D.sample_negatives(ds, np.random.default_rng(1))).cuda()
             k = min(args.train_steps, len(trip) // 1024)
+            # (0) HBM a step allocates beyond the resident state (params, Adam
+            #     moments, adjacency, batches): one eager step under
+            #     torch.cuda.max_memory_allocated (graph replays reuse a pool)
+            from paper_2212_04540_b200.train import _record_step
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
+            base_alloc = torch.cuda.memory_allocated()
+            _, g0, _ = _record_step(ds, adj, params, mcfg, cfg, stream, trip[:1024], True)
+            del g0
+            torch.cuda.synchronize()
+            step_peak = torch.cuda.max_memory_allocated() - base_alloc
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if graphs:
@@ -281,6 +347,7 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
             m = rep["memory"]
             mem = memory_report(m["activation_bytes_peak"], m["fp32_equivalent_bytes"], m.get("adjacency_bytes", 0))
             res[bits] = (ms, mem, rep["loss_curve"][-1], epoch_s)
+            hbm_peak[bits] = step_peak
         else:
             ms = _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args)
             res[bits] = (ms, None, None, None)
@@ -362,6 +429,14 @@ def train_bench(args, world, rank, shape=None, with_fp32=True, with_cpu=True):
             "definition": "reference ledger (tape.py:86-93): quantized contexts + masks + indices + "
                           "margins; 'incl' also counts the shared CSR adjacency once (reference definition)"}
         out["epoch3_mean_loss"] = round(loss2, 5)
+    if hbm_peak:
+        out["hbm_step_peak_MB"] = {f"int{b}" if b != 32 else "fp32": round(v / 1e6, 3) for b, v in hbm_peak.items()}
+        if 2 in hbm_peak and 32 in hbm_peak:
+            out["hbm_step_peak_MB"]["ratio_fp32_over_int2"] = round(hbm_peak[32] / hbm_peak[2], 3)
+        out["hbm_step_peak_MB"]["definition"] = (
+            "torch.cuda.max_memory_allocated during one eager step (forward + backward, no Adam) "
+            "minus the allocation before it: contexts, layer outputs, gradients and scratch; "
+            "fp32 = the same engine at bits=32 (pass-through contexts)")
     return out
 
 
@@ -522,7 +597,10 @@ def industry_bench(args):
                 "steps_per_epoch": -(-n_train // B),
                 "epoch_hours_estimate": round(-(-n_train // B) * (worst + xbytes / 770e9 * 1e3) / 3.6e6, 2),
                 "note": "1-GPU box: compute per rank measured, collectives simulated (not timed); the "
-                        "exchange time is bytes / 770 GB/s measured peer bandwidth, no overlap assumed"})
+                        "exchange time is bytes / 770 GB/s, the peer-copy bandwidth per direction "
+                        "measured on this pool's 8-GPU boxes (B200_PROFILING.md, builder guide; this "
+                        "run had 1 GPU, so it is not re-measured here), no overlap assumed; "
+                        "per-rank compute is SIMULATED one rank at a time"})
     return out
 
 
@@ -534,7 +612,9 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     from paper_2212_04540_b200.parallel import Comm, GpuOps, RowPartition, partitioned_step
     indptr, indices, vals = D.adjacency_arrays(ds)
     part = RowPartition.build(indptr, world, rank)
-    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda")
+    layout = part.preferred_layout()
+    a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda",
+                                     part=part if layout == "padded" else None)
     from paper_2212_04540_b200.train import AdamState, adam_step
     params = init_params(ds.num_nodes, mcfg, 0)
     local = {"E0": params.entity_embeddings[part.lo:part.hi].clone()}
@@ -550,7 +630,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
         b = trip[(i % n_full) * 1024:][:1024]
         thetas = [local[f"theta{k}"] for k in range(mcfg.layers)]
         loss, de0, dth = partitioned_step(part, a_local, local["E0"], thetas, b[:, 0], n_users + b[:, 1],
-                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, layout="global")
+                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, layout=layout)
         grads = {"E0": de0}
         grads.update({f"theta{k}": g for k, g in enumerate(dth)})
         adam_step(local, grads, state, cfg.lr)
@@ -566,7 +646,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 sg = PartitionedStepGraph(part, a_local, local, state, cfg, stream, comm, mcfg.layers, 1024,
-                                          args.train_steps + 2, layout="global")
+                                          args.train_steps + 2, layout=layout)
             torch.cuda.current_stream().wait_stream(side)
         except Exception as exc:      # noqa: BLE001 - keep the eager number
             print(f"[bench] partitioned graph capture failed ({type(exc).__name__}: {exc}); eager", file=sys.stderr)
@@ -739,12 +819,19 @@ def run_ours(args):
                     "calls": "quantize_tensor(host, out=pinned ctx) -> dequantize_tensor(host ctx, "
                              "out=pinned), blocking, wall clock"}
         del qh, oh2, ctx
+        link = pcie_probe(xh, oh)
+        # the e2e step moves 4 B/elem each way at once: its link-bound ceiling
+        # is the slower direction of the simultaneous two-stream copy
+        ceil_s = max(e_rows * cols * 4 / (link["both_h2d_GBps"] * 1e9),
+                     e_rows * cols * 4 / (link["both_d2h_GBps"] * 1e9))
+        link["e2e_ceiling"] = round(2 * e_rows * cols * bpe / ceil_s / 1e9, 3)
+        link["e2e_frac_of_link"] = round(e_val / world / link["e2e_ceiling"], 4)
         e2e = {"value": round(e_val, 3), "unit": UNIT, "h2d_bytes_per_step": e_rows * cols * 4,
                "d2h_bytes_per_step": e_rows * cols * 4,
                "sample": f"{e_rows}x{cols} fp32 per GPU per step (pinned host buffers), "
                          f"{len(bounds)} row chunks pipelined on 3 streams through "
                          f"quantize_tensor/dequantize_tensor",
-               "host_api": host_api}
+               "host_api": host_api, "link": link}
 
     train = None
     if not args.skip_train:
@@ -811,10 +898,15 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.skip_cpu:
         threads = os.cpu_count() or 1
         gbs, el, reps = cpu_port_run(args.cpu_rows, cols, bits, group, threads, min_seconds=10.0,
-                                     max_reps=50)
+                                     max_reps=50, rng=args.rng)
+        c_gbs, c_el, c_reps = cpu_port_run(args.cpu_rows, cols, bits, group, threads, min_seconds=5.0,
+                                           max_reps=20, rng="compat")
         cpu = {"value": round(gbs, 4), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{reps} x ({args.cpu_rows}x{cols} fp32 quantize+dequantize, compat "
-                         f"Philox4x64 stream) in {el:.1f}s; oracle/kgq_oracle.c, pthreads"}
+               "sample": f"{reps} x ({args.cpu_rows}x{cols} fp32 quantize+dequantize, rng={args.rng} as "
+                         f"in config) in {el:.1f}s; oracle/kgq_oracle.c, pthreads",
+               "value_rng_compat": round(c_gbs, 4),
+               "sample_rng_compat": f"{c_reps} x ({args.cpu_rows}x{cols}), the reference's numpy "
+                                    f"Philox4x64-10 stream, in {c_el:.1f}s"}
 
     if rank == 0:
         line = {
@@ -856,6 +948,57 @@ def run_ours(args):
     return 0
 
 
+def launch(args, argv):
+    """``bench.py --gpus N`` starts its own N ranks, one process per GPU:
+    under torchrun (WORLD_SIZE set) this process is one rank and runs; with
+    N > 1 and no torchrun it re-executes itself through
+    ``torch.distributed.run`` (127.0.0.1 rendezvous, the driver's own launch
+    line) and returns the launcher's exit code -- rank 0 prints the one JSON
+    line; N == 1 runs in this process (world 1, the same code path).
+    Returns None when this process should run the benchmark itself."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:                   # a free rendezvous port
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    if not args.launch_selftest:                  # NCCL communicator setup (NVLS / ring / tree) in the log
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    import subprocess
+    return subprocess.call(cmd, env=env)
+
+
+def launch_selftest(args):
+    """The launcher's plumbing without a GPU (gloo): every rank times a
+    rank-dependent sleep between barriers, the max over ranks goes to rank 0,
+    which prints the line a real run would (n_gpus = world)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "selftest": True, "n_gpus": world, "steps": args.steps,
+                          "max_rank_seconds": round(float(t.item()), 4),
+                          "ranks_seen": world}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -887,7 +1030,18 @@ def main():
                     help="use the row-partitioned (multi-GPU) training step even at 1 GPU")
     ap.add_argument("--train-shape", default="amazon", choices=["small", "lastfm", "amazon"])
     ap.add_argument("--train-steps", type=int, default=100)
-    args = ap.parse_args()
+    ap.add_argument("--launch-selftest", action="store_true",
+                    help="exercise the --gpus N launcher on CPU (gloo), no benchmark")
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
+    rc = launch(args, argv)
+    if rc is not None:
+        return rc
+    if args.launch_selftest:
+        return launch_selftest(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("KGQ_ALLOW_SHORT_WARMUP"):
         args.warmup = 3
     if args.impl == "reference":
