@@ -95,6 +95,23 @@ uint32_t oracle_fast_u16(uint64_t seed, uint64_t tid, uint64_t g, int64_t k) {
     return (out[k & 3] >> (16 * ((k >> 4) & 1))) & 0xFFFFu;
 }
 
+/* All G draws of group g at once: each Philox call yields 8 of them (4 words
+ * x 2 halves), the same values oracle_fast_u16 gives element by element. */
+static void fast_group_u16(uint64_t seed, uint64_t tid, uint64_t g, int64_t G, uint16_t *buf) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32) ^ (uint32_t)(tid >> 32)};
+    int64_t n_calls = 4 * ((G + 31) / 32);
+    for (int64_t c = 0; c < n_calls; c++) {
+        uint32_t ctr[4] = {(uint32_t)c, (uint32_t)g, (uint32_t)(g >> 32), (uint32_t)tid};
+        uint32_t out[4];
+        oracle_philox4x32_r(ctr, key, out, ORACLE_FAST_ROUNDS);
+        for (int h = 0; h < 2; h++)
+            for (int w = 0; w < 4; w++) {
+                int64_t k = 32 * (c >> 2) + 16 * h + 4 * (c & 3) + w;
+                if (k < G) buf[k] = (uint16_t)((out[w] >> (16 * h)) & 0xFFFFu);
+            }
+    }
+}
+
 void oracle_fast_noise_u16(uint64_t seed, uint64_t tid, int64_t n_groups, int64_t G, uint16_t *out) {
     for (int64_t g = 0; g < n_groups; g++)
         for (int64_t k = 0; k < G; k++)
@@ -120,7 +137,8 @@ static inline float f32_div(float a, float b) { volatile float q = a / b; return
 
 static void quantize_groups(const float *x, int64_t g0, int64_t g1, int64_t G, int bits, int mode,
                             uint64_t seed, uint64_t tid, int64_t goff, const double *noise,
-                            uint8_t *codes, float *ranges, float *offsets, uint8_t *scratch) {
+                            uint8_t *codes, float *ranges, float *offsets, uint8_t *scratch,
+                            uint16_t *noise16) {
     const int64_t gbytes = (G * bits + 7) / 8;
     const float B = (float)((1u << bits) - 1u);
     const uint64_t bpr = (uint64_t)((G + 3) / 4);
@@ -158,7 +176,8 @@ static void quantize_groups(const float *x, int64_t g0, int64_t g1, int64_t G, i
                 float frac = s - fl;
                 double u;
                 if (mode == KGQ_MODE_SR_FAST) {
-                    u = (double)oracle_fast_u16(seed, tid, (uint64_t)(g + goff), k) * (1.0 / 65536.0);
+                    if (k == 0) fast_group_u16(seed, tid, (uint64_t)(g + goff), G, noise16);
+                    u = (double)noise16[k] * (1.0 / 65536.0);
                 } else if (mode == KGQ_MODE_SR_COMPAT) {
                     uint64_t blk = (uint64_t)(g + goff) * bpr + (uint64_t)(k / 4) + 1u;
                     if (blk != blk_cache) {
@@ -192,8 +211,10 @@ typedef struct {
 static void *quantize_worker(void *p) {
     qjob_t *j = (qjob_t *)p;
     uint8_t *scratch = (uint8_t *)malloc((size_t)j->G);
+    uint16_t *noise16 = (uint16_t *)malloc((size_t)j->G * sizeof(uint16_t));
     quantize_groups(j->x, j->g0, j->g1, j->G, j->bits, j->mode, j->seed, j->tid, j->goff, j->noise,
-                    j->codes, j->ranges, j->offsets, scratch);
+                    j->codes, j->ranges, j->offsets, scratch, noise16);
+    free(noise16);
     free(scratch);
     return NULL;
 }
