@@ -24,6 +24,7 @@
 //    fused quantizer).  The next column ids are prefetched while the current
 //    neighbour rows are gathered.
 #include "kgq_common.cuh"
+#include "kgq_tc.cuh"
 
 namespace kgq {
 
@@ -696,6 +697,134 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
 }
 
 
+// Split layer forward, part 2 on the tensor cores (K6t, d in {32, 64}): the
+// same per-row quantization as layer_epilogue_kernel (light_row_quantize, one
+// LPR-lane group per row), then J = H . theta as a tcgen05 GEMM -- H split
+// into TF32 hi/lo and staged in the K-major interleaved UMMA layout, theta
+// staged once per CTA, 3xTF32 (hi.hi + hi.lo + lo.hi, fp32-level accuracy)
+// into a TMEM accumulator of 128 lanes x D columns issued by one thread --
+// and a TMEM drain that applies relu, writes E_next rows and the mask words.
+// J differs from the FFMA chain of the fused kernel in the last bits (another
+// summation order, as OpenBLAS's differs from both): split and fused agree to
+// fp32 rounding, not bitwise (tests/test_gpu_train.py).
+template <int D>
+struct EpiTc {
+    static constexpr int M = 128;                                   // rows per tile
+    static constexpr size_t smem = (size_t)(2 * M * D + 2 * D * D) * sizeof(float);
+};
+
+template <int D, int BITS, int MODE>
+__global__ void __launch_bounds__(256)
+layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
+                         uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
+                         int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
+                         float *__restrict__ offsets, float *__restrict__ e_next,
+                         uint32_t *__restrict__ mask) {
+    constexpr int M = EpiTc<D>::M;
+    constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
+    constexpr int NP = M / (8 * RPW);               // load/quantize passes per tile
+    constexpr uint32_t TCOLS = D < 32 ? 32 : D;
+    extern __shared__ __align__(128) float tc_smem[];
+    float *ah = tc_smem, *al = tc_smem + M * D;               // H tile hi / lo [M x D]
+    float *bh = tc_smem + 2 * M * D, *bl = bh + D * D;        // theta^T hi / lo: B(n, k) = theta[k][n]
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int gl = lane % LPR, grp = lane / LPR;
+    const int fa = rg_f4a<D, true>(gl), fb = rg_f4b<D, true>(gl);
+
+    for (int i = t; i < D * D; i += 256) {
+        const int n = i / D, k = i % D;
+        float hi, lo;
+        tc::split_tf32(__ldg(theta + k * D + n), hi, lo);
+        bh[tc::tile_off(n, k, D) / 4] = hi;
+        bl[tc::tile_off(n, k, D) / 4] = lo;
+    }
+    if (t == 0) tc::mbar_init(&mbar, 1);
+    if (warp == 0) tc::tmem_alloc(&tmem_base, TCOLS);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    if (tid_base) tid += __ldg(tid_base);
+    const FastKey fk = make_fast_key(seed, tid);
+
+    const int64_t n_tiles = (n_rows + M - 1) / M;
+    float4 nh[2];
+    auto fetch = [&](int64_t tl, int ps) {
+        const int64_t rw = tl * M + (ps * 8 + warp) * RPW + grp;
+        if (tl < n_tiles && rw < n_rows) {
+            const float4 *src = reinterpret_cast<const float4 *>(hin + rw * D);
+            nh[0] = __ldg(src + fa);
+            nh[1] = __ldg(src + fb);
+        } else {
+            nh[0] = nh[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    fetch(blockIdx.x, 0);
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * M;
+        // ---- 1. load + quantize + split/stage (register prefetch one pass ahead) ----
+#pragma unroll
+        for (int pass = 0; pass < NP; pass++) {
+            const int lr = (pass * 8 + warp) * RPW + grp;
+            const int64_t row = r0 + lr;
+            const bool active = row < n_rows;
+            float4 h[2] = {nh[0], nh[1]};
+            if (pass + 1 < NP) fetch(tile, pass + 1);
+            else fetch(tile + gridDim.x, 0);
+            if constexpr (BITS != 32)
+            light_row_quantize<D, BITS, MODE>(h, active, active ? row : 0, gl, fk, seed, tid, row_offset,
+                                              codes, ranges, offsets);
+#pragma unroll
+            for (int hf = 0; hf < 2; hf++) {
+                const float xs[4] = {h[hf].x, h[hf].y, h[hf].z, h[hf].w};
+                float hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) tc::split_tf32(xs[e], hi[e], lo[e]);
+                const uint32_t off = tc::tile_off(lr, 4 * (hf ? fb : fa), M) / 4;
+                *reinterpret_cast<float4 *>(ah + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<float4 *>(al + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+        // ---- 2. J = H . theta on the tensor cores ----
+        if (t == 0) {
+            tc::fence_after();
+            tc::mma_3xtf32<M, D, D>(tmem, ah, al, bh, bl);
+            tc::commit(&mbar);
+        }
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        // ---- 3. drain: warp w -> TMEM lanes 32*(w%4).. (its rows), columns 32*(w/4)..; relu, E_next, mask ----
+        if (warp < 4 * (D / 32)) {
+            const int q = warp & 3, cb = 32 * (warp >> 2);
+            float v[32];
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
+            const int64_t row = r0 + 32 * q + lane;
+            uint32_t word = 0;
+#pragma unroll
+            for (int c = 0; c < 32; c++) {
+                word |= (v[c] > 0.0f ? 1u : 0u) << c;
+                v[c] = v[c] > 0.0f ? v[c] : 0.0f;
+            }
+            if (row < n_rows) {
+                float4 *dst = reinterpret_cast<float4 *>(e_next + row * D + cb);
+#pragma unroll
+                for (int j = 0; j < 8; j++) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                mask[row * (D / 32) + (cb >> 5)] = word;
+            }
+        }
+        tc::fence_before();
+        __syncthreads();
+    }
+    if (warp == 0) tc::tmem_free(tmem, TCOLS);
+}
+
+
 }  // namespace kgq
 
 using namespace kgq;
@@ -782,11 +911,52 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
     return KGQ_OK;
 }
 
+// K6t (tcgen05 J) is the default for d in {32, 64}; KGQ_EPI_FFMA=1 in the
+// environment selects the FFMA epilogue (bit-identical to the fused kernel).
+static bool epi_use_tc(int d) {
+    const char *e = getenv("KGQ_EPI_FFMA");      // read per launch (host side, cheap)
+    return !(e && e[0] == '1') && (d == 32 || d == 64);
+}
+
+template <int D, int BITS>
+static int launch_epilogue_tc(int rounding, const float *h, int64_t n_rows, const float *theta,
+                              uint64_t seed, uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
+                              uint8_t *codes, float *ranges, float *offsets, float *e_next,
+                              uint32_t *mask, cudaStream_t s) {
+    const size_t smem = EpiTc<D>::smem;
+    void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
+                 uint8_t *, float *, float *, float *, uint32_t *);
+    switch (rounding) {
+        case KGQ_ROUND_NEAREST: kern = layer_epilogue_tc_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
+        case KGQ_ROUND_SR_FAST: kern = layer_epilogue_tc_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
+        case KGQ_ROUND_SR_COMPAT: kern = layer_epilogue_tc_kernel<D, BITS, KGQ_ROUND_SR_COMPAT>; break;
+        default: return KGQ_ERR_INVALID_ARG;
+    }
+    static bool smem_set[3] = {false, false, false};
+    if (!smem_set[rounding]) {
+        cudaError_t ea = ensure_smem(kern, smem);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set[rounding] = true;
+    }
+    const int64_t tiles = (n_rows + EpiTc<D>::M - 1) / EpiTc<D>::M;
+    const int64_t cap = (int64_t)kSMs * (D > 32 ? 2 : 4);
+    const int grid = (int)(tiles < cap ? tiles : cap);
+    kern<<<grid, 256, smem, s>>>(h, n_rows, theta, seed, tid, tid_base, row_offset, codes, ranges,
+                                 offsets, e_next, mask);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
 template <int D, int BITS>
 static int launch_epilogue(int rounding, const float *h, int64_t n_rows, const float *theta,
                            uint64_t seed, uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
                            uint8_t *codes, float *ranges, float *offsets, float *e_next,
                            uint32_t *mask, cudaStream_t s) {
+    if constexpr (D == 32 || D == 64) {
+        if (epi_use_tc(D))
+            return launch_epilogue_tc<D, BITS>(rounding, h, n_rows, theta, seed, tid, tid_base, row_offset,
+                                               codes, ranges, offsets, e_next, mask, s);
+    }
     const size_t smem = EpiTile<D>::smem;
     void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
                  uint8_t *, float *, float *, float *, uint32_t *);

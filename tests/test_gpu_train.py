@@ -172,10 +172,13 @@ def test_fused_layer_matches_unfused_and_oracle():
 
 @pytest.mark.parametrize("d", [32, 64, 128])
 def test_split_layer_bit_identical_to_fused(d):
-    """spmm_kernel + layer_epilogue_kernel (kgq_layer_epilogue_f32) produce the
-    same bytes as the single fused kernel: E_next, codes, ranges, offsets,
-    mask, at every bit width and rounding mode, with hub (CTA-path) rows and
-    a row offset."""
+    """spmm_kernel + the FFMA epilogue (KGQ_EPI_FFMA=1) produce the same bytes
+    as the single fused kernel: E_next, codes, ranges, offsets, mask, at every
+    bit width and rounding mode, with hub (CTA-path) rows and a row offset.
+    The default split epilogue at d <= 64 computes J on tcgen05 (K6t): the
+    quantized context is still bit-identical (it depends on H only); E_next
+    agrees to fp32 rounding and the mask only differs where J is ~0."""
+    import os
     kgq = _kgq()
     from paper_2212_04540_b200 import functional as F
     rng = np.random.default_rng(d)
@@ -187,14 +190,29 @@ def test_split_layer_bit_identical_to_fused(d):
     for bits in (1, 2, 4, 8):
         for rng_mode, rounding in (("fast", "stochastic"), ("compat", "stochastic"), ("fast", "nearest")):
             cfg = kgq.QuantConfig(bits=bits, rounding=rounding, rng=rng_mode)
-            outs = [F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(5), 3, row_offset=17, split=sp)
-                    for sp in (False, True)]
-            (e0, m0, q0, _), (e1, m1, q1, _) = outs
+            e0, m0, q0, _ = F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(5), 3, row_offset=17,
+                                                 split=False)
+            os.environ["KGQ_EPI_FFMA"] = "1"
+            try:
+                e1, m1, q1, _ = F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(5), 3, row_offset=17,
+                                                     split=True)
+            finally:
+                del os.environ["KGQ_EPI_FFMA"]
             assert torch.equal(e0.view(torch.int32), e1.view(torch.int32)), (bits, rounding, rng_mode)
-            assert torch.equal(q0.codes, q1.codes)
-            assert torch.equal(q0.ranges.view(torch.int32), q1.ranges.view(torch.int32))
-            assert torch.equal(q0.offsets.view(torch.int32), q1.offsets.view(torch.int32))
             assert torch.equal(m0.packed, m1.packed)
+            e2, m2, q2, h2 = F.graph_conv_forward(A, e, th, cfg, kgq.RandomStream(5), 3, row_offset=17,
+                                                  split=True, want_h=True)
+            for qq in (q1, q2):
+                assert torch.equal(q0.codes, qq.codes)
+                assert torch.equal(q0.ranges.view(torch.int32), qq.ranges.view(torch.int32))
+                assert torch.equal(q0.offsets.view(torch.int32), qq.offsets.view(torch.int32))
+            # tcgen05 J (3xTF32) vs fp64 J: within a few fp32 ulps of sum |h||theta|
+            hd, thd = h2.double(), th.double()
+            j64 = hd @ thd
+            scale = hd.abs() @ thd.abs()
+            assert bool(((e2.double() - j64.clamp(min=0)).abs() <= 4e-7 * scale + 1e-30).all()), (bits, rounding)
+            flip = m2.to_bool() != (j64 > 0)
+            assert bool((j64[flip].abs() <= 4e-7 * scale[flip]).all())
 
 
 def test_dequant_gemm_matches_dequantize_then_matmul():
