@@ -3,245 +3,347 @@
 //
 //   g_j = (g_read + g_e) * mask;  dH = g_j . theta^T;  dtheta += Hhat^T . g_j
 //
-// One CTA (512 threads) per SM walks 128-row tiles.  All threads stage the
-// tile: thread t owns row t/4 and column quads 4j + (t&3), forms g_j and the
-// IEEE-dequantized
-// Hhat in registers and writes their 3xTF32 hi/lo splits into shared memory in
-// the K-major interleaved layout (kgq_tc.cuh) three times over:
-//   Ag  (r, k=c)        A of dH       (M = 128 rows, K = 64)
-//   Ah' (i=c, k=r)      A of dtheta   (M = 64,       K = 128 rows)
-//   Bg' (j=c, k=r)      B of dtheta   (N = 64,       K = 128 rows)
-// theta^T's split (B of dH, B(n,k) = theta[n][k]) is staged once per CTA.
-// One elected thread issues 3 x 8 MMAs for dH into TMEM columns [0, 64) and
-// 3 x 16 MMAs accumulating dtheta into columns [64, 128) across the CTA's
-// tiles, then commits to an mbarrier; the 8 warps drain dH with tcgen05.ld.
-// The M = 64 dtheta accumulator lives in TMEM lanes 32q + (0..15) for rows
-// 16q..16q+15 (probed: tools/tc_probe/m64_layout.cu).  Per-CTA dtheta
-// partials are reduced in a fixed order (reduce_partials_bwd_kernel).
-// 3xTF32 = hi*hi + hi*lo + lo*hi with fp32 accumulation: fp32-level accuracy
-// (the reference's BLAS GEMMs are tolerance-compared).
-#include "kgq_tc.cuh"
+// One persistent CTA per SM walks 128-row tiles, warp-specialized and
+// pipelined so that the staging of one tile overlaps the MMAs of the previous:
+//
+// * 16 staging warps in two groups.  Warp w covers TMEM lane quadrant w % 4
+//   (rows 32 (w % 4) .. + 31 of the tile, thread = row) and columns
+//   16 (w / 4) .. + 15.  Group g = (w % 4) / 2 owns rows [64 g, 64 g + 64) of
+//   every tile and its own shared-memory slot.  g_read and g_e arrive by TMA
+//   (one 64-row x 32-column SWIZZLE_128B box per array and column half, per
+//   group, issued one tile ahead as soon as the group has read the previous
+//   one; rows past the end read as zeros); the per-row mask bits, codes, R, Z
+//   come by register prefetch one tile ahead.  A thread reads its row's slice
+//   (LDS.128, conflict-free through the swizzle), forms g_j and the
+//   IEEE-dequantized Hhat, splits both into 3xTF32 hi/lo (hi = x itself, lo =
+//   x - trunc_tf32(x)) and writes
+//     - Hhat hi|lo and g_j hi|lo into its group's slot as MN-major
+//       SWIZZLE_128B_BASE32B tiles (row-major 128-B rows, the layout
+//       kind::tf32 reads MN-major; kgq_tc.cuh b32_off), 16-byte stores; lanes
+//       with bit 2 set write the two halves of each 32-B granule in swapped
+//       order so a quarter-warp's eight stores hit eight distinct bank groups;
+//     - g_j hi|lo into TMEM (tcgen05.st, lane = row): the A operand of dH.
+//   then arrives on its slot's `full` barrier, and drains the previous tile's
+//   dH rows (tcgen05.ld -> 64-B row stores).
+// * 1 MMA warp: per tile, per group slot: dtheta += [Hhat_hi | Hhat_lo]^T .
+//   [g_hi | g_lo] as 8 MMAs M = 128, N = 128, K = 8 (both operands MN-major,
+//   the hi/lo halves stacked along M and N, so one accumulator collects all
+//   four products: hi.hi, hi.lo, lo.hi and lo.lo), commit -> the slot's
+//   `empty` barrier; then dH = g_j . theta^T with A from TMEM (3 passes x 8
+//   MMAs M = 128, N = 64: lo.hi + hi.lo + hi.hi, theta^T split staged once in
+//   SWIZZLE_128B K-major) into a double-buffered TMEM accumulator, commit ->
+//   `dhdone` (which also frees that tile's TMEM A buffer).
+// TMEM (512 columns): dtheta accumulator [0,128), dH buffers [128,192) and
+// [192,256), A buffers (hi 64 | lo 64) [256,384) and [384,512).
+// At the end the four 64x64 quadrants of the dtheta accumulator are summed
+// per CTA in a fixed order; reduce_partials_bwd_kernel (kgq_backward.cu)
+// reduces the per-CTA partials in a fixed order (deterministic).
+// 3xTF32 with fp32 accumulation: fp32-level accuracy (the reference's BLAS
+// GEMMs are tolerance-compared).
+#include "kgq_tma.cuh"
 
 namespace kgq {
 
 constexpr int kTcRows = 128;
 constexpr int kTcD = 64;
-
-// The transposed operands (k = row) use a padded K-quad stride LBO_T = 1040 B
-// (1024 + 16): with thread (row r, column quads 2j+h) the 32 scalar stores of
-// a warp then hit 32 distinct banks.  Ag is written with 128-bit stores.
-constexpr uint32_t kLboT = 1040;
-constexpr uint32_t kLboA = 2080;     // Ag K-quad stride: 2048 + 32 B spreads a row's 4 quarter-threads
-constexpr int kBtcThreads = 512;     // 4 threads per row: 16 warps keep more loads in flight
+constexpr int kBtcThreads = 544;            // 16 staging warps + 1 MMA warp
 struct BwdTcSmem {
-    static constexpr int AG = ((kTcD / 4 - 1) * kLboA + 2048) / 4;          // Ag hi or lo (floats)
-    static constexpr int AT = ((kTcRows / 4 - 1) * kLboT + 1024) / 4;      // Ah'/Bg' hi or lo (floats)
-    static constexpr int TH = kTcD * kTcD;
-    static constexpr size_t bytes = (size_t)(2 * TH + 2 * AG + 4 * AT) * sizeof(float);   // 226.9 KB
+    static constexpr uint32_t SLOT = 64 * 1024;      // one group's 64 rows: Hhi, Hlo, Ghi, Glo (2 x 8 KB each)
+    static constexpr uint32_t TH = 16 * 1024;        // theta split hi or lo (64 x 64 fp32, SW128 K-major)
+    static constexpr uint32_t IN = 32 * 1024;        // one group's TMA stage: g_read, g_e (2 x 8 KB boxes each)
+    static constexpr uint32_t INB = 2 * SLOT + 2 * TH;
+    static constexpr uint32_t BAR = INB + 2 * IN;
+    static constexpr size_t bytes = (size_t)BAR + 128 + 1024;   // + barriers + alignment slack (225.1 KB)
 };
-__device__ __forceinline__ uint32_t toff_t(int c, int r) {   // (row c, k = r), padded K-quad stride
-    return (uint32_t)((r >> 2) * kLboT + (c >> 3) * 128 + (c & 7) * 16 + (r & 3) * 4);
-}
+constexpr uint32_t kTmAcc = 0, kTmDh = 128, kTmA = 256;
 
 template <int BITS>
 __global__ void __launch_bounds__(kBtcThreads, 1)
-layer_backward_tc_kernel(const float *__restrict__ g_read, const float *__restrict__ g_e,
-                         const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
+layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid_constant__ CUtensorMap tm_ge,
+                         int has_gr, int has_ge, const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
                          const float *__restrict__ ranges, const float *__restrict__ offsets,
                          int64_t rows, const float *__restrict__ theta, float *__restrict__ dh,
                          float *__restrict__ partial) {
-    constexpr int M = kTcRows, D = kTcD, RB = D * BITS / 8;
+    constexpr int D = kTcD, M = kTcRows, RB = D * BITS / 8;
     constexpr uint32_t CM = BITS >= 32 ? 0xFFFFFFFFu : (1u << BITS) - 1u;
-    constexpr int NCW = BITS >= 32 ? 1 : 2 * BITS;      // code words per row held in registers
-    extern __shared__ __align__(128) float tsm[];
-    float *th_hi = tsm, *th_lo = tsm + BwdTcSmem::TH;
-    float *ag_hi = tsm + 2 * BwdTcSmem::TH, *ag_lo = ag_hi + BwdTcSmem::AG;
-    float *ah_hi = ag_lo + BwdTcSmem::AG, *ah_lo = ah_hi + BwdTcSmem::AT;
-    float *bg_hi = ah_lo + BwdTcSmem::AT, *bg_lo = bg_hi + BwdTcSmem::AT;
-    __shared__ __align__(8) uint64_t mbar;
-    __shared__ uint32_t tmem_base;
+    constexpr int NCW = BITS >= 32 ? 1 : (16 * BITS + 31) / 32;     // code words of a 16-column slice
+    extern __shared__ uint8_t tsm_raw[];
+    uint8_t *sm = tsm_raw + ((1024u - (tc::smem_u32(tsm_raw) & 1023u)) & 1023u);   // stays a shared-space pointer
+    float *thh = reinterpret_cast<float *>(sm + 2 * BwdTcSmem::SLOT);
+    float *thl = reinterpret_cast<float *>(sm + 2 * BwdTcSmem::SLOT + BwdTcSmem::TH);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + BwdTcSmem::BAR);
+    uint64_t *full = bar, *empty = bar + 2, *dhdone = bar + 4, *dhempty = bar + 6, *ldfull = bar + 8;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 10);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
 
-    // theta^T split: B(n, k) = theta[n][k]
-    for (int i = t; i < D * D; i += kBtcThreads) {
-        const int n = i / D, k = i % D;
-        float hi, lo;
-        tc::split_tf32(__ldg(theta + i), hi, lo);
-        th_hi[tc::tile_off(n, k, D) / 4] = hi;
-        th_lo[tc::tile_off(n, k, D) / 4] = lo;
+    // theta^T split, B of dH: B(n, k) = theta[n][k]
+    {
+        constexpr int PER = (D * D + kBtcThreads - 1) / kBtcThreads;
+        float tv[PER];
+#pragma unroll
+        for (int k = 0; k < PER; k++) tv[k] = t + k * kBtcThreads < D * D ? __ldg(theta + t + k * kBtcThreads) : 0.f;
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const int i = t + k * kBtcThreads;
+            if (i < D * D) {
+                const uint32_t o = tc::sw128_off(i / D, i % D, D) / 4;
+                tc::split_tf32_fast(tv[k], thh[o], thl[o]);
+            }
+        }
     }
-    if (t == 0) tc::mbar_init(&mbar, 1);
-    if (warp == 0) tc::tmem_alloc(&tmem_base, 128);
+    if (t == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(full + i, 256);
+            tc::mbar_init(empty + i, 1);
+            tc::mbar_init(dhdone + i, 1);
+            tc::mbar_init(dhempty + i, 512);
+            tc::mbar_init(ldfull + i, 1);
+        }
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t tmem = tmem_base;
-
-    // staging: thread owns row r = t/4 and the column quads 4j + h (j = 0..3)
-    const int r = t >> 2, h = t & 3;
-    uint32_t phase = 0;
-    bool first = true;
+    const uint32_t tmem = *tmem_slot;
     const int64_t n_tiles = (rows + M - 1) / M;
-    // register prefetch of one tile's inputs (issued while the previous
-    // tile's MMAs run, so the loads overlap the tensor-core work)
-    float4 pa[4], pe[4];
-    float prg = 0.f, pzz = 0.f;
-    uint32_t pm0 = 0u, pm1 = 0u, pcw[NCW];
-    float4 ph[BITS == 32 ? 4 : 1];                       // pass-through: the fp32 H quads
-    auto load = [&](int64_t tl) {
-        const int64_t row = tl * M + r;
-        const bool ok = tl < n_tiles && row < rows;
-        prg = (ok && BITS != 32) ? __ldg(ranges + row) : 0.f;
-        pzz = (ok && BITS != 32) ? __ldg(offsets + row) : 0.f;
-        pm0 = ok ? __ldg(mask + row * 2) : 0u;
-        pm1 = ok ? __ldg(mask + row * 2 + 1) : 0u;
-        if (BITS == 32) {
-            const float4 *h4 = reinterpret_cast<const float4 *>(codes) + row * (D / 4);
+    const int nj = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);   // >= 1 (grid <= n_tiles)
+
+    if (warp == 16) {
+        // ------------------------------ MMA issuer ------------------------------
+        if (lane == 0) {
+            constexpr uint32_t id_th = tc::idesc_tf32_major(128, 128, true, true);
+            constexpr uint32_t id_dh = tc::idesc_tf32(128, 64);
+            const uint32_t sbase = tc::smem_u32(sm);
+            const uint32_t bh = tc::smem_u32(thh), bl = tc::smem_u32(thl);
+            for (int j = 0; j < nj; j++) {
+                for (int g = 0; g < 2; g++) {
+                    tc::mbar_wait(full + g, (uint32_t)(j & 1));
+                    tc::fence_after();
+                    const uint32_t base = sbase + g * BwdTcSmem::SLOT;
 #pragma unroll
-            for (int j = 0; j < (BITS == 32 ? 4 : 1); j++) ph[j] = ok ? __ldg(h4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-            const uint32_t *crow = reinterpret_cast<const uint32_t *>(codes + row * RB);
+                    for (int s = 0; s < 8; s++)
+                        tc::mma_tf32(tmem + kTmAcc, tc::mnmajor_b32_desc(base, s, 64),
+                                     tc::mnmajor_b32_desc(base + 32768, s, 64), id_th, (j | g | s) != 0);
+                    tc::commit(empty + g);
+                }
+                const int b = j & 1;
+                if (j >= 2) {
+                    tc::mbar_wait(dhempty + b, (uint32_t)(((j >> 1) - 1) & 1));
+                    tc::fence_after();
+                }
+                const uint32_t ab = tmem + kTmA + 128u * b, dd = tmem + kTmDh + 64u * b;
 #pragma unroll
-            for (int w = 0; w < NCW; w++) pcw[w] = ok ? __ldg(crow + w) : 0u;
+                for (int p = 0; p < 3; p++) {          // lo.hi, hi.lo, hi.hi
+                    const uint32_t ao = p == 0 ? 64u : 0u;
+                    const uint32_t bs = p == 1 ? bl : bh;
+#pragma unroll
+                    for (int s = 0; s < 8; s++)
+                        tc::mma_tf32_ts(dd, ab + ao + 8u * s, tc::kmajor_sw128_desc(bs, s, D), id_dh, (p | s) != 0);
+                }
+                tc::commit(dhdone + b);
+            }
         }
-        const float4 *gr4 = reinterpret_cast<const float4 *>(g_read + row * D);
-        const float4 *ge4 = reinterpret_cast<const float4 *>(g_e + row * D);
+        __syncwarp();
+    } else {
+        // --------------------------- staging / drain ---------------------------
+        const int q = warp & 3, cq = warp >> 2, g = q >> 1;
+        const int r_tile = 32 * q + lane;            // row within the tile (= TMEM lane)
+        const int r_unit = 32 * (q & 1) + lane;      // row within the group's 64-row unit
+        const int sw = (lane >> 2) & 1;              // granule-half swap (bank spread)
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        float *slot = reinterpret_cast<float *>(sm + g * BwdTcSmem::SLOT);
+        // block offsets (floats) inside the slot: Hhi blocks 0,1; Hlo 2,3; Ghi 4,5; Glo 6,7 (8 KB each)
+        const int blk = cq >> 1;
+        const int cbase = 16 * (cq & 1);             // first column inside the 32-column block
+        float4 pa[4], pe[4];
+        float prg = 0.f, pzz = 0.f;
+        uint32_t pm = 0u, pcw[NCW];
+        float4 ph[BITS == 32 ? 4 : 1];
+        const uint8_t *instage = sm + BwdTcSmem::INB + g * BwdTcSmem::IN;
+        const bool issuer = (warp == 2 * g) && lane == 0;   // first warp of the group
+        const int in_bytes = (has_gr ? 16384 : 0) + (has_ge ? 16384 : 0);
+        auto row_of = [&](int jj) {
+            return ((int64_t)blockIdx.x + (int64_t)jj * gridDim.x) * M + r_tile;
+        };
+        // TMA: the group's 64 rows of tile jj (g_read boxes at +0 / +8 KB, g_e at +16 / +24 KB)
+        auto issue_in = [&](int jj) {
+            const int r0 = (int)(((int64_t)blockIdx.x + (int64_t)jj * gridDim.x) * M + 64 * g);
+            tma::expect_tx(ldfull + g, (uint32_t)in_bytes);
+            if (has_gr) {
+                tma::load_2d(const_cast<uint8_t *>(instage), &tm_gr, 0, r0, ldfull + g);
+                tma::load_2d(const_cast<uint8_t *>(instage) + 8192, &tm_gr, 32, r0, ldfull + g);
+            }
+            if (has_ge) {
+                tma::load_2d(const_cast<uint8_t *>(instage) + 16384, &tm_ge, 0, r0, ldfull + g);
+                tma::load_2d(const_cast<uint8_t *>(instage) + 24576, &tm_ge, 32, r0, ldfull + g);
+            }
+        };
+        // the per-row scalars (and, at b = 32, the raw H slice) by register prefetch
+        auto load_small = [&](int jj) {
+            const int64_t row = row_of(jj);
+            const bool ok = jj < nj && row < rows;
+            prg = (ok && BITS != 32) ? __ldg(ranges + row) : 0.f;
+            pzz = (ok && BITS != 32) ? __ldg(offsets + row) : 0.f;
+            pm = ok ? __ldg(mask + row * 2 + (cq >> 1)) : 0u;        // raw word: bits 16 (cq & 1) ..
+            if constexpr (BITS == 1) {
+                pcw[0] = ok ? (uint32_t)__ldg(reinterpret_cast<const uint16_t *>(codes + row * RB) + cq) : 0u;
+            } else if constexpr (BITS != 32) {
+                const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes + row * RB) + cq * NCW;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            pa[j] = (ok && g_read) ? __ldg(gr4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
-            pe[j] = (ok && g_e) ? __ldg(ge4 + 4 * j + h) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
-    load(blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t row = tile * M + r;
-        const bool ok = row < rows;
-        // ---- 1. stage g_j and Hhat (hi/lo, three layouts) from the prefetched registers ----
-        {
+                for (int w = 0; w < NCW; w++) pcw[w] = ok ? __ldg(cw + w) : 0u;
+            } else {
+                const float4 *h4 = reinterpret_cast<const float4 *>(codes) + row * (D / 4) + 4 * cq;
+#pragma unroll
+                for (int i = 0; i < 4; i++) ph[i] = ok ? __ldg(h4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        auto drain = [&](int jj) {
+            const int b = jj & 1;
+            tc::mbar_wait(dhdone + b, (uint32_t)((jj >> 1) & 1));
+            tc::fence_after();
+            uint32_t v[16];
+            tc::tmem_ld16_nowait(tmem + lane_addr + kTmDh + 64u * b + 16u * cq, v);
+            tc::tmem_ld_wait();
+            const int64_t row = ((int64_t)blockIdx.x + (int64_t)jj * gridDim.x) * M + r_tile;
+            if (row < rows) {
+                float4 *dst = reinterpret_cast<float4 *>(dh + row * D) + 4 * cq;
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                         __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+            }
+            tc::fence_before();
+            tc::mbar_arrive(dhempty + b);
+        };
+        if (issuer) issue_in(0);
+        load_small(0);
+        for (int j = 0; j < nj; j++) {
             const float rg = prg, zz = pzz;
-            // b <= 2: the row's 2^b reconstruction values once (IEEE, lut_entry),
-            // then a select per element instead of the division sequence
+            const uint32_t mw = (pm >> (16 * (cq & 1))) & 0xFFFFu;
+            uint32_t cw[NCW];
+#pragma unroll
+            for (int w = 0; w < NCW; w++) cw[w] = pcw[w];
+            float4 hq4[BITS == 32 ? 4 : 1];
+            if constexpr (BITS == 32) {
+#pragma unroll
+                for (int i = 0; i < 4; i++) hq4[i] = ph[i];
+            }
+            load_small(j + 1);
+            // this tile's g_read / g_e slice from the TMA stage, then the stage is refilled
+            tc::mbar_wait(ldfull + g, (uint32_t)(j & 1));
+            {
+                const int bx = cq >> 1;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const uint32_t o = bx * 8192 + tma::box_off(r_unit, 16 * (cq & 1) + 4 * i);
+                    pa[i] = has_gr ? *reinterpret_cast<const float4 *>(instage + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    pe[i] = has_ge ? *reinterpret_cast<const float4 *>(instage + 16384 + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            tma::named_sync(1 + g, 256);
+            if (issuer && j + 1 < nj) {
+                tc::fence_proxy_async();           // generic reads of the stage before the async-proxy refill
+                issue_in(j + 1);
+            }
+            // b <= 2: the row's 2^b IEEE dequantized values (K2's arithmetic) once,
+            // then a select per element; b = 4 / 8: Hhat = Z + c * (R / B) with one
+            // FFMA per element (a GEMM operand, <= 2 ulp from K2's value).
+            const float rb = __fmul_rn(rg, 1.0f / (float)((1u << (BITS < 32 ? BITS : 1)) - 1u));
             float lut[BITS <= 2 ? (1 << BITS) : 1];
             if constexpr (BITS <= 2) {
 #pragma unroll
                 for (int c = 0; c < (1 << BITS); c++) lut[c] = lut_entry<BITS>(rg, zz, c);
             }
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const float av[4] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w}, ev[4] = {pe[j].x, pe[j].y, pe[j].z, pe[j].w};
-                float gh[4], gl[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const int c = 16 * j + 4 * h + q;
-                    // g = g_read + g_e in the reference's routing order (tape.py:204-209)
-                    const float g = (g_read && g_e) ? __fadd_rn(av[q], ev[q]) : (g_read ? av[q] : ev[q]);
-                    const uint32_t mw = c < 32 ? pm0 : pm1;
-                    const float gj = __fmul_rn(g, ((mw >> (c & 31)) & 1u) ? 1.0f : 0.0f);
-                    const int bp = c * BITS;
-                    const uint32_t code = BITS == 32 ? 0u : (pcw[(bp >> 5) % NCW] >> (bp & 31)) & CM;
-                    float hv;
-                    if (BITS == 32) {
-                        const float4 hq = ph[BITS == 32 ? j : 0];
-                        hv = q == 0 ? hq.x : q == 1 ? hq.y : q == 2 ? hq.z : hq.w;
-                    } else if (BITS == 1) hv = code ? lut[BITS <= 2 ? 1 : 0] : lut[0];
-                    else if (BITS == 2) hv = (code & 2u) ? ((code & 1u) ? lut[BITS == 2 ? 3 : 0] : lut[BITS == 2 ? 2 : 0])
-                                                     : ((code & 1u) ? lut[BITS <= 2 ? 1 : 0] : lut[0]);
-                    else hv = lut_entry<BITS <= 8 ? BITS : 8>(rg, zz, (int)code);
-                    hv = ok ? hv : 0.0f;
-                    float hh, hl;
-                    tc::split_tf32(gj, gh[q], gl[q]);
-                    tc::split_tf32(hv, hh, hl);
-                    const uint32_t ob = toff_t(c, r) / 4;              // Ah', Bg' (c, k=r)
-                    bg_hi[ob] = gh[q]; bg_lo[ob] = gl[q];
-                    ah_hi[ob] = hh; ah_lo[ob] = hl;
-                }
-                const uint32_t oa = ((4 * j + h) * kLboA + (r >> 3) * 128 + (r & 7) * 16) / 4;   // Ag (r, quad)
-                *reinterpret_cast<float4 *>(ag_hi + oa) = make_float4(gh[0], gh[1], gh[2], gh[3]);
-                *reinterpret_cast<float4 *>(ag_lo + oa) = make_float4(gl[0], gl[1], gl[2], gl[3]);
-            }
-        }
-        tc::fence_proxy_async();
-        __syncthreads();
-        // ---- 2. MMAs: dH (cols 0..63), dtheta accumulate (cols 64..127) ----
-        if (t == 0) {
+            // slot free (dtheta MMAs of the previous tile done), TMEM A buffer free (dH of tile j-2 done)
+            if (j >= 1) tc::mbar_wait(empty + g, (uint32_t)((j - 1) & 1));
+            const int b = j & 1;
+            if (j >= 2) tc::mbar_wait(dhdone + b, (uint32_t)(((j >> 1) - 1) & 1));
             tc::fence_after();
-            {   // dH: A = Ag (K-quad stride kLboA), B = theta^T split (standard stride)
-                constexpr uint32_t idA = tc::idesc_tf32(M, D), LBO_B = (D / 8) * 128;
-                const uint32_t gah = tc::smem_u32(ag_hi), gal = tc::smem_u32(ag_lo);
-                const uint32_t tbh = tc::smem_u32(th_hi), tbl = tc::smem_u32(th_lo);
-                uint32_t acc0 = 0;
 #pragma unroll
-                for (int pass = 0; pass < 3; pass++) {
-                    const uint32_t sa = pass == 0 ? gal : gah;
-                    const uint32_t sb = pass == 1 ? tbl : tbh;
+            for (int pr = 0; pr < 2; pr++) {          // chunk pairs (2 pr, 2 pr + 1): 8 columns
+                float gh[8], gl[8], hh[8], hl[8];
 #pragma unroll
-                    for (int st = 0; st < D / 8; st++) {
-                        tc::mma_tf32(tmem, tc::smem_desc(sa + 2 * st * kLboA, kLboA, 128),
-                                     tc::smem_desc(sb + 2 * st * LBO_B, LBO_B, 128), idA, acc0);
-                        acc0 = 1u;
+                for (int u = 0; u < 2; u++) {
+                    const int i = 2 * pr + u;
+                    const float av[4] = {pa[i].x, pa[i].y, pa[i].z, pa[i].w};
+                    const float ev[4] = {pe[i].x, pe[i].y, pe[i].z, pe[i].w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int c = 4 * i + e;                 // column inside the 16-column slice
+                        // g = g_read + g_e in the reference's routing order (tape.py:204-209)
+                        const float gv = (has_gr && has_ge) ? __fadd_rn(av[e], ev[e]) : (has_gr ? av[e] : ev[e]);
+                        const float gj = ((mw >> c) & 1u) ? gv : 0.0f;   // relu backward (sign of 0 immaterial: GEMM operand)
+                        float hv;
+                        if constexpr (BITS == 32) {
+                            const float4 hq = hq4[BITS == 32 ? i : 0];
+                            hv = e == 0 ? hq.x : e == 1 ? hq.y : e == 2 ? hq.z : hq.w;
+                        } else {
+                            const int bp = c * BITS;
+                            const uint32_t code = (cw[(bp >> 5) % NCW] >> (bp & 31)) & CM;
+                            if constexpr (BITS == 1) hv = code ? lut[BITS <= 2 ? 1 : 0] : lut[0];
+                            else if constexpr (BITS == 2)
+                                hv = (code & 2u) ? ((code & 1u) ? lut[BITS == 2 ? 3 : 0] : lut[BITS == 2 ? 2 : 0])
+                                                 : ((code & 1u) ? lut[BITS <= 2 ? 1 : 0] : lut[0]);
+                            else hv = __fmaf_rn(__uint2float_rn(code), rb, zz);
+                        }
+                        tc::split_tf32_fast(gj, gh[4 * u + e], gl[4 * u + e]);
+                        tc::split_tf32_fast(hv, hh[4 * u + e], hl[4 * u + e]);
                     }
                 }
-            }
-            constexpr uint32_t LBO = kLboT;                          // padded K-quad stride
-            constexpr uint32_t idesc = tc::idesc_tf32(D, D);         // M = 64, N = 64
-            const uint32_t sah = tc::smem_u32(ah_hi), sal = tc::smem_u32(ah_lo);
-            const uint32_t sbh = tc::smem_u32(bg_hi), sbl = tc::smem_u32(bg_lo);
-            uint32_t acc = first ? 0u : 1u;
+                // smem: logical chunk (2 pr + u) ^ sw at instruction u
 #pragma unroll
-            for (int pass = 0; pass < 3; pass++) {
-                const uint32_t sa = pass == 0 ? sal : sah;
-                const uint32_t sb = pass == 1 ? sbl : sbh;
-#pragma unroll
-                for (int s = 0; s < M / 8; s++) {
-                    tc::mma_tf32(tmem + 64, tc::smem_desc(sa + 2 * s * LBO, LBO, 128),
-                                 tc::smem_desc(sb + 2 * s * LBO, LBO, 128), idesc, acc);
-                    acc = 1u;
+                for (int u = 0; u < 2; u++) {
+#ifdef KGQ_BWD_NOSWAP
+                    const int src = u;
+#else
+                    const int src = u ^ sw;                        // which chunk's registers (0/1 of the pair)
+#endif
+                    const int col = cbase + 4 * (2 * pr + src);    // its first column in the block
+                    const uint32_t o = tc::b32_off(r_unit, col, 64) / 4;
+                    auto pick = [&](const float *v) {
+                        return make_float4(src ? v[4] : v[0], src ? v[5] : v[1], src ? v[6] : v[2], src ? v[7] : v[3]);
+                    };
+                    *reinterpret_cast<float4 *>(slot + (0 + blk) * 2048 + o) = pick(hh);
+                    *reinterpret_cast<float4 *>(slot + (2 + blk) * 2048 + o) = pick(hl);
+                    *reinterpret_cast<float4 *>(slot + (4 + blk) * 2048 + o) = pick(gh);
+                    *reinterpret_cast<float4 *>(slot + (6 + blk) * 2048 + o) = pick(gl);
                 }
+                // TMEM A: g_j hi at columns 16 cq + 8 pr, lo 64 further
+                const uint32_t ta = tmem + lane_addr + kTmA + 128u * b + 16u * cq + 8u * pr;
+                tc::tmem_st8(ta, gh);
+                tc::tmem_st8(ta + 64u, gl);
             }
-            tc::commit(&mbar);
+            tc::tmem_st_wait();
+            tc::fence_proxy_async();
+            tc::fence_before();
+            tc::mbar_arrive(full + g);
+            if (j >= 1) drain(j - 1);
         }
-        first = false;
-        load(tile + gridDim.x);                     // next tile's inputs, in flight during the MMAs
-        tc::mbar_wait(&mbar, phase);
-        phase ^= 1u;
-        tc::fence_after();
-        // ---- 3. drain dH: warp w < 8 -> lanes 32*(w%4).., columns 32*(w/4).. ----
-        if (warp < 8) {
-            const int q = warp & 3, cb = (warp >> 2) * 32;
-            float v[32];
-            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
-            const int64_t orow = tile * M + 32 * q + lane;
-            if (orow < rows) {
-                float4 *dst = reinterpret_cast<float4 *>(dh + orow * D + cb);
-#pragma unroll
-                for (int j = 0; j < 8; j++) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-        }
-        tc::fence_before();
-        __syncthreads();
+        drain(nj - 1);
     }
-    // ---- dtheta partial of this CTA: rows i = 16q + l live in lanes 32q + l ----
+
+    // ---- dtheta partial of this CTA: sum of the accumulator's four 64x64 quadrants ----
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    float *red = reinterpret_cast<float *>(sm);            // [128][65] (slot memory is free now; padded rows)
     if (warp < 4) {
-        float *dst = partial + (int64_t)blockIdx.x * D * D;
+        float v0[32], v1[32];
 #pragma unroll
         for (int cb = 0; cb < 64; cb += 32) {
-            float v[32];
-            if (first) {
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + kTmAcc + cb, v0);
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + kTmAcc + 64 + cb, v1);
 #pragma unroll
-                for (int j = 0; j < 32; j++) v[j] = 0.0f;     // no tile: zero partial
-            } else {
-                tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 64u + (uint32_t)cb, v);
-            }
-            if (lane < 16) {
-                float4 *o = reinterpret_cast<float4 *>(dst + (16 * warp + lane) * D + cb);
-#pragma unroll
-                for (int j = 0; j < 8; j++) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
+            for (int c = 0; c < 32; c++) red[(32 * warp + lane) * 65 + cb + c] = __fadd_rn(v0[c], v1[c]);
         }
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_free(tmem, 128);
+    float *dst = partial + (int64_t)blockIdx.x * D * D;
+    for (int i = t; i < D * D; i += kBtcThreads)
+        dst[i] = __fadd_rn(red[(i / D) * 65 + i % D], red[(i / D + 64) * 65 + i % D]);
+    if (warp == 0) tc::tmem_free(tmem, 512);
 }
 
 }  // namespace kgq
@@ -254,6 +356,12 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
                                  int64_t rows, int32_t bits, const float *theta, float *dh,
                                  float *partial, int grid, cudaStream_t s) {
     static bool attr[33] = {false};
+    CUtensorMap tgr, tge;
+    const float *any = g_read ? g_read : g_e;
+    if (!tma::make_rowmajor_f32(&tgr, g_read ? g_read : any, (uint64_t)rows, kTcD, 64) ||
+        !tma::make_rowmajor_f32(&tge, g_e ? g_e : any, (uint64_t)rows, kTcD, 64))
+        return KGQ_ERR_CUDA;
+    const int hr = g_read ? 1 : 0, he = g_e ? 1 : 0;
 #define KGQ_BTC(B) do {                                                                            \
         if (!attr[B]) {                                                                            \
             cudaError_t e = cudaFuncSetAttribute(layer_backward_tc_kernel<B>,                        \
@@ -262,7 +370,7 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
             if (e != cudaSuccess) return kgq_set_cuda_error(e);                                    \
             attr[B] = true;                                                                        \
         }                                                                                          \
-        layer_backward_tc_kernel<B><<<grid, kBtcThreads, BwdTcSmem::bytes, s>>>(g_read, g_e, mask, codes, \
+        layer_backward_tc_kernel<B><<<grid, kBtcThreads, BwdTcSmem::bytes, s>>>(tgr, tge, hr, he, mask, codes, \
                                                                         ranges, offsets, rows, theta, dh, partial); \
     } while (0)
     switch (bits) {
