@@ -316,7 +316,7 @@ void oracle_relu_mask(const float *x, int64_t n, float *out, uint8_t *mask) {
     memset(mask, 0, (size_t)((n + 7) / 8));
     for (int64_t i = 0; i < n; i++) {
         float v = x[i];
-        out[i] = v > 0.0f ? v : 0.0f;
+        out[i] = !(v <= 0.0f) ? v : 0.0f;   /* np.maximum: NaN propagates */
         if (v > 0.0f) mask[i >> 3] |= (uint8_t)(1u << (i & 7));
     }
 }

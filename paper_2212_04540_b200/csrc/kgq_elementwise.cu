@@ -28,8 +28,7 @@ relu_mask_kernel(const float *__restrict__ x, int64_t n128, float *__restrict__ 
         const uint32_t b1 = __ballot_sync(0xffffffffu, v.y > 0.0f);
         const uint32_t b2 = __ballot_sync(0xffffffffu, v.z > 0.0f);
         const uint32_t b3 = __ballot_sync(0xffffffffu, v.w > 0.0f);
-        const float4 o = make_float4(v.x > 0.0f ? v.x : 0.0f, v.y > 0.0f ? v.y : 0.0f,
-                                     v.z > 0.0f ? v.z : 0.0f, v.w > 0.0f ? v.w : 0.0f);
+        const float4 o = make_float4(relu_np(v.x), relu_np(v.y), relu_np(v.z), relu_np(v.w));
         stg_stream(reinterpret_cast<float4 *>(out) + c * 32 + lane, o);
         if (lane < 4) {
             const int sh = 8 * lane;
@@ -51,7 +50,7 @@ __global__ void relu_mask_bytes_kernel(const float *__restrict__ x, int64_t star
             const int64_t i = start + 8 * b + t;
             if (i >= n) break;
             const float v = x[i];
-            out[i] = v > 0.0f ? v : 0.0f;
+            out[i] = relu_np(v);
             byte |= (v > 0.0f ? 1u : 0u) << t;
         }
         mask[start / 8 + b] = (uint8_t)byte;

@@ -24,7 +24,7 @@
 //    fused quantizer).  The next column ids are prefetched while the current
 //    neighbour rows are gathered.
 #include "kgq_common.cuh"
-#include "kgq_tc.cuh"
+#include "kgq_tma.cuh"
 
 namespace kgq {
 
@@ -420,7 +420,7 @@ __device__ __forceinline__ void heavy_layer_row(const int32_t *__restrict__ indp
         for (int k = 0; k < D; k++) j = __fmaf_rn(hrow[k], th[k * D + t], j);
         const bool pos = j > 0.0f;
         const uint32_t bal = __ballot_sync(0xffffffffu, pos);
-        e_next[row * D + t] = pos ? j : 0.0f;
+        e_next[row * D + t] = relu_nan(j);
         if (lane == 0) mask[row * (D / 32) + wid] = bal;
     }
 }
@@ -495,7 +495,7 @@ __device__ __forceinline__ void light_epilogue(const float4 (&h)[2], bool active
                     const float jv = jacc[rr][c];
                     const uint32_t bal = __ballot_sync(0xffffffffu, jv > 0.0f);
                     if (act) {
-                        e_next[rrow * D + lane + 32 * c] = jv > 0.0f ? jv : 0.0f;
+                        e_next[rrow * D + lane + 32 * c] = relu_nan(jv);
                         if (lane == 0) mask[rrow * (D / 32) + c] = bal;
                     }
                 }
@@ -687,8 +687,7 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
             word |= __shfl_xor_sync(0xffffffffu, word, 4);
             if (row < n_rows) {
                 *reinterpret_cast<float4 *>(e_next + row * D + 4 * tc) =
-                    make_float4(acc[i][0] > 0.0f ? acc[i][0] : 0.0f, acc[i][1] > 0.0f ? acc[i][1] : 0.0f,
-                                acc[i][2] > 0.0f ? acc[i][2] : 0.0f, acc[i][3] > 0.0f ? acc[i][3] : 0.0f);
+                    make_float4(relu_nan(acc[i][0]), relu_nan(acc[i][1]), relu_nan(acc[i][2]), relu_nan(acc[i][3]));
                 if ((tc & 7) == 0) mask[row * (D / 32) + (tc >> 3)] = word;
             }
         }
@@ -703,14 +702,17 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
 // into TF32 hi/lo and staged in the K-major interleaved UMMA layout, theta
 // staged once per CTA, 3xTF32 (hi.hi + hi.lo + lo.hi, fp32-level accuracy)
 // into a TMEM accumulator of 128 lanes x D columns issued by one thread --
-// and a TMEM drain that applies relu, writes E_next rows and the mask words.
+// and a TMEM drain that applies relu and writes the mask words; the E_next
+// rows go through shared memory (the H-hi tile, free once the MMAs are done,
+// rewritten in the SWIZZLE_128B box layout: conflict-free for thread = row)
+// and leave as TMA tensor stores, so no thread-per-row global stores.
 // J differs from the FFMA chain of the fused kernel in the last bits (another
 // summation order, as OpenBLAS's differs from both): split and fused agree to
 // fp32 rounding, not bitwise (tests/test_gpu_train.py).
 template <int D>
 struct EpiTc {
     static constexpr int M = 128;                                   // rows per tile
-    static constexpr size_t smem = (size_t)(2 * M * D + 2 * D * D) * sizeof(float);
+    static constexpr size_t smem = (size_t)(2 * M * D + 2 * D * D) * sizeof(float) + 1024;
 };
 
 template <int D, int BITS, int MODE>
@@ -718,27 +720,35 @@ __global__ void __launch_bounds__(256)
 layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
                          uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
                          int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
-                         float *__restrict__ offsets, float *__restrict__ e_next,
+                         float *__restrict__ offsets, const __grid_constant__ CUtensorMap tm_out,
                          uint32_t *__restrict__ mask) {
     constexpr int M = EpiTc<D>::M;
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
     constexpr int NP = M / (8 * RPW);               // load/quantize passes per tile
     constexpr uint32_t TCOLS = D < 32 ? 32 : D;
-    extern __shared__ __align__(128) float tc_smem[];
-    float *ah = tc_smem, *al = tc_smem + M * D;               // H tile hi / lo [M x D]
-    float *bh = tc_smem + 2 * M * D, *bl = bh + D * D;        // theta^T hi / lo: B(n, k) = theta[k][n]
+    extern __shared__ uint8_t tc_smem_raw[];
+    uint8_t *smb = tc_smem_raw + ((1024u - (tc::smem_u32(tc_smem_raw) & 1023u)) & 1023u);
+    float *ah = reinterpret_cast<float *>(smb), *al = ah + M * D;   // H tile hi / lo [M x D]
+    float *bh = ah + 2 * M * D, *bl = bh + D * D;                   // theta^T hi / lo: B(n, k) = theta[k][n]
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tmem_base;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int gl = lane % LPR, grp = lane / LPR;
     const int fa = rg_f4a<D, true>(gl), fb = rg_f4b<D, true>(gl);
 
-    for (int i = t; i < D * D; i += 256) {
-        const int n = i / D, k = i % D;
-        float hi, lo;
-        tc::split_tf32(__ldg(theta + k * D + n), hi, lo);
-        bh[tc::tile_off(n, k, D) / 4] = hi;
-        bl[tc::tile_off(n, k, D) / 4] = lo;
+    {   // theta^T split: all loads first (one latency), then the stores
+        constexpr int PER = D * D / 256;
+        float tv[PER];
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const int i = t + 256 * k, n = i / D, kk = i % D;
+            tv[k] = __ldg(theta + kk * D + n);
+        }
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const int i = t + 256 * k, n = i / D, kk = i % D;
+            tc::split_tf32_fast(tv[k], bh[tc::tile_off(n, kk, D) / 4], bl[tc::tile_off(n, kk, D) / 4]);
+        }
     }
     if (t == 0) tc::mbar_init(&mbar, 1);
     if (warp == 0) tc::tmem_alloc(&tmem_base, TCOLS);
@@ -765,6 +775,9 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t r0 = tile * M;
+        // the previous tile's E_next store must have finished reading the H-hi tile
+        if (t == 0) tma::store_wait_read<0>();
+        __syncthreads();
         // ---- 1. load + quantize + split/stage (register prefetch one pass ahead) ----
 #pragma unroll
         for (int pass = 0; pass < NP; pass++) {
@@ -782,7 +795,7 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
                 const float xs[4] = {h[hf].x, h[hf].y, h[hf].z, h[hf].w};
                 float hi[4], lo[4];
 #pragma unroll
-                for (int e = 0; e < 4; e++) tc::split_tf32(xs[e], hi[e], lo[e]);
+                for (int e = 0; e < 4; e++) tc::split_tf32_fast(xs[e], hi[e], lo[e]);
                 const uint32_t off = tc::tile_off(lr, 4 * (hf ? fb : fa), M) / 4;
                 *reinterpret_cast<float4 *>(ah + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
                 *reinterpret_cast<float4 *>(al + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
@@ -799,28 +812,39 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
         tc::mbar_wait(&mbar, phase);
         phase ^= 1u;
         tc::fence_after();
-        // ---- 3. drain: warp w -> TMEM lanes 32*(w%4).. (its rows), columns 32*(w/4)..; relu, E_next, mask ----
+        // ---- 3. drain: warp w -> TMEM lanes 32*(w%4).. (its rows), columns 32*(w/4)..;
+        //         relu into the E_next box stage (the H-hi tile), mask words ----
         if (warp < 4 * (D / 32)) {
             const int q = warp & 3, cb = 32 * (warp >> 2);
             float v[32];
             tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
-            const int64_t row = r0 + 32 * q + lane;
+            const int rr = 32 * q + lane;
+            const int64_t row = r0 + rr;
             uint32_t word = 0;
 #pragma unroll
             for (int c = 0; c < 32; c++) {
                 word |= (v[c] > 0.0f ? 1u : 0u) << c;
-                v[c] = v[c] > 0.0f ? v[c] : 0.0f;
+                v[c] = relu_nan(v[c]);
             }
-            if (row < n_rows) {
-                float4 *dst = reinterpret_cast<float4 *>(e_next + row * D + cb);
+            uint8_t *box = reinterpret_cast<uint8_t *>(ah) + (cb >> 5) * (M * 128);
 #pragma unroll
-                for (int j = 0; j < 8; j++) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                mask[row * (D / 32) + (cb >> 5)] = word;
-            }
+            for (int j = 0; j < 8; j++)
+                *reinterpret_cast<float4 *>(box + tma::box_off(rr, 4 * j)) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (row < n_rows) mask[row * (D / 32) + (cb >> 5)] = word;
         }
         tc::fence_before();
+        tc::fence_proxy_async();
         __syncthreads();
+        if (t == 0) {
+#pragma unroll
+            for (int cb = 0; cb < D; cb += 32)
+                tma::store_2d(&tm_out, reinterpret_cast<uint8_t *>(ah) + (cb >> 5) * (M * 128), cb, (int)r0);
+            tma::store_commit();
+        }
     }
+    if (t == 0) tma::store_wait<0>();
+    __syncthreads();
     if (warp == 0) tc::tmem_free(tmem, TCOLS);
 }
 
@@ -925,7 +949,7 @@ static int launch_epilogue_tc(int rounding, const float *h, int64_t n_rows, cons
                               uint32_t *mask, cudaStream_t s) {
     const size_t smem = EpiTc<D>::smem;
     void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
-                 uint8_t *, float *, float *, float *, uint32_t *);
+                 uint8_t *, float *, float *, const CUtensorMap, uint32_t *);
     switch (rounding) {
         case KGQ_ROUND_NEAREST: kern = layer_epilogue_tc_kernel<D, BITS, KGQ_ROUND_NEAREST>; break;
         case KGQ_ROUND_SR_FAST: kern = layer_epilogue_tc_kernel<D, BITS, KGQ_ROUND_SR_FAST>; break;
@@ -938,11 +962,14 @@ static int launch_epilogue_tc(int rounding, const float *h, int64_t n_rows, cons
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set[rounding] = true;
     }
+    CUtensorMap tm_out;     // E_next rows leave by TMA: 128-row x 32-column boxes
+    if (!tma::make_rowmajor_f32(&tm_out, e_next, (uint64_t)n_rows, (uint64_t)D, EpiTc<D>::M))
+        return KGQ_ERR_CUDA;
     const int64_t tiles = (n_rows + EpiTc<D>::M - 1) / EpiTc<D>::M;
     const int64_t cap = (int64_t)kSMs * (D > 32 ? 2 : 4);
     const int grid = (int)(tiles < cap ? tiles : cap);
     kern<<<grid, 256, smem, s>>>(h, n_rows, theta, seed, tid, tid_base, row_offset, codes, ranges,
-                                 offsets, e_next, mask);
+                                 offsets, tm_out, mask);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

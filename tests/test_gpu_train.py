@@ -865,7 +865,11 @@ def test_lastfm_one_epoch_matches_reference_run(bits, rng_mode):
     _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q), TrainConfig(epochs=1, quant=q), graphs=True)
     assert rep["memory"]["activation_bytes_peak"] == ref["memory"]["activation_bytes_peak"]
     assert rep["memory"]["fp32_equivalent_bytes"] == ref["memory"]["fp32_equivalent_bytes"]
-    assert rep["loss_curve"][0] == pytest.approx(ref["loss_curve"][0], rel=1e-2)
+    # fp32 (b = 32): two valid fp32 summation orders of our own (FFMA-chain vs
+    # tcgen05 J, tools/fp32_path_divergence.py) end this epoch up to ~2 % apart
+    # in loss, so the bound is the measured spread; INT2's noise dominates
+    # that and keeps 1 %.
+    assert rep["loss_curve"][0] == pytest.approx(ref["loss_curve"][0], rel=2.5e-2 if bits == 32 else 1e-2)
     assert abs(rep["metrics"]["recall_at_20"] - ref["recall_at_20"]) <= 0.005
     assert abs(rep["metrics"]["ndcg_at_20"] - ref["ndcg_at_20"]) <= 0.005
 
@@ -876,8 +880,9 @@ def _ulp_rel(a, b):
     return float(np.abs(a.astype(np.float64) - b.astype(np.float64)).max()) / s if s else 0.0
 
 
+@pytest.mark.parametrize("epilogue", ["tcgen05", "ffma"])
 @pytest.mark.parametrize("bits", [32, 2])
-def test_lastfm_step_level_pin(bits):
+def test_lastfm_step_level_pin(bits, epilogue, monkeypatch):
     """BASELINE configs[2] step by step against the reference's own loop
     (tests/golden/lastfm_steps.npz, datasets/record_reference_steps.py): same
     init, batches and (bits 2) the reference's noise stream.  Step 1's loss
@@ -893,6 +898,10 @@ def test_lastfm_step_level_pin(bits):
     path = os.path.join(golden_io.GOLDEN, "lastfm_steps.npz")
     if not os.path.exists(path):
         pytest.skip("lastfm_steps.npz not recorded")
+    # the split-layer epilogue computes J = H . theta either on the tensor cores
+    # (K6t, default: 3xTF32, tensor-core accumulation order) or as the FFMA
+    # ascending-k chain (KGQ_EPI_FFMA=1, read per launch)
+    monkeypatch.setenv("KGQ_EPI_FFMA", "1" if epilogue == "ffma" else "0")
     z = np.load(path)
     pre = f"b{bits}_"
     n_steps = int(z["n_steps"])
@@ -936,18 +945,23 @@ def test_lastfm_step_level_pin(bits):
         report[f"s{c}_E0rows_maxabs"] = float(np.abs(er).max())
         report[f"s{c}_E0rows_frac_gt_1e-6"] = float(np.mean(np.abs(er) > 1e-6))
         report[f"s{c}_E0_sum_gap"] = float(abs(e.astype(np.float64).sum() - z[pre + f"s{c}_E0_sum"][0]))
-    print(f"PIN b{bits}", {k: float(f"{v:.3g}") for k, v in report.items()})
-    # Observed on B200 (round 2), b32 / b2: step-1 loss gap 0 / 0, step-1
-    # gradients 6.4e-6 / 6.2e-6 of max, step-1 params at ulp level (theta
-    # 6.9e-8 rel, E0 rows 9.3e-10 abs), step 10 theta 2.5e-6 / 2.2e-6 rel and
-    # E0 rows 6.1e-7 / 3.2e-6 abs, loss gap over 100 steps 1.6e-6 / 7.1e-6;
-    # by step 100 Adam has amplified the last-bit noise to ~1e-3 abs in E0.
-    # Bounds ~3x the observed maxima:
+    print(f"PIN b{bits} {epilogue}", {k: float(f"{v:.3g}") for k, v in report.items()})
+    # Observed on B200 (round 2), b32 / b2.  FFMA epilogue: step-1 loss gap
+    # 0 / 0, step-1 gradients 6.4e-6 / 6.2e-6 of max, step-1 params at ulp
+    # level (theta 6.9e-8 rel, E0 rows 9.3e-10 abs), step 10 theta 2.5e-6 /
+    # 2.2e-6 rel and E0 rows 6.1e-7 / 3.2e-6 abs, loss gap over 100 steps
+    # 1.6e-6 / 7.1e-6.  tcgen05 epilogue: step-1 gradients 4.2e-6 / 6.8e-6,
+    # step-1 theta 3.4e-7 / 2.4e-7 rel (a few ulp: the tensor core's
+    # accumulation order), E0 rows 1.2e-8 abs, step 10 theta 2.8e-6 / 7.7e-6
+    # and E0 rows 6.1e-7 / 3.2e-6, loss gap 1.5e-7 / 9.5e-6.  By step 100
+    # Adam has amplified the last-bit noise to ~1e-3 abs in E0 either way.
+    # Bounds ~3x the observed maxima of each path:
+    tc = epilogue == "tcgen05"
     assert report["loss_gap_step1"] <= 1e-6
     assert report["grad1_rel"] <= 2e-5
-    assert report["s1_theta_rel"] <= 2e-7
-    assert report["s1_E0rows_maxabs"] <= 3e-9
-    assert report["s10_theta_rel"] <= 1e-5
+    assert report["s1_theta_rel"] <= (1e-6 if tc else 2e-7)
+    assert report["s1_E0rows_maxabs"] <= (4e-8 if tc else 3e-9)
+    assert report["s10_theta_rel"] <= (2.5e-5 if tc else 1e-5)
     assert report["s10_E0rows_maxabs"] <= 1e-5
     assert report["loss_gap_max"] <= 3e-5
 
@@ -1020,3 +1034,35 @@ def test_topk_rows_beyond_kernel_k_matches_stable_argsort():
         assert np.array_equal(got[:, :min(k, 300)], ref), k
         if k > 300:
             assert (got[:, 300:] == -1).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", [False, True])
+def test_relu_and_layer_epilogue_special_values(split):
+    """np.maximum(x, 0) semantics (tensorops.py:90) in K5 and in the layer
+    epilogues: -0.0 -> +0.0, NaN propagated, +inf kept, mask bit x > 0."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import functional as F
+    from oracle import oracle as orc
+    x = np.array([[-0.0, 0.0, np.nan, -np.nan, np.inf, -np.inf, -1.0, 2.0,
+                   1e-45, -1e-45, 3.0e38, -3.0e38, 0.5, -0.5, np.nan, 7.0] * 4] * 3, dtype=np.float32)
+    out, mask = kgq.relu(torch.from_numpy(x).cuda())
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), np.maximum(x, 0).view(np.uint32))
+    assert np.array_equal(mask.packed.cpu().numpy(), np.packbits((x > 0).reshape(-1), bitorder="little"))
+    # a theta column of +inf / NaN makes J non-finite: relu must keep it non-finite
+    ds = D.reference_dataset("default")
+    adj = D.build_adjacency(ds, "cuda")
+    e = torch.randn(adj.shape[0], 64, device="cuda")
+    th = torch.randn(64, 64, device="cuda") / 8
+    th[:, 3] = float("inf")
+    th[:, 9] = float("nan")
+    e_next, msk, _, _ = F.graph_conv_forward(adj, e, th, kgq.QuantConfig(bits=2), kgq.RandomStream(0), 1,
+                                             split=split)
+    en = e_next.cpu().numpy()
+    assert np.isnan(en[:, 9]).all()
+    assert not np.isfinite(en[:, 3]).all() or np.isnan(en[:, 3]).any()
+    assert np.isfinite(np.delete(en, [3, 9], axis=1)).all()
+
+
+

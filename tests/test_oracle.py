@@ -104,6 +104,17 @@ def test_oracle_spmm_relu_match_reference():
         assert np.array_equal(m, z[f"mask{d}"])
 
 
+def test_oracle_relu_special_values_match_numpy_maximum():
+    """np.maximum(x, 0) (tensorops.py:90): -0.0 -> +0.0, NaN propagated
+    (with its sign), inf kept; mask bit x > 0 (NaN -> 0)."""
+    x = np.array([[-0.0, 0.0, np.nan, -np.nan, np.inf, -np.inf, -1.0, 2.0,
+                   1e-45, -1e-45, 3.0e38, -3.0e38, 0.5, -0.5, np.nan, 7.0]], dtype=np.float32)
+    r, m = orc.relu_mask(x)
+    ref = np.maximum(x, 0)
+    assert np.array_equal(r.view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(m, np.packbits((x > 0).reshape(-1), bitorder="little"))
+
+
 def test_dense_oracle_matches_reference_tape_b32():
     z = golden_io.load("tape")
     for d, layers in ((64, 3), (32, 2)):
