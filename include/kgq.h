@@ -274,6 +274,24 @@ KGQ_API int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, 
 KGQ_API int kgq_topk_rows_f32(const float *scores, int64_t n_rows, int64_t n_cols, int64_t ld, int32_t k,
                       int32_t *out_idx, void *stream);
 
+/* Fused evaluation scoring + Top-K (K12; replaces train.py:121-160's score
+ * block + per-user argsort): for each of n_users rows users[i] of readout
+ * (n x d fp32, row-major), the k best items of readout[users[i]] . item_emb^T
+ * (item_emb: n_items x d fp32) after setting the user's train positives
+ * train_items[train_start[i] .. train_end[i]) (sorted ascending) to -inf,
+ * best first, in kgq_topk_rows_f32's order (descending score, ties by
+ * ascending index, -0.0 == +0.0, -inf then NaN last); -1 past n_items.
+ * Scores are 3xTF32 tensor-core dot products (fp32-level); no score matrix is
+ * written.  d in {32, 64}, 1 <= k <= 32 (others: KGQ_ERR_INVALID_ARG, the host
+ * uses scores + kgq_topk_rows_f32).  workspace >= kgq_score_topk_workspace_bytes
+ * (the split item embeddings), 16-byte aligned.  out: n_users x k int32. */
+KGQ_API size_t kgq_score_topk_workspace_bytes(int64_t n_items, int32_t d);
+KGQ_API int kgq_score_topk_f32(const float *readout, const int64_t *users, int64_t n_users,
+                               const float *item_emb, int64_t n_items, int32_t d,
+                               const int32_t *train_items, const int64_t *train_start,
+                               const int64_t *train_end, int32_t k, int32_t *out,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -151,6 +151,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
         :: "r"(smem_u32(mbar)), "r"(parity) : "memory");
 }
 
+// polling with a short sleep between tries: for producer / MMA threads that
+// share an SM sub-partition with the warps they wait for
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *mbar, uint32_t parity) {
+    uint32_t ok;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                     "selp.b32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
+        if (ok) break;
+        __nanosleep(64);
+    }
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

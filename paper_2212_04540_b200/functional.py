@@ -312,3 +312,31 @@ def topk_rows(scores: torch.Tensor, k: int) -> torch.Tensor:
                                        _lib.stream_ptr(scores.device))
     _lib.check(st, "kgq_topk_rows_f32")
     return out
+
+
+def score_topk(readout: torch.Tensor, users: torch.Tensor, item_emb: torch.Tensor, train_items: torch.Tensor,
+               train_start: torch.Tensor, train_end: torch.Tensor, k: int) -> torch.Tensor:
+    """K12 (kgq_score_topk_f32): for each user row readout[users[i]], the k
+    best items of its dot products with item_emb after its train positives
+    train_items[train_start[i]:train_end[i]] (sorted) are set to -inf -- the
+    score block + ``np.argsort(-s, kind="stable")[:k]`` of train.py:121-160
+    with no score block in memory (3xTF32 tensor-core scores, fp32-level).
+    d in {32, 64}, 1 <= k <= 32; int32 (n_users, k), -1 past the item count."""
+    n, d = readout.shape
+    I = item_emb.shape[0]
+    if not (readout.is_cuda and readout.dtype == torch.float32 and item_emb.dtype == torch.float32):
+        raise TypeError("score_topk: fp32 CUDA tensors expected")
+    if d not in (32, 64) or not 1 <= k <= 32:
+        raise ValueError("score_topk: d must be 32 or 64 and 1 <= k <= 32")
+    readout, item_emb = readout.contiguous(), item_emb.contiguous()
+    users = users.to(torch.int64).contiguous()
+    out = torch.empty((users.numel(), k), dtype=torch.int32, device=readout.device)
+    lib = _lib.load()
+    ws = torch.empty(lib.kgq_score_topk_workspace_bytes(I, d), dtype=torch.uint8, device=readout.device)
+    st = lib.kgq_score_topk_f32(readout.data_ptr(), users.data_ptr(), users.numel(), item_emb.data_ptr(), I, d,
+                                train_items.to(torch.int32).contiguous().data_ptr(),
+                                train_start.to(torch.int64).contiguous().data_ptr(),
+                                train_end.to(torch.int64).contiguous().data_ptr(), k, out.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _lib.stream_ptr(readout.device))
+    _lib.check(st, "kgq_score_topk_f32")
+    return out

@@ -100,3 +100,55 @@ def test_evaluate_duplicate_test_pairs_and_chunking():
     r = torch.from_numpy(readout).cuda()
     for chunk in (None, 7, 64):
         np.testing.assert_allclose(evaluate(ds, r, 20, chunk=chunk), want, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("d", [32, 64])
+@pytest.mark.parametrize("k", [1, 7, 20, 32])
+@pytest.mark.parametrize("n_items", [1, 130, 1000, 24915])
+def test_score_topk_fused_matches_stable_argsort(d, k, n_items):
+    """K12 (kgq_score_topk_f32) == s = U . I^T; s[train] = -inf;
+    np.argsort(-s, kind="stable")[:k] (train.py:137-143).  Integer-valued
+    embeddings make every score exact (ties by index decide the order); item
+    rows with NaN give NaN scores (ranked last), an all-zero user ties every
+    item at +-0."""
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(d * 1000 + k * 17 + n_items)
+    n_users = 300
+    U = rng.integers(-3, 4, (n_users + 11, d)).astype(np.float32)
+    U[5] = 0.0
+    items = rng.integers(-3, 4, (n_items, d)).astype(np.float32)
+    if n_items > 10:
+        items[rng.integers(0, n_items, 3)] = np.nan
+    users = np.sort(rng.choice(n_users + 11, n_users, replace=False)).astype(np.int64)
+    tr_items, tr_start, tr_end = [], [], []
+    for i in range(n_users):
+        m = int(rng.integers(0, min(n_items, 40) + 1)) if i % 9 else min(n_items, 5 * k)
+        its = np.sort(rng.choice(n_items, m, replace=False))
+        tr_start.append(len(tr_items)); tr_items.extend(its.tolist()); tr_end.append(len(tr_items))
+    s = U[users].astype(np.float64) @ items.astype(np.float64).T
+    for i in range(n_users):
+        s[i, tr_items[tr_start[i]:tr_end[i]]] = -np.inf
+    want = _expect(s, k)
+    dev = lambda a, t: torch.from_numpy(np.asarray(a, dtype=t)).cuda()
+    got = F.score_topk(dev(U, np.float32), dev(users, np.int64), dev(items, np.float32),
+                       dev(tr_items if tr_items else [0], np.int32), dev(tr_start, np.int64),
+                       dev(tr_end, np.int64), k).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("k", [5, 20])
+def test_evaluate_fused_equals_score_block_path(k):
+    """train.evaluate with K12 == the score-block path (cuBLAS scores + K11),
+    on the BASELINE configs[0] dataset with an integer-valued d = 64 readout
+    (exact scores under either summation order), and == oracle.evaluate."""
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200.train import evaluate
+    ds = D.reference_dataset("default")
+    rng = np.random.default_rng(k)
+    readout = rng.integers(-2, 3, (ds.num_nodes, 64)).astype(np.float32)
+    r = torch.from_numpy(readout).cuda()
+    a = evaluate(ds, r, k, fused=True)
+    b = evaluate(ds, r, k, fused=False)
+    want = orc.evaluate(ds.num_users, ds.num_items, ds.train, ds.test, readout, k)
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(a, want, rtol=0, atol=1e-12)
