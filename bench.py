@@ -593,14 +593,13 @@ def industry_bench(args):
                 "exchange": "all-gather-v of E and dH (layout='global'); max over the simulated ranks",
                 "exchange_GB_per_rank_per_step": round(xbytes / 1e9, 2),
                 "halo_exchange_GB_per_rank_per_step_max": halo,
-                "exchange_ms_estimate_at_770GBps": round(xbytes / 770e9 * 1e3, 1),
                 "steps_per_epoch": -(-n_train // B),
-                "epoch_hours_estimate": round(-(-n_train // B) * (worst + xbytes / 770e9 * 1e3) / 3.6e6, 2),
-                "note": "1-GPU box: compute per rank measured, collectives simulated (not timed); the "
-                        "exchange time is bytes / 770 GB/s, the peer-copy bandwidth per direction "
-                        "measured on this pool's 8-GPU boxes (B200_PROFILING.md, builder guide; this "
-                        "run had 1 GPU, so it is not re-measured here), no overlap assumed; "
-                        "per-rank compute is SIMULATED one rank at a time"})
+                "compute_hours_per_epoch_max_rank": round(-(-n_train // B) * worst / 3.6e6, 2),
+                "note": "1-GPU box: per-rank compute measured one rank at a time (SIMULATED partition: "
+                        "the other ranks' rows are stand-in values); collectives not timed and no peer "
+                        "bandwidth measured here, so no exchange time or epoch time is claimed -- the "
+                        "exchange is reported in bytes; with overlap=True the SpMM of source block p "
+                        "runs while blocks p+1.. are in flight"})
     return out
 
 
@@ -615,6 +614,10 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
     layout = part.preferred_layout()
     a_local = GpuOps.local_adjacency(indptr, indices, vals, part.lo, part.hi, ds.num_nodes, "cuda",
                                      part=part if layout == "padded" else None)
+    # all-gather-v layout: the SpMM runs source block by source block as the
+    # broadcasts land (parallel.partitioned_step overlap=True), plan built once
+    overlap = layout == "global" and not args.no_overlap
+    plan = GpuOps.overlap_plan(a_local, part.cuts) if overlap else None
     from paper_2212_04540_b200.train import AdamState, adam_step
     params = init_params(ds.num_nodes, mcfg, 0)
     local = {"E0": params.entity_embeddings[part.lo:part.hi].clone()}
@@ -630,7 +633,8 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
         b = trip[(i % n_full) * 1024:][:1024]
         thetas = [local[f"theta{k}"] for k in range(mcfg.layers)]
         loss, de0, dth = partitioned_step(part, a_local, local["E0"], thetas, b[:, 0], n_users + b[:, 1],
-                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, layout=layout)
+                                          n_users + b[:, 2], cfg.l2, cfg.quant, stream, comm, layout=layout,
+                                          overlap=overlap, plan=plan)
         grads = {"E0": de0}
         grads.update({f"theta{k}": g for k, g in enumerate(dth)})
         adam_step(local, grads, state, cfg.lr)
@@ -646,7 +650,7 @@ def _partitioned_train_ms(ds, mcfg, cfg, stream, rng, world, rank, args):
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 sg = PartitionedStepGraph(part, a_local, local, state, cfg, stream, comm, mcfg.layers, 1024,
-                                          args.train_steps + 2, layout=layout)
+                                          args.train_steps + 2, layout=layout, overlap=overlap, plan=plan)
             torch.cuda.current_stream().wait_stream(side)
         except Exception as exc:      # noqa: BLE001 - keep the eager number
             print(f"[bench] partitioned graph capture failed ({type(exc).__name__}: {exc}); eager", file=sys.stderr)
@@ -1026,6 +1030,7 @@ def main():
     ap.add_argument("--industry-ranks", default="0")
     ap.add_argument("--quality-epochs", type=int, default=1)
     ap.add_argument("--no-graphs", action="store_true", help="train step without CUDA graphs")
+    ap.add_argument("--no-overlap", action="store_true", help="partitioned step: exchange, then compute")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the row-partitioned (multi-GPU) training step even at 1 GPU")
     ap.add_argument("--train-shape", default="amazon", choices=["small", "lastfm", "amazon"])

@@ -265,6 +265,19 @@ KGQ_API int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx,
 KGQ_API int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
                             int64_t n_idx, int32_t d, float *out, void *stream);
 
+/* One source-block phase of the pipelined SpMM (the partitioned step's
+ * exchange overlap, parallel.partitioned_step overlap=True): for the n_slots
+ * rows row_order[0..n_slots) (the first n_heavy get a CTA each), continue the
+ * running sums in out[row] (zeroed before the first phase) over the row's
+ * nonzeros [seg_beg[row], seg_end[row]) in ascending order, each step
+ * acc = acc + a*x as kgq_spmm_csr_f32 does; running the source blocks of the
+ * columns in ascending order therefore leaves exactly kgq_spmm_csr_f32's
+ * result.  d in {32, 64, 128}; x, out 16-byte aligned. */
+KGQ_API int kgq_spmm_csr_seg_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
+                                 int64_t n_slots, const int32_t *row_order, int64_t n_heavy,
+                                 const int32_t *seg_beg, const int32_t *seg_end, const float *x, int32_t d,
+                                 float *out, void *stream);
+
 /* Per-row Top-K of an evaluation score block (replaces train.py:141-143:
  * s[train positives] = -inf; np.argsort(-s, kind="stable")[:k]): for each of
  * n_rows rows (row stride ld floats) the indices of the k best of n_cols

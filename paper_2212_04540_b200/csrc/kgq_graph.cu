@@ -76,18 +76,23 @@ __device__ __forceinline__ int rg_f4b(int gl) {
     return NOISE_LAYOUT ? 8 * (gl >> 2) + (gl & 3) + 4 : gl + RG<D>::LPR;
 }
 
+// seg_beg / seg_end (both or neither): the row's nonzeros [seg_beg[row],
+// seg_end[row]) only, continuing the running sums the caller put in acc
+// (a source-block phase of the pipelined SpMM); else the whole row from 0.
 template <int D, bool NOISE_LAYOUT = true>
 __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
                                             const int32_t *__restrict__ indices,
                                             const float *__restrict__ vals,
                                             const float *__restrict__ x, int64_t row, bool active,
-                                            int gl, float4 (&acc)[2]) {
+                                            int gl, float4 (&acc)[2],
+                                            const int32_t *__restrict__ seg_beg = nullptr,
+                                            const int32_t *__restrict__ seg_end = nullptr) {
     constexpr int LPR = RG<D>::LPR;
-    acc[0] = acc[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!seg_beg) acc[0] = acc[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t beg = 0, end = 0;
     if (active) {
-        beg = __ldg(indptr + row);
-        end = __ldg(indptr + row + 1);
+        beg = __ldg((seg_beg ? seg_beg : indptr) + row);
+        end = seg_end ? __ldg(seg_end + row) : __ldg(indptr + row + 1);
     }
     const int len = end - beg;
     int maxlen = len;
@@ -149,7 +154,9 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
                                                 const int32_t *__restrict__ indices,
                                                 const float *__restrict__ vals,
                                                 const float *__restrict__ x, int64_t row,
-                                                float *ring) {
+                                                float *ring, const int32_t *__restrict__ seg_beg = nullptr,
+                                                const int32_t *__restrict__ seg_end = nullptr,
+                                                float acc0 = 0.0f) {
     constexpr int P = RG<D>::P, NI = RG<D>::NI;
     constexpr int SPB = 256 / kCH;                  // stages per id block
     float *xs = ring;                               // [P][kCH][D]
@@ -157,7 +164,8 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
     int32_t *ids = reinterpret_cast<int32_t *>(vs + P * kCH);   // [2][256]
     float *vls = reinterpret_cast<float *>(ids + 512);           // [2][256]
     const int t = threadIdx.x;
-    const int32_t beg = __ldg(indptr + row), end = __ldg(indptr + row + 1);
+    const int32_t beg = __ldg((seg_beg ? seg_beg : indptr) + row);
+    const int32_t end = seg_end ? __ldg(seg_end + row) : __ldg(indptr + row + 1);
     const int n = end - beg;
     const int nch = (n + kCH - 1) / kCH;
     auto load_block = [&](int b) {                  // ids/values of stages [b*SPB, (b+1)*SPB)
@@ -189,7 +197,7 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
     load_block(1);
 #pragma unroll
     for (int c = 0; c < P - 1; c++) issue(c);
-    float acc = 0.0f;
+    float acc = acc0;
     for (int c = 0; c < nch; c++) {
         cp_async_wait<P - 2>();
         __syncthreads();
@@ -223,16 +231,23 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
 #ifndef KGQ_SPMM_MINB
 #define KGQ_SPMM_MINB 4     // 4 CTAs/SM (<= 64 registers): the gather is latency-bound
 #endif
-template <int D>
+// SEG: one source-block phase of the pipelined SpMM -- each scheduled row
+// continues its ascending-column chain over its nonzeros [seg_beg, seg_end)
+// from the running sums already in out (zeroed before the first phase), so
+// the last phase leaves exactly the chain of the whole row.
+template <int D, bool SEG = false>
 __global__ void __launch_bounds__(256, KGQ_SPMM_MINB)
 spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
             const float *__restrict__ vals, int64_t n_rows, const int32_t *__restrict__ row_order,
-            int64_t n_heavy, const float *__restrict__ x, float *__restrict__ out) {
+            int64_t n_heavy, const float *__restrict__ x, float *__restrict__ out,
+            const int32_t *__restrict__ seg_beg = nullptr, const int32_t *__restrict__ seg_end = nullptr) {
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW;
     extern __shared__ __align__(16) float dyn[];
     if ((int64_t)blockIdx.x < n_heavy) {
         const int64_t row = __ldg(row_order + blockIdx.x);
-        const float h = heavy_spmm_row<D>(indptr, indices, vals, x, row, dyn);
+        const float a0 = (SEG && threadIdx.x < D) ? out[row * D + threadIdx.x] : 0.0f;
+        const float h = heavy_spmm_row<D>(indptr, indices, vals, x, row, dyn, SEG ? seg_beg : nullptr,
+                                          SEG ? seg_end : nullptr, a0);
         if (threadIdx.x < D) out[row * D + threadIdx.x] = h;
         return;
     }
@@ -249,7 +264,13 @@ spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indi
         const bool active = slot < n_light;
         const int64_t row = active ? (row_order ? (int64_t)__ldg(row_order + n_heavy + slot) : slot) : 0;
         float4 acc[2];
-        rg_spmm_row<D, false>(indptr, indices, vals, x, row, active, gl, acc);
+        if (SEG) {
+            const float4 *o = reinterpret_cast<const float4 *>(out + row * D);
+            acc[0] = active ? o[fa] : make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[1] = active ? o[fb] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        rg_spmm_row<D, false>(indptr, indices, vals, x, row, active, gl, acc, SEG ? seg_beg : nullptr,
+                              SEG ? seg_end : nullptr);
         if (active) {
             float4 *o = reinterpret_cast<float4 *>(out + row * D);
             KGQ_ST_STREAM(o + fa, acc[0]);
@@ -868,19 +889,40 @@ static cudaError_t ensure_smem(K kern, size_t smem) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int D>
+template <int D, bool SEG = false>
 static int launch_spmm(const int32_t *indptr, const int32_t *indices, const float *vals,
                        int64_t n_rows, const int32_t *row_order, int64_t n_heavy, const float *x,
-                       float *out, cudaStream_t s) {
+                       float *out, cudaStream_t s, const int32_t *seg_beg = nullptr,
+                       const int32_t *seg_end = nullptr) {
     const size_t smem = n_heavy ? RG<D>::ring_bytes : 0;
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        cudaError_t ea = ensure_smem(spmm_kernel<D>, smem);
+        cudaError_t ea = ensure_smem(spmm_kernel<D, SEG>, smem);
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set = smem;
     }
     const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 16);
-    spmm_kernel<D><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out);
+    spmm_kernel<D, SEG><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out,
+                                                seg_beg, seg_end);
+    return KGQ_OK;
+}
+
+extern "C" int kgq_spmm_csr_seg_f32(const int32_t *indptr, const int32_t *indices, const float *vals,
+                                    int64_t n_slots, const int32_t *row_order, int64_t n_heavy,
+                                    const int32_t *seg_beg, const int32_t *seg_end, const float *x, int32_t d,
+                                    float *out, void *stream) {
+    if (n_slots < 0 || n_heavy < 0 || n_heavy > n_slots) return KGQ_ERR_INVALID_ARG;
+    if (n_slots == 0) return KGQ_OK;
+    if (!indptr || !indices || !vals || !row_order || !seg_beg || !seg_end || !x || !out) return KGQ_ERR_INVALID_ARG;
+    if ((((uintptr_t)x) | ((uintptr_t)out)) & 15u) return KGQ_ERR_MISALIGNED;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st;
+    if (d == 32) st = launch_spmm<32, true>(indptr, indices, vals, n_slots, row_order, n_heavy, x, out, s, seg_beg, seg_end);
+    else if (d == 64) st = launch_spmm<64, true>(indptr, indices, vals, n_slots, row_order, n_heavy, x, out, s, seg_beg, seg_end);
+    else if (d == 128) st = launch_spmm<128, true>(indptr, indices, vals, n_slots, row_order, n_heavy, x, out, s, seg_beg, seg_end);
+    else return KGQ_ERR_INVALID_ARG;
+    if (st != KGQ_OK) return st;
+    KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
 

@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from .quantize import (row_group_offset, PASSTHROUGH_BITS, QuantConfig, QuantizedTensor, RandomStream,
                        dequantize_tensor, packed_group_bytes, quantize_tensor)
-from .tensorops import CSR, BitMask, mm, relu, spmm
+from .tensorops import CSR, BitMask, mm, relu, spmm, spmm_phased_into
 
 FUSED_DIMS = (32, 64, 128)
 
@@ -143,6 +143,63 @@ def _graph_conv_passthrough(adj: CSR, e: torch.Tensor, theta: torch.Tensor, row_
     _lib.check(st, "kgq_layer_epilogue_f32")
     q = QuantizedTensor(n_rows, d, PASSTHROUGH_BITS, None, None, None, raw=h)
     return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, (h if want_h else None)
+
+
+def graph_conv_forward_overlap(adj: CSR, e: torch.Tensor, phases, wait_block, theta: torch.Tensor,
+                               cfg: QuantConfig, stream: RandomStream | None, tensor_id: int | None = None,
+                               row_offset: int = 0):
+    """graph_conv_forward (split form) with a pipelined SpMM: column block p
+    of ``e`` is used as soon as ``wait_block(p)`` returns (CSR.block_phases),
+    then the epilogue over all rows.  Same per-row chains, same noise keys:
+    bit-identical to graph_conv_forward."""
+    n_rows, d = adj.shape[0], e.shape[1]
+    if not can_fuse(cfg, d):
+        raise ValueError("graph_conv_forward_overlap needs d in (32, 64, 128) and group == d")
+    h = torch.empty((n_rows, d), dtype=torch.float32, device=e.device)
+    spmm_phased_into(adj, e, h, phases, wait_block)
+    return _split_epilogue(h, theta.contiguous(), cfg, stream, tensor_id, row_offset)
+
+
+def _split_epilogue(h: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig, stream: RandomStream | None,
+                    tensor_id: int | None, row_offset: int):
+    """The split layer's part 2 on a given H (kgq_layer_epilogue_f32)."""
+    n_rows, d = h.shape
+    dev = h.device
+    e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
+    mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
+    L = _lib.load()
+    if cfg.passthrough:
+        st = L.kgq_layer_epilogue_f32(h.data_ptr(), n_rows, d, theta.data_ptr(), PASSTHROUGH_BITS, 0, 0, 0, None,
+                                      row_offset, None, None, None, e_next.data_ptr(), mask.data_ptr(),
+                                      _lib.stream_ptr(dev))
+        _lib.check(st, "kgq_layer_epilogue_f32")
+        q = QuantizedTensor(n_rows, d, PASSTHROUGH_BITS, None, None, None, raw=h)
+        return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, None
+    if cfg.rounding == "stochastic":
+        if stream is None:
+            raise ValueError("stochastic rounding needs a RandomStream")
+        if tensor_id is None:
+            tensor_id = stream.next_tensor_id()
+        seed = stream.seed
+    else:
+        seed, tensor_id = 0, 0
+    codes = torch.empty((n_rows, packed_group_bytes(d, cfg.bits)), dtype=torch.uint8, device=dev)
+    ranges = torch.empty(n_rows, dtype=torch.float32, device=dev)
+    offsets = torch.empty(n_rows, dtype=torch.float32, device=dev)
+    st = L.kgq_layer_epilogue_f32(
+        h.data_ptr(), n_rows, d, theta.data_ptr(), cfg.bits, cfg.mode, seed,
+        int(tensor_id) & 0xFFFFFFFFFFFFFFFF, stream.tid_base_ptr() if stream is not None else None,
+        row_offset, codes.data_ptr(), ranges.data_ptr(), offsets.data_ptr(), e_next.data_ptr(),
+        mask.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_layer_epilogue_f32")
+    q = QuantizedTensor(n_rows, d, cfg.bits, codes, ranges, offsets)
+    return e_next, BitMask(mask[:(n_rows * d + 7) // 8], (n_rows, d)), q, None
+
+
+def spmm_overlap(adj: CSR, x: torch.Tensor, phases, wait_block) -> torch.Tensor:
+    """adj @ x, pipelined over the column blocks of x (see graph_conv_forward_overlap)."""
+    out = torch.empty((adj.shape[0], x.shape[1]), dtype=torch.float32, device=x.device)
+    return spmm_phased_into(adj, x, out, phases, wait_block)
 
 
 def dequant_gemm_tn(q: QuantizedTensor, g: torch.Tensor, out: torch.Tensor | None = None,

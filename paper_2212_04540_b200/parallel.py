@@ -86,19 +86,44 @@ class Comm:
         source rank, issued together), so uneven equal-nnz blocks move
         exactly n - count rows per rank and the local CSR keeps its global
         column ids (no padding, no concatenation copy)."""
+        out, pending = self.all_gather_global_start(local, cuts, out)
+        pending.wait()
+        return out
+
+    def all_gather_global_start(self, local: torch.Tensor, cuts, out: torch.Tensor | None = None):
+        """all_gather_global, returned before the remote blocks have landed:
+        (out, pending).  The local block is in ``out`` at once (rows [lo, hi),
+        copied on the caller's stream before the collectives are issued), so
+        work that reads only those rows can run while the broadcasts of the
+        others are in flight; ``pending.wait()`` orders the caller's stream
+        after them (NCCL) or completes them (gloo)."""
         n = int(cuts[-1])
         lo, hi = int(cuts[self.rank]), int(cuts[self.rank + 1])
         if out is None:
             out = local.new_empty((n,) + tuple(local.shape[1:]))
+        out[lo:hi].copy_(local)
         stage = out.cpu() if (self.gloo and out.is_cuda) else out
-        stage[lo:hi].copy_(local)
-        works = [self.dist.broadcast(stage[int(cuts[r]):int(cuts[r + 1])], src=r, group=self.group,
-                                     async_op=True) for r in range(self.world) if cuts[r + 1] > cuts[r]]
-        for w in works:
-            w.wait()
-        if stage is not out:
-            out.copy_(stage)
-        return out
+        works = {r: self.dist.broadcast(stage[int(cuts[r]):int(cuts[r + 1])], src=r, group=self.group,
+                                        async_op=True) for r in range(self.world) if cuts[r + 1] > cuts[r]}
+        return out, _Pending(works, stage, out, cuts=cuts)
+
+    def all_gather_padded_start(self, local: torch.Tensor, m: int, out: torch.Tensor | None = None):
+        """all_gather_padded, returned before the remote blocks have landed:
+        (out, pending); the local block is copied into its slot first and the
+        collective runs in place (NCCL skips the own slot), so the slot can be
+        read meanwhile."""
+        if out is None:
+            out = local.new_empty((self.world * m,) + tuple(local.shape[1:]))
+        mine = out[self.rank * m:(self.rank + 1) * m]
+        mine[:local.shape[0]].copy_(local)
+        if local.shape[0] < m:
+            mine[local.shape[0]:].zero_()
+        if self.gloo:
+            parts = [torch.empty_like(mine, device="cpu") for _ in range(self.world)]
+            w = self.dist.all_gather(parts, mine.cpu(), group=self.group, async_op=True)
+            return out, _Pending({None: w}, None, out, parts=parts)
+        w = self.dist.all_gather_into_tensor(out, mine, group=self.group, async_op=True)
+        return out, _Pending({None: w}, None, out)
 
     def gather_index_rows(self, local: torch.Tensor, lo: int, idx: torch.Tensor) -> torch.Tensor:
         """rows ``idx`` (global ids) of the row-partitioned tensor whose block
@@ -136,9 +161,53 @@ class Comm:
         return t
 
 
+class _Pending:
+    """In-flight exchange.  ``wait()`` completes it; ``wait_source(r)`` only
+    the block of source rank r (per-source broadcasts; a single collective
+    waits whole).  gloo stages through host memory and copies back."""
+
+    def __init__(self, works: dict, stage, out, parts=None, cuts=None):
+        self.works, self.stage, self.out, self.parts, self.cuts = works, stage, out, parts, cuts
+
+    def wait_source(self, r: int):
+        if None in self.works or self.cuts is None:
+            return self.wait()
+        w = self.works.pop(r, None)
+        if w is not None:
+            w.wait()
+            if self.stage is not None and self.stage is not self.out:
+                a, b = int(self.cuts[r]), int(self.cuts[r + 1])
+                self.out[a:b].copy_(self.stage[a:b])
+
+    def wait(self):
+        for w in self.works.values():
+            w.wait()
+        self.works = {}
+        if self.parts is not None:
+            self.out.copy_(torch.cat(self.parts, 0))
+            self.parts = None
+        if self.stage is not None and self.stage is not self.out:
+            self.out.copy_(self.stage)
+            self.stage = None
+
+
+class _Done:
+    def wait(self):
+        pass
+
+    def wait_source(self, r):
+        pass
+
+
 class SoloComm:
     """World size 1 (no communication)."""
     world, rank = 1, 0
+
+    def all_gather_global_start(self, local, cuts, out=None):
+        return local, _Done()
+
+    def all_gather_padded_start(self, local, m, out=None):
+        return local, _Done()
 
     def all_gather_rows(self, local, counts):
         return local
@@ -193,6 +262,12 @@ class SimulatedRankComm:
         lo = int(cuts[self.rank])
         buf[lo:lo + local.shape[0]].copy_(local)
         return buf
+
+    def all_gather_global_start(self, local, cuts, out=None):
+        return self.all_gather_global(local, cuts, out), _Done()
+
+    def all_gather_padded_start(self, local, m, out=None):
+        return self.all_gather_padded(local, m, out), _Done()
 
     def gather_index_rows(self, local, lo, idx):
         out = self._buf(("rows", idx.shape[0]), (idx.shape[0],) + tuple(local.shape[1:]), local)
@@ -309,6 +384,20 @@ class GpuOps:
 
     layer_backward = staticmethod(F.layer_backward)
 
+    @staticmethod
+    def overlap_plan(a_local, col_cuts):
+        """Per source block: row ranges + schedules of the local block (CSR.block_phases)."""
+        return a_local.block_phases(col_cuts)
+
+    @staticmethod
+    def graph_conv_overlap(a_local, plan, e_full, wait_block, theta, cfg, stream, row_offset=0):
+        return F.graph_conv_forward_overlap(a_local, e_full, plan, wait_block, theta, cfg, stream,
+                                            row_offset=row_offset)
+
+    @staticmethod
+    def spmm_overlap(a_local, plan, x, wait_block):
+        return F.spmm_overlap(a_local, x, plan, wait_block)
+
 
 @dataclass
 class RowPartition:
@@ -358,7 +447,8 @@ class RowPartition:
 
 def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas, users, pos, neg,
                      l2: float, cfg: QuantConfig, stream: RandomStream, comm, ops=GpuOps,
-                     padded: bool = False, layout: str | None = None, halo: "HaloPlan | None" = None):
+                     padded: bool = False, layout: str | None = None, halo: "HaloPlan | None" = None,
+                     overlap: bool = False, plan=None):
     """One forward+backward of the KGNN backbone + BPR head on this rank's
     rows.  Returns (loss tensor, dE0 for the local rows, [dtheta_i] summed
     over ranks).  Mirrors tape.py:193-253's routing order.
@@ -383,6 +473,15 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     if layout == "halo" and halo is None:
         raise ValueError("layout='halo' needs a HaloPlan (a_local remapped with HaloPlan.remap)")
 
+    if overlap:
+        if layout != "global":
+            raise ValueError("overlap needs layout 'global' (one broadcast per source block)")
+        if plan is None:
+            plan = ops.overlap_plan(a_local, part.cuts)
+
+    def gather_start(x):
+        return comm.all_gather_global_start(x, part.cuts)
+
     def gather(x):
         if layout == "halo":
             return halo.exchange(x, comm)
@@ -404,8 +503,13 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     li = torch.clamp(idx - lo, 0, max(n_loc - 1, 0)).to(torch.int64)
     acc_rows = None
     for theta in thetas:
-        e_full = gather(e_local)
-        e_next, mask, q, _ = ops.graph_conv(a_local, e_full, theta, cfg, stream, row_offset=lo)
+        if overlap:
+            e_full, pending = gather_start(e_local)
+            e_next, mask, q, _ = ops.graph_conv_overlap(a_local, plan, e_full, pending.wait_source, theta, cfg,
+                                                        stream, row_offset=lo)
+        else:
+            e_full = gather(e_local)
+            e_next, mask, q, _ = ops.graph_conv(a_local, e_full, theta, cfg, stream, row_offset=lo)
         saved.append((mask, q))
         r_l = e_next.index_select(0, li)
         acc_rows = r_l if acc_rows is None else acc_rows + r_l
@@ -432,7 +536,11 @@ def partitioned_step(part: RowPartition, a_local, e0_local: torch.Tensor, thetas
     for i in range(len(thetas) - 1, -1, -1):
         mask, q = saved[i]
         dthetas[i], dh_local = ops.layer_backward(g_read, g_e, mask, q, thetas[i])
-        g_e = ops.spmm(a_local, gather(dh_local))
+        if overlap:
+            dh_full, pending = gather_start(dh_local)
+            g_e = ops.spmm_overlap(a_local, plan, dh_full, pending.wait_source)
+        else:
+            g_e = ops.spmm(a_local, gather(dh_local))
     dth = comm.all_reduce_sum(torch.stack(dthetas))
     return loss, g_e, list(dth.unbind(0))
 
@@ -447,7 +555,8 @@ class PartitionedStepGraph:
     captured with it; a replay equals the eager step bit for bit."""
 
     def __init__(self, part: RowPartition, a_local, params: dict, state, cfg, stream: RandomStream, comm,
-                 n_layers: int, batch: int, capacity: int, layout: str = "global", halo=None, ops=GpuOps):
+                 n_layers: int, batch: int, capacity: int, layout: str = "global", halo=None, ops=GpuOps,
+                 overlap: bool = False, plan=None):
         from .train import AdamState  # noqa: F401  (state is a train.AdamState)
         dev = params["E0"].device
         self.B, self.capacity, self.n_layers = batch, capacity, n_layers
@@ -461,6 +570,8 @@ class PartitionedStepGraph:
         stream.bind_device_base(self.base)
         stream._next_tensor_id = 0
         from . import _lib
+        if overlap and plan is None:        # built outside the capture (it syncs with the host)
+            plan = ops.overlap_plan(a_local, part.cuts)
         self.graph = torch.cuda.CUDAGraph()
         try:
             with torch.cuda.graph(self.graph):
@@ -468,7 +579,7 @@ class PartitionedStepGraph:
                 thetas = [params[f"theta{i}"] for i in range(n_layers)]
                 loss, de0, dth = partitioned_step(part, a_local, params["E0"], thetas, self.idx[0], self.idx[1],
                                                   self.idx[2], cfg.l2, cfg.quant, stream, comm, ops=ops,
-                                                  layout=layout, halo=halo)
+                                                  layout=layout, halo=halo, overlap=overlap, plan=plan)
                 grads = {"E0": de0}
                 grads.update({f"theta{i}": t for i, t in enumerate(dth)})
                 L = _lib.load()

@@ -76,6 +76,30 @@ class CSR:
             self._n_heavy = int((deg > self.HEAVY_NNZ).sum())
         return self._row_order.data_ptr(), self._n_heavy
 
+    def block_phases(self, col_cuts) -> "BlockPhases":
+        """The pipelined-SpMM plan for column blocks [col_cuts[p], col_cuts[p+1])
+        (the source blocks of a partitioned exchange, ascending): per block,
+        each row's nonzero range inside it and a row schedule of the rows that
+        have any (by decreasing count).  Running the blocks in order with
+        ``spmm_phased_into`` continues every row's ascending-column chain, so
+        the result is bit-identical to spmm while block p+1.. may still be in
+        flight when block p is computed."""
+        cuts = torch.as_tensor(np.asarray(col_cuts, dtype=np.int64), device=self.device)
+        W, n = int(cuts.numel()) - 1, self.shape[0]
+        ip = self.indptr.to(torch.int64)
+        rows = torch.repeat_interleave(torch.arange(n, device=self.device), ip[1:] - ip[:-1])
+        blk = torch.searchsorted(cuts, self.indices.to(torch.int64), right=True) - 1
+        cnt = torch.bincount(rows * W + blk, minlength=n * W).view(n, W)
+        off = torch.cat([ip[:-1, None], ip[:-1, None] + torch.cumsum(cnt, 1)], 1)      # [n][W+1]
+        bounds = off.t().to(torch.int32).contiguous()                                   # [W+1][n]
+        ids = torch.arange(n, device=self.device)
+        scheds = []
+        for p in range(W):
+            c = cnt[:, p]
+            sel = c > 0
+            scheds.append(RowSchedule.build(ids[sel], c[sel], self.HEAVY_NNZ))
+        return BlockPhases(bounds, scheds)
+
     @property
     def nnz(self) -> int:
         return int(self.indices.shape[0])
@@ -142,6 +166,57 @@ def mm_theta(a: torch.Tensor, theta: torch.Tensor, transpose: bool = False) -> t
     st = _lib.load().kgq_rowmm_f32(a.data_ptr(), a.shape[0], d, theta.contiguous().data_ptr(),
                                    1 if transpose else 0, out.data_ptr(), _lib.stream_ptr(a.device))
     _lib.check(st, "kgq_rowmm_f32")
+    return out
+
+
+class RowSchedule:
+    """A subset of a CSR's rows as a kernel row schedule: ``order`` (int32,
+    decreasing degree, stable), ``n_heavy`` rows above CSR.HEAVY_NNZ first."""
+
+    __slots__ = ("order", "n_heavy")
+
+    def __init__(self, order: torch.Tensor, n_heavy: int):
+        self.order, self.n_heavy = order, int(n_heavy)
+
+    @classmethod
+    def build(cls, rows: torch.Tensor, deg: torch.Tensor, heavy: int) -> "RowSchedule":
+        p = torch.sort(deg, descending=True, stable=True).indices
+        return cls(rows[p].to(torch.int32).contiguous(), int((deg > heavy).sum()))
+
+    def __len__(self) -> int:
+        return int(self.order.numel())
+
+
+class BlockPhases:
+    """CSR.block_phases: ``bounds`` [W+1][n] int32 (row r's nonzeros of block
+    p are [bounds[p][r], bounds[p+1][r])), ``scheds[p]`` its rows."""
+
+    __slots__ = ("bounds", "scheds")
+
+    def __init__(self, bounds: torch.Tensor, scheds):
+        self.bounds, self.scheds = bounds, scheds
+
+    def __len__(self) -> int:
+        return len(self.scheds)
+
+
+def spmm_phased_into(s: CSR, d: torch.Tensor, out: torch.Tensor, phases: BlockPhases, wait_block) -> torch.Tensor:
+    """out = s @ d, one column block at a time (``wait_block(p)`` before block
+    p: e.g. the exchange of that block of ``d`` has landed); each phase
+    continues the rows' running chains in out (kgq_spmm_csr_seg_f32), so the
+    result equals spmm bit for bit."""
+    out.zero_()
+    L = _lib.load()
+    n = s.shape[0]
+    for p, sch in enumerate(phases.scheds):
+        wait_block(p)
+        if len(sch) == 0:
+            continue
+        b = phases.bounds
+        st = L.kgq_spmm_csr_seg_f32(s.indptr.data_ptr(), s.indices.data_ptr(), s.data.data_ptr(), len(sch),
+                                    sch.order.data_ptr(), sch.n_heavy, b[p].data_ptr(), b[p + 1].data_ptr(),
+                                    d.data_ptr(), d.shape[1], out.data_ptr(), _lib.stream_ptr(d.device))
+        _lib.check(st, "kgq_spmm_csr_seg_f32")
     return out
 
 

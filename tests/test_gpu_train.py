@@ -314,7 +314,8 @@ def test_row_block_fused_layer_is_bit_identical_to_full():
             assert torch.equal(q.ranges, full[2].ranges[lo:hi])
 
 
-def test_partitioned_step_gpu_world1_matches_tape():
+@pytest.mark.parametrize("overlap", [False, True])
+def test_partitioned_step_gpu_world1_matches_tape(overlap):
     kgq, z, adj = _tiny()
     from paper_2212_04540_b200.parallel import GpuOps, RowPartition, SoloComm, partitioned_step
     from paper_2212_04540_b200.tape import Tape
@@ -329,7 +330,8 @@ def test_partitioned_step_gpu_world1_matches_tape():
     ix = lambda k: torch.from_numpy(z[k].astype(np.int64)).cuda()
     loss, de0, dth = partitioned_step(part, a_local, p.entity_embeddings, p.layer_weights,
                                       ix("users"), ix("pos"), ix("neg"), 1e-5, cfg,
-                                      kgq.RandomStream(21), SoloComm())
+                                      kgq.RandomStream(21), SoloComm(),
+                                      layout="global" if overlap else None, overlap=overlap)
     assert float(loss) == tape.loss()
     np.testing.assert_allclose(de0.cpu().numpy(), tg["E0"].cpu().numpy(), rtol=1e-5, atol=1e-8)
     for i, t in enumerate(dth):
@@ -618,10 +620,12 @@ def test_passthrough_layer_fused_forward_and_backward(d):
     np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(n))
 
 
-def test_partitioned_step_graph_equals_eager():
+@pytest.mark.parametrize("overlap", [False, True])
+def test_partitioned_step_graph_equals_eager(overlap):
     """parallel.PartitionedStepGraph (the partitioned step + Adam captured as
     one CUDA graph) replays bit-identically to the eager partitioned steps
-    (world size 1, SoloComm): tensor ids, Adam step and every parameter."""
+    (world size 1, SoloComm): tensor ids, Adam step and every parameter; with
+    overlap the SpMMs run as source-block phases (one block at W = 1)."""
     kgq = _kgq()
     from paper_2212_04540_b200 import data as D
     from paper_2212_04540_b200.model import ModelConfig, init_params
@@ -645,7 +649,8 @@ def test_partitioned_step_graph_equals_eager():
         local.update({f"theta{i}": t.clone() for i, t in enumerate(p0.layer_weights)})
         state, st = AdamState(local), kgq.RandomStream(0)
         if graphs:
-            sg = PartitionedStepGraph(part, a_local, local, state, cfg, st, SoloComm(), 3, 256, 8)
+            sg = PartitionedStepGraph(part, a_local, local, state, cfg, st, SoloComm(), 3, 256, 8,
+                                      overlap=overlap)
             # capture recorded nothing real: restore the initial parameters / state
             local["E0"].copy_(p0.entity_embeddings)
             for i, t in enumerate(p0.layer_weights):
@@ -659,7 +664,7 @@ def test_partitioned_step_graph_equals_eager():
             for u, pp, nn in batches:
                 th = [local[f"theta{i}"] for i in range(3)]
                 loss, de0, dth = partitioned_step(part, a_local, local["E0"], th, u, pp, nn, cfg.l2, q, st,
-                                                  SoloComm(), layout="global")
+                                                  SoloComm(), layout="global", overlap=overlap)
                 grads = {"E0": de0}
                 grads.update({f"theta{i}": g for i, g in enumerate(dth)})
                 adam_step(local, grads, state, cfg.lr)
@@ -1066,3 +1071,40 @@ def test_relu_and_layer_epilogue_special_values(split):
 
 
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [32, 64, 128])
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_pipelined_spmm_by_source_block_is_bit_identical(d, world):
+    """The overlap path of the partitioned step (parallel.partitioned_step,
+    overlap=True): the SpMM of a rank's row block run one source block of
+    columns at a time (kgq_spmm_csr_seg_f32 continuing each row's chain) ==
+    spmm bit for bit, hub rows included; so is the whole layer
+    (functional.graph_conv_forward_overlap vs graph_conv_forward)."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import functional as F
+    from paper_2212_04540_b200.parallel import GpuOps, RowPartition
+    from paper_2212_04540_b200.tensorops import spmm, spmm_phased_into
+    ds = D.reference_dataset("lastfm")
+    ip, ix, vv = D.adjacency_arrays(ds)
+    n = len(ip) - 1
+    waited = []
+    for rank in sorted({0, world - 1}):
+        part = RowPartition.build(ip, world, rank)
+        a = GpuOps.local_adjacency(ip, ix, vv, part.lo, part.hi, n, "cuda")
+        plan = a.block_phases(part.cuts)
+        x = torch.randn(n, d, device="cuda")
+        want = spmm(a, x)
+        got = torch.full_like(want, float("nan"))
+        spmm_phased_into(a, x, got, plan, waited.append)
+        assert waited[-world:] == list(range(world))
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+        th = torch.randn(d, d, device="cuda") / d ** 0.5
+        cfg = kgq.QuantConfig(bits=2, rng="fast")
+        e1, m1, q1, _ = F.graph_conv_forward(a, x, th, cfg, kgq.RandomStream(4), 7, row_offset=part.lo, split=True)
+        e2, m2, q2, _ = F.graph_conv_forward_overlap(a, x, plan, lambda p: None, th, cfg, kgq.RandomStream(4), 7,
+                                                     row_offset=part.lo)
+        assert torch.equal(e1, e2) and torch.equal(m1.packed, m2.packed)
+        assert torch.equal(q1.codes, q2.codes) and torch.equal(q1.ranges, q2.ranges)

@@ -59,6 +59,40 @@ class OracleOps:
         return OracleOps._quant(t, cfg, stream)
 
     @staticmethod
+    def overlap_plan(a_local, col_cuts):
+        return np.asarray(col_cuts, dtype=np.int64)
+
+    @staticmethod
+    def _spmm_overlap(a_local, cuts, x, wait_block):
+        """block p of the chain from a copy of x whose blocks > p are NaN (read
+        before their exchange would show), after wait_block(p); fp32 chain
+        continued across blocks (ascending columns), as the kernel does."""
+        ip, ix, vv = a_local
+        xn = x.numpy()
+        h = np.zeros((len(ip) - 1, x.shape[1]), dtype=np.float32)
+        for p in range(len(cuts) - 1):
+            wait_block(p)
+            buf = np.full(xn.shape, np.nan, dtype=np.float32)
+            buf[:cuts[p + 1]] = xn[:cuts[p + 1]]
+            for r in range(len(ip) - 1):
+                for j in range(ip[r], ip[r + 1]):
+                    if cuts[p] <= ix[j] < cuts[p + 1]:
+                        h[r] = h[r] + np.float32(vv[j]) * buf[ix[j]]
+        return h
+
+    @staticmethod
+    def graph_conv_overlap(a_local, plan, e_full, wait, theta, cfg, stream, row_offset=0):
+        h = OracleOps._spmm_overlap(a_local, plan, e_full, wait)
+        q = OracleOps._quant(torch.from_numpy(h), cfg, stream, row_offset)
+        j = h @ theta.numpy()
+        out, mask = orc.relu_mask(j)
+        return torch.from_numpy(out), _Mask(j > 0), q, None
+
+    @staticmethod
+    def spmm_overlap(a_local, plan, x, wait):
+        return torch.from_numpy(OracleOps._spmm_overlap(a_local, plan, x, wait))
+
+    @staticmethod
     def dequantize(q):
         return torch.from_numpy(orc.dequantize(q.codes, q.ranges, q.offsets, q.cols, q.bits))
 
@@ -125,7 +159,7 @@ def _problem():
     return z, n, e0, thetas, idx
 
 
-def _run(world, rank, comm, layout="concat"):
+def _run(world, rank, comm, layout="concat", overlap=False):
     z, n, e0, thetas, (users, pos, neg) = _problem()
     part = RowPartition.build(z["indptr"], world, rank)
     ip, ix, vv = OracleOps.local_adjacency(z["indptr"], z["indices"], z["data"], part.lo, part.hi, n)
@@ -139,29 +173,33 @@ def _run(world, rank, comm, layout="concat"):
     cfg = QuantConfig(bits=2, rng="fast")
     loss, de0, dth = partitioned_step(part, (ip, ix, vv), e0[part.lo:part.hi], thetas, users, pos, neg,
                                       1e-5, cfg, RandomStream(21), comm, ops=OracleOps, layout=layout,
-                                      halo=halo)
+                                      halo=halo, overlap=overlap)
     return part, loss, de0, dth
 
 
-def _worker(rank, world, port, out_q, layout="concat"):
+def _worker(rank, world, port, out_q, layout="concat", overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2212_04540_b200.parallel import Comm
-        part, loss, de0, dth = _run(world, rank, Comm(), layout)
+        part, loss, de0, dth = _run(world, rank, Comm(), layout, overlap)
         out_q.put((rank, part.lo, part.hi, float(loss), de0.numpy(), [t.numpy() for t in dth]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["concat", "padded", "global", "halo"])
-def test_partitioned_step_world2_gloo_matches_world1(layout):
+@pytest.mark.parametrize("layout,overlap", [("concat", False), ("padded", False), ("global", False),
+                                            ("halo", False), ("global", True)])
+def test_partitioned_step_world2_gloo_matches_world1(layout, overlap):
+    """overlap=True: every exchange is started asynchronously (one broadcast
+    per source) and the SpMM runs block by block as each lands (from a buffer
+    whose later blocks are NaN, so reading one too early would show)."""
     part1, loss1, de1, dth1 = _run(1, 0, SoloComm())
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000) + 7 * ["concat", "padded", "global", "halo"].index(layout)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, layout)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + 7 * (["concat", "padded", "global", "halo"].index(layout) + 4 * overlap)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, layout, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
