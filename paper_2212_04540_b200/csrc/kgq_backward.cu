@@ -209,7 +209,7 @@ using namespace kgq;
 // selects the FFMA kernel below (read once).  Amazon shape: 62 us vs 110 us.
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
-                                 int64_t rows, int32_t bits, const float *theta, float *dh,
+                                 int64_t rows, int32_t d, int32_t bits, const float *theta, float *dh,
                                  float *partial, int grid, cudaStream_t s);
 static bool use_tc_backward() {
     static int v = -1;
@@ -252,11 +252,11 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     const uint32_t *m32 = reinterpret_cast<const uint32_t *>(mask);
     const bool aligned16 = ((((uintptr_t)g_read) | ((uintptr_t)g_e) | ((uintptr_t)dh)) & 15u) == 0 &&
                            ((uintptr_t)codes & (bits == 32 ? 15u : 3u)) == 0;
-    if (d == 64 && aligned16 && use_tc_backward()) {
-        const int64_t tiles = (rows + 127) / 128;
+    if ((d == 64 || d == 128) && aligned16 && use_tc_backward()) {
+        const int64_t tiles = d == 128 ? (rows + 31) / 32 : (rows + 127) / 128;
         grid = (int)(tiles < kSMs ? tiles : kSMs);
-        const int st = kgq_launch_layer_backward_tc(g_read, g_e, m32, codes, ranges, offsets, rows, bits, theta,
-                                                    dh, partial, grid, s);
+        const int st = kgq_launch_layer_backward_tc(g_read, g_e, m32, codes, ranges, offsets, rows, d, bits,
+                                                    theta, dh, partial, grid, s);
         if (st != KGQ_OK) return st;
         const int dd = d * d;
         reduce_partials_bwd_kernel<<<(dd + 31) / 32, 256, 0, s>>>(partial, grid, dd, dtheta, accumulate);
