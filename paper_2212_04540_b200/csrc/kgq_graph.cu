@@ -25,6 +25,7 @@
 //    neighbour rows are gathered.
 #include "kgq_common.cuh"
 #include "kgq_tma.cuh"
+#include <type_traits>
 
 namespace kgq {
 
@@ -870,6 +871,300 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
 }
 
 
+
+// K6t at d = 64, thread = row (`layer_epilogue_tc64_kernel`): persistent CTA,
+// warp-specialized -- warp 0 streams H tiles (128 rows x 64 fp32, two
+// SWIZZLE_128B boxes) by TMA through a 3-stage ring; warp 1 issues J = H .
+// theta (3xTF32: 3 passes x 8 kind::tf32 MMAs, M = 128, N = 64, A = H hi|lo
+// from TMEM, B = theta^T split in smem); two sets of 4 row warps (set s takes
+// tiles j = s mod 2, so one set quantizes while the other waits for its MMAs)
+// where thread = row = TMEM lane: it reads its row from the stage
+// (conflict-free through the swizzle), quantizes it whole in registers -- the
+// same arithmetic and the same fast-noise words per element as
+// light_row_quantize / K1 (element k: call 4(k>>5) + ((k>>2)&3), word k&3,
+// half (k>>4)&1), so codes and R/Z are bit-identical -- writes its 16-byte code
+// row and R/Z, puts H hi|lo into TMEM (tcgen05.st) and, once the MMAs are
+// done, drains J: relu, the two mask words, E' into the set's box stage for a
+// TMA tensor store.  No shuffles, no cross-lane reductions, no thread-per-row
+// global loads or stores.
+
+// The rare exact path of layer_epilogue_tc64_kernel: one row's codes with the
+// checked division (div_a), x re-read from the SWIZZLE_128B stage.
+template <int BITS, int MODE>
+__device__ __noinline__ void tc64_row_codes_exact(const uint8_t *hst, int r, float z, DivR dv, FastKey fk,
+                                                 uint64_t gglob, uint64_t seed, uint64_t tid, uint32_t *cw) {
+    constexpr int D = 64, NW = 2 * BITS;
+    constexpr float Bf = (float)((1u << BITS) - 1u);
+    const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
+    for (int w = 0; w < NW; w++) cw[w] = 0u;
+#pragma unroll 1
+    for (int c = 0; c < 8; c++) {
+        uint4 rnd = make_uint4(0, 0, 0, 0);
+        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)c);
+        const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+#pragma unroll 1
+        for (int h = 0; h < 2; h++) {
+            const int k0 = 32 * (c >> 2) + 4 * (c & 3) + 16 * h;
+            u64x4 r64 = {0, 0, 0, 0};
+            if (MODE == KGQ_ROUND_SR_COMPAT)
+                r64 = philox4x64_10(gglob * (uint64_t)(D / 4) + (uint64_t)(k0 >> 2) + 1ull, 0, 0, 0, seed, tid);
+            const uint64_t cw64[4] = {r64.x, r64.y, r64.z, r64.w};
+            const float4 v = *reinterpret_cast<const float4 *>(hst + (k0 >> 5) * (128 * 128) + tma::box_off(r, k0 & 31));
+            const float xs[4] = {v.x, v.y, v.z, v.w};
+            uint32_t acc = 0;
+#pragma unroll
+            for (int el = 0; el < 4; el++) {
+                const float sv = __fmul_rn(div_a(dv, __fsub_rn(xs[el], z)), Bf);
+                const float uf = h ? u16_carrier_hi(rw[el], kc) : u16_carrier_lo(rw[el], kc);
+                acc += code_bits<MODE>(sv, uf, cw64[el] >> 11) << (BITS * el);
+            }
+            const int bit = k0 * BITS;
+            cw[bit >> 5] |= (acc - magic_sum4<BITS>()) << (bit & 31);
+        }
+    }
+}
+
+constexpr int kE2Stages = 3;
+constexpr int kE2Threads = 320;             // TMA warp, MMA warp, 2 x 4 row warps
+struct Epi64Smem {
+    static constexpr uint32_t TH = 64 * 64 * 4;          // theta^T hi or lo (16 KB)
+    static constexpr uint32_t HS = 128 * 64 * 4;         // one H tile (32 KB)
+    static constexpr uint32_t ES = 128 * 64 * 4;         // one E' tile stage (32 KB)
+    static constexpr uint32_t RING = 2 * TH;
+    static constexpr uint32_t EST = RING + kE2Stages * HS;
+    static constexpr uint32_t BAR = EST + 2 * ES;
+    static constexpr size_t bytes = (size_t)BAR + 128 + 1024;
+};
+// TMEM: A (H hi | lo) of set s at 128 s, J of set s at 256 + 64 s
+constexpr uint32_t kE2A = 0, kE2J = 256;
+
+template <int BITS, int MODE>
+__global__ void __launch_bounds__(kE2Threads, 1)
+layer_epilogue_tc64_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_rows, const float *__restrict__ theta,
+                           uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t row_offset,
+                           uint8_t *__restrict__ codes, float *__restrict__ ranges, float *__restrict__ offsets,
+                           const __grid_constant__ CUtensorMap tm_out, uint32_t *__restrict__ mask) {
+    constexpr int D = 64, M = 128, RB = D * BITS / 8;
+    constexpr int NW = BITS >= 32 ? 1 : 2 * BITS;                 // 32-bit code words per row
+    constexpr float Bf = (float)((1u << (BITS < 32 ? BITS : 1)) - 1u);
+    using S = Epi64Smem;
+    extern __shared__ uint8_t e2_raw[];
+    uint8_t *sm = e2_raw + ((1024u - (tc::smem_u32(e2_raw) & 1023u)) & 1023u);
+    float *thh = reinterpret_cast<float *>(sm), *thl = reinterpret_cast<float *>(sm + S::TH);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S::BAR);
+    uint64_t *hfull = bar, *hempty = bar + kE2Stages, *afull = bar + 2 * kE2Stages, *dfull = afull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 2);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    // theta^T split (B of J = H . theta): B(n, k) = theta[k][n], K-major SWIZZLE_128B
+    {
+        constexpr int PER = (D * D + kE2Threads - 1) / kE2Threads;
+        float tv[PER];
+#pragma unroll
+        for (int k = 0; k < PER; k++) {                 // coalesced: i = kk * D + n -> B(n, kk)
+            const int i = t + kE2Threads * k;
+            tv[k] = i < D * D ? __ldg(theta + i) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const int i = t + kE2Threads * k;
+            if (i < D * D) {
+                const uint32_t o = tc::sw128_off(i % D, i / D, D) / 4;
+                tc::split_tf32_fast(tv[k], thh[o], thl[o]);
+            }
+        }
+    }
+    if (t == 0) {
+        for (int i = 0; i < kE2Stages; i++) { tc::mbar_init(hfull + i, 1); tc::mbar_init(hempty + i, 128); }
+        for (int i = 0; i < 2; i++) { tc::mbar_init(afull + i, 128); tc::mbar_init(dfull + i, 1); }
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int64_t n_tiles = (n_rows + M - 1) / M;
+    const int nj = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);   // >= 1 (grid <= n_tiles)
+    auto tile_of = [&](int j) { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            for (int j = 0; j < nj; j++) {
+                const int st = j % kE2Stages;
+                if (j >= kE2Stages) tc::mbar_wait_sleep(hempty + st, (uint32_t)((j / kE2Stages - 1) & 1));
+                uint8_t *dst = sm + S::RING + st * S::HS;
+                tma::expect_tx(hfull + st, S::HS);
+                const int r0 = (int)(tile_of(j) * M);
+                tma::load_2d(dst, &tm_h, 0, r0, hfull + st);
+                tma::load_2d(dst + S::HS / 2, &tm_h, 32, r0, hfull + st);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer ------------------------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(M, D);
+            const uint32_t bh = tc::smem_u32(thh), bl = tc::smem_u32(thl);
+            for (int j = 0; j < nj; j++) {
+                const int s = j & 1;
+                tc::mbar_wait(afull + s, (uint32_t)((j >> 1) & 1));
+                tc::fence_after();
+                const uint32_t ab = tmem + kE2A + 128u * s, dd = tmem + kE2J + 64u * s;
+#pragma unroll
+                for (int p = 0; p < 3; p++) {          // lo.hi, hi.lo, hi.hi
+                    const uint32_t ao = p == 0 ? 64u : 0u;
+                    const uint32_t bs = p == 1 ? bl : bh;
+#pragma unroll
+                    for (int ks = 0; ks < D / 8; ks++)
+                        tc::mma_tf32_ts(dd, ab + ao + 8u * ks, tc::kmajor_sw128_desc(bs, ks, D), idesc, (p | ks) != 0);
+                }
+                tc::commit(dfull + s);
+            }
+        }
+        __syncwarp();
+    } else {
+        // --------------------------- row warps (thread = row) ---------------------------
+        const int s = (warp - 2) >> 2, q = warp & 3;
+        const int r = 32 * q + lane;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        uint8_t *estage = sm + S::EST + s * S::ES;
+        if (tid_base) tid += __ldg(tid_base);
+        const FastKey fk = make_fast_key(seed, tid);
+        const bool leader = q == 0 && lane == 0;
+        for (int j = s; j < nj; j += 2) {
+            const int st = j % kE2Stages;
+            const int64_t row = tile_of(j) * M + r;
+            const bool active = row < n_rows;
+            tc::mbar_wait(hfull + st, (uint32_t)((j / kE2Stages) & 1));
+            float x[D];
+            const uint8_t *hst = sm + S::RING + st * S::HS;
+#pragma unroll
+            for (int c4 = 0; c4 < D / 4; c4++) {
+                const float4 v = *reinterpret_cast<const float4 *>(hst + (c4 >> 3) * (S::HS / 2) + tma::box_off(r, 4 * c4));
+                x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+            }
+            if constexpr (BITS != 32) {
+                // ---- quantize the row (light_row_quantize's arithmetic and noise) ----
+                // min / max as a tree (exact, order-free); the division as the
+                // Markstein fast path for every element with a per-row flag for
+                // the rare elements outside its window, which then redo the row
+                // with the checked division (no per-element branch)
+                float mn4[4], mx4[4];                 // four interleaved chains
+#pragma unroll
+                for (int u = 0; u < 4; u++) { mn4[u] = x[u]; mx4[u] = x[u]; }
+#pragma unroll
+                for (int k = 4; k < D; k++) { mn4[k & 3] = fminf(mn4[k & 3], x[k]); mx4[k & 3] = fmaxf(mx4[k & 3], x[k]); }
+                const float z = fminf(fminf(mn4[0], mn4[1]), fminf(mn4[2], mn4[3]));
+                const float rr = __fsub_rn(fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])), z);
+                const DivR dv = make_div(rr);
+                const uint64_t gglob = (uint64_t)(row_offset + row);
+                uint32_t cw[NW];
+#pragma unroll
+                for (int w = 0; w < NW; w++) cw[w] = 0u;
+                if (rr > 0.0f) {
+                    bool slow = !dv.fast;
+                    const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {           // fast-noise call c: elements 32(c>>2) + 4(c&3) + w + 16h
+                        uint4 rnd = make_uint4(0, 0, 0, 0);
+                        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)c);
+                        const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const int k0 = 32 * (c >> 2) + 4 * (c & 3) + 16 * h;      // 4 consecutive elements
+                            u64x4 r64 = {0, 0, 0, 0};
+                            if (MODE == KGQ_ROUND_SR_COMPAT)
+                                r64 = philox4x64_10(gglob * (uint64_t)(D / 4) + (uint64_t)(k0 >> 2) + 1ull, 0, 0, 0,
+                                                    seed, tid);
+                            const uint64_t cw64[4] = {r64.x, r64.y, r64.z, r64.w};
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int el = 0; el < 4; el++) {
+                                const float a = __fsub_rn(x[k0 + el], z);
+                                slow |= (__float_as_uint(a) - 1u) < dv.thr_m1;      // 0 < a < threshold
+                                const float sv = __fmul_rn(div_a_unguarded(dv, a), Bf);
+                                const float uf = h ? u16_carrier_hi(rw[el], kc) : u16_carrier_lo(rw[el], kc);
+                                acc += code_bits<MODE>(sv, uf, cw64[el] >> 11) << (BITS * el);
+                            }
+                            const uint32_t piece = acc - magic_sum4<BITS>();
+                            const int bit = k0 * BITS;
+                            cw[bit >> 5] |= piece << (bit & 31);
+                        }
+                    }
+                    // rare: an element outside the Markstein window -> the row again with the
+                    // checked division (x re-read from the stage, one element at a time)
+                    if (slow)
+                        tc64_row_codes_exact<BITS, MODE>(hst, r, z, dv, fk, gglob, seed, tid, cw);
+                }
+                if (active) {
+                    uint32_t *crow = reinterpret_cast<uint32_t *>(codes + row * RB);
+                    if constexpr (NW % 4 == 0) {
+#pragma unroll
+                        for (int w = 0; w < NW; w += 4)
+                            *reinterpret_cast<uint4 *>(crow + w) = make_uint4(cw[w], cw[w + 1], cw[w + 2], cw[w + 3]);
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < NW; w++) crow[w] = cw[w];
+                    }
+                    ranges[row] = rr;
+                    offsets[row] = z;
+                }
+            }
+            tc::mbar_arrive(hempty + st);                 // the stage is no longer read
+            // ---- H hi | lo into TMEM (A of J), then the MMA warp takes it ----
+            {
+                const uint32_t ta = tmem + lane_addr + kE2A + 128u * s;
+#pragma unroll
+                for (int cb = 0; cb < D; cb += 8) {
+                    float hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; e++) tc::split_tf32_fast(x[cb + e], hi[e], lo[e]);
+                    tc::tmem_st8(ta + (uint32_t)cb, hi);
+                    tc::tmem_st8(ta + 64u + (uint32_t)cb, lo);
+                }
+                tc::tmem_st_wait();
+                tc::fence_before();
+                tc::mbar_arrive(afull + s);
+            }
+            // ---- drain J: relu, mask words, E' into the box stage ----
+            if (leader) tma::store_wait_read<0>();          // previous tile's E' store has read the stage
+            tma::named_sync(1 + s, 128);
+            tc::mbar_wait(dfull + s, (uint32_t)((j >> 1) & 1));
+            tc::fence_after();
+#pragma unroll
+            for (int cb = 0; cb < D; cb += 32) {
+                float v[32];
+                tc::tmem_ld32(tmem + lane_addr + kE2J + 64u * s + (uint32_t)cb, v);
+                uint32_t word = 0;
+#pragma unroll
+                for (int c = 0; c < 32; c++) {
+                    word |= (v[c] > 0.0f ? 1u : 0u) << c;
+                    v[c] = relu_nan(v[c]);
+                }
+                uint8_t *box = estage + (cb >> 5) * (M * 128);
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    *reinterpret_cast<float4 *>(box + tma::box_off(r, 4 * e)) =
+                        make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                if (active) mask[row * (D / 32) + (cb >> 5)] = word;
+            }
+            tc::fence_before();
+            tc::fence_proxy_async();
+            tma::named_sync(1 + s, 128);
+            if (leader) {
+                tma::store_2d(&tm_out, estage, 0, (int)(tile_of(j) * M));
+                tma::store_2d(&tm_out, estage + M * 128, 32, (int)(tile_of(j) * M));
+                tma::store_commit();
+            }
+        }
+        if (leader) tma::store_wait<0>();
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free(tmem, 512);
+}
+
 }  // namespace kgq
 
 using namespace kgq;
@@ -984,11 +1279,47 @@ static bool epi_use_tc(int d) {
     return !(e && e[0] == '1') && (d == 32 || d == 64);
 }
 
+
+template <int BITS>
+static int launch_epilogue_tc64(int rounding, const float *h, int64_t n_rows, const float *theta, uint64_t seed,
+                                uint64_t tid, const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
+                                float *ranges, float *offsets, float *e_next, uint32_t *mask, cudaStream_t s) {
+    void (*kern)(const CUtensorMap, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
+                 uint8_t *, float *, float *, const CUtensorMap, uint32_t *);
+    switch (rounding) {
+        case KGQ_ROUND_NEAREST: kern = layer_epilogue_tc64_kernel<BITS, KGQ_ROUND_NEAREST>; break;
+        case KGQ_ROUND_SR_FAST: kern = layer_epilogue_tc64_kernel<BITS, KGQ_ROUND_SR_FAST>; break;
+        case KGQ_ROUND_SR_COMPAT: kern = layer_epilogue_tc64_kernel<BITS, KGQ_ROUND_SR_COMPAT>; break;
+        default: return KGQ_ERR_INVALID_ARG;
+    }
+    static bool smem_set[3] = {false, false, false};
+    if (!smem_set[rounding]) {
+        cudaError_t ea = ensure_smem(kern, Epi64Smem::bytes);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set[rounding] = true;
+    }
+    CUtensorMap tm_h, tm_out;
+    if (!tma::make_rowmajor_f32(&tm_h, h, (uint64_t)n_rows, 64, 128) ||
+        !tma::make_rowmajor_f32(&tm_out, e_next, (uint64_t)n_rows, 64, 128))
+        return KGQ_ERR_CUDA;
+    const int64_t tiles = (n_rows + 127) / 128;
+    const int grid = (int)(tiles < kSMs ? tiles : kSMs);
+    kern<<<grid, kE2Threads, Epi64Smem::bytes, s>>>(tm_h, n_rows, theta, seed, tid, tid_base, row_offset, codes,
+                                                    ranges, offsets, tm_out, mask);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
 template <int D, int BITS>
 static int launch_epilogue_tc(int rounding, const float *h, int64_t n_rows, const float *theta,
                               uint64_t seed, uint64_t tid, const uint64_t *tid_base, int64_t row_offset,
                               uint8_t *codes, float *ranges, float *offsets, float *e_next,
                               uint32_t *mask, cudaStream_t s) {
+    if constexpr (D == 64) {
+        if (!(getenv("KGQ_EPI_TC1") && getenv("KGQ_EPI_TC1")[0] == '1'))
+            return launch_epilogue_tc64<BITS>(rounding, h, n_rows, theta, seed, tid, tid_base, row_offset, codes,
+                                              ranges, offsets, e_next, mask, s);
+    }
     const size_t smem = EpiTc<D>::smem;
     void (*kern)(const float *, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
                  uint8_t *, float *, float *, const CUtensorMap, uint32_t *);
