@@ -70,10 +70,32 @@ for d in (64, 32, 128):
                       max_steps=2)
 F.SPLIT_LAYER_DEFAULT = None
 
-# K11 top-k
+# pass-through (b = 32) training steps through the same fused kernels
+for d in (64, 128):
+    q = kgq.QuantConfig(bits=32)
+    mcfg, cfg = ModelConfig(layers=2, dim=d, quant=q), T.TrainConfig(batch_size=256, quant=q)
+    params = init_params(ds.num_nodes, mcfg, 0, dev)
+    state = T.AdamState(params.as_dict())
+    T.train_epoch(ds, adj, params, mcfg, cfg, state, kgq.RandomStream(0), np.random.default_rng(0), max_steps=1)
+
+# source-block phases of the SpMM (the partitioned step's exchange overlap)
+from paper_2212_04540_b200.parallel import GpuOps, RowPartition  # noqa: E402
+from paper_2212_04540_b200.tensorops import spmm_phased_into  # noqa: E402
+ip, ix, vv = D.adjacency_arrays(ds)
+for world in (3,):
+    part = RowPartition.build(ip, world, 1)
+    al = GpuOps.local_adjacency(ip, ix, vv, part.lo, part.hi, ds.num_nodes, dev)
+    for d in (32, 64, 128):
+        xx = torch.randn(ds.num_nodes, d, device=dev)
+        spmm_phased_into(al, xx, torch.empty(al.shape[0], d, device=dev), al.block_phases(part.cuts), lambda p: None)
+
+# K11 top-k and K12 fused scoring + top-k (evaluation)
 s = torch.randn(300, 5000, device=dev)
 F.topk_rows(s, 20)
 F.topk_rows(s, 64)
+for d in (32, 64):
+    ro = torch.randn(ds.num_nodes, d, device=dev)
+    T.evaluate(ds, ro, 20, fused=True)
 # the tcgen05 rowmm
 from paper_2212_04540_b200.tensorops import mm_theta  # noqa: E402
 for d in (32, 64):
