@@ -278,6 +278,34 @@ KGQ_API int kgq_spmm_csr_seg_f32(const int32_t *indptr, const int32_t *indices, 
                                  const int32_t *seg_beg, const int32_t *seg_end, const float *x, int32_t d,
                                  float *out, void *stream);
 
+/* Compact scatter (kgq_scatter_rows_multi_f32 without the sort, m <= 16384,
+ * d <= 128): the summed gradient of each distinct id to rows[i] (i = its first
+ * position in the concatenated lists) and rowmap[id] = i; rowmap is
+ * pre-filled with -1 by the caller (untouched ids: zero gradient). */
+KGQ_API int kgq_scatter_rows_multi_sparse_f32(const int32_t *idx, int64_t m, const int64_t *list_end,
+                                              int32_t n_lists, const float *g, int32_t d, float *rows,
+                                              int32_t *rowmap, void *stream);
+
+/* kgq_layer_backward_f32 with g_read in that compact form (row r: gr_rows[gr_map[r]]
+ * if gr_map[r] >= 0, else +0), so the readout gradient of a batch is never
+ * densified.  d = 64 only (else KGQ_ERR_INVALID_ARG). */
+KGQ_API int kgq_layer_backward_rows_f32(const int32_t *gr_map, const float *gr_rows, const float *g_e,
+                                        const uint8_t *mask, const uint8_t *codes, const float *ranges,
+                                        const float *offsets, int64_t rows, int32_t d, int32_t bits,
+                                        const float *theta, float *dh, float *dtheta, void *workspace,
+                                        size_t workspace_bytes, int32_t accumulate, void *stream);
+
+/* Device counters of a captured training step advanced in one launch:
+ * *a += da, *b += db, *c += dc (null pointers skipped). */
+KGQ_API int kgq_counters_add(int64_t *a, int64_t da, int64_t *b, int64_t db, int64_t *c, int64_t dc,
+                             void *stream);
+
+/* The BPR batch's gather index lists (train.py:80-85): from a row-major
+ * [B][3] int32 (user, positive item, negative item) batch, the node ids
+ * users | num_users + pos | num_users + neg as int32 and int64 [3][B]. */
+KGQ_API int kgq_batch_indices(const int32_t *batch, int64_t B, int64_t num_users, int32_t *idx32,
+                              int64_t *idx64, void *stream);
+
 /* Per-row Top-K of an evaluation score block (replaces train.py:141-143:
  * s[train positives] = -inf; np.argsort(-s, kind="stable")[:k]): for each of
  * n_rows rows (row stride ld floats) the indices of the k best of n_cols

@@ -69,6 +69,11 @@ SIGNATURES = {
     "kgq_gather_rows_sum_f32": (ctypes.c_int, [_P, _I32, _P, _I64, _I32, _P, _P]),
     "kgq_topk_rows_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _P, _P]),
     "kgq_spmm_csr_seg_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _P, _P, _I32, _P, _P]),
+    "kgq_batch_indices": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _P]),
+    "kgq_scatter_rows_multi_sparse_f32": (ctypes.c_int, [_P, _I64, _P, _I32, _P, _I32, _P, _P, _P]),
+    "kgq_layer_backward_rows_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _P,
+                                                    _SZ, _I32, _P]),
+    "kgq_counters_add": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I64, _P]),
     "kgq_score_topk_workspace_bytes": (_SZ, [_I64, _I32]),
     "kgq_score_topk_f32": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _I32, _P, _P, _P, _I32, _P, _P, _SZ, _P]),
 }

@@ -177,28 +177,40 @@ layer_backward_kernel(const float *__restrict__ g_read, const float *__restrict_
     }
 }
 
-// dtheta[i] = sum over the CTA partials in a fixed order: 8 interleaved
-// ascending chains (partials p = u mod 8) combined as ((0+1)+(2+3))+((4+5)+(6+7)).
-// A CTA owns 32 consecutive outputs; warp u runs chain u for them (coalesced
-// 128-byte loads), so 8x more loads are in flight than one thread per output.
-__global__ void __launch_bounds__(256)
+// dtheta[i] = sum over the CTA partials in a fixed order: 32 interleaved
+// ascending chains (partials p = c mod 32, c = the thread's chain), combined
+// by a fixed pairwise tree.  A CTA (1024 threads) owns 32 consecutive outputs;
+// each thread loads its <= ceil(nparts / 32) partials at once (coalesced
+// 128-byte rows per warp), so the kernel is one load round trip deep.
+__global__ void __launch_bounds__(1024)
 reduce_partials_bwd_kernel(const float *__restrict__ partial, int nparts, int dd,
                            float *__restrict__ out, int accumulate) {
-    __shared__ float s8[8][32];
-    const int c = threadIdx.x & 31, u = threadIdx.x >> 5;
-    const int i = blockIdx.x * 32 + c;
+    __shared__ float s[32][33];
+    const int o = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + o;
     float acc = 0.0f;
     if (i < dd) {
-#pragma unroll 4
-        for (int p = u; p < nparts; p += 8) acc = __fadd_rn(acc, __ldg(partial + (int64_t)p * dd + i));
+        constexpr int KB = 8;
+        for (int p0 = c; p0 < nparts; p0 += 32 * KB) {
+            float v[KB];
+#pragma unroll
+            for (int k = 0; k < KB; k++) {
+                const int p = p0 + 32 * k;
+                v[k] = p < nparts ? __ldg(partial + (int64_t)p * dd + i) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < KB; k++)
+                if (p0 + 32 * k < nparts) acc = __fadd_rn(acc, v[k]);
+        }
     }
-    s8[u][c] = acc;
+    s[c][o] = acc;
     __syncthreads();
-    if (u == 0 && i < dd) {
-        const float sum = __fadd_rn(__fadd_rn(__fadd_rn(s8[0][c], s8[1][c]), __fadd_rn(s8[2][c], s8[3][c])),
-                                    __fadd_rn(__fadd_rn(s8[4][c], s8[5][c]), __fadd_rn(s8[6][c], s8[7][c])));
-        out[i] = accumulate ? __fadd_rn(out[i], sum) : sum;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        if (c < w) s[c][o] = __fadd_rn(s[c][o], s[c + w][o]);
+        __syncthreads();
     }
+    if (c == 0 && i < dd) out[i] = accumulate ? __fadd_rn(out[i], s[0][o]) : s[0][o];
 }
 
 }  // namespace kgq
@@ -210,7 +222,8 @@ using namespace kgq;
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t d, int32_t bits, const float *theta, float *dh,
-                                 float *partial, int grid, cudaStream_t s);
+                                 float *partial, int grid, cudaStream_t s, const int32_t *gr_map = nullptr,
+                                 const float *gr_rows = nullptr);
 static bool use_tc_backward() {
     static int v = -1;
     if (v < 0) {
@@ -259,7 +272,7 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
                                                     theta, dh, partial, grid, s);
         if (st != KGQ_OK) return st;
         const int dd = d * d;
-        reduce_partials_bwd_kernel<<<(dd + 31) / 32, 256, 0, s>>>(partial, grid, dd, dtheta, accumulate);
+        reduce_partials_bwd_kernel<<<(dd + 31) / 32, 1024, 0, s>>>(partial, grid, dd, dtheta, accumulate);
         KGQ_LAUNCH_CHECK();
         return KGQ_OK;
     }
@@ -288,7 +301,38 @@ extern "C" int kgq_layer_backward_f32(const float *g_read, const float *g_e, con
     }
 #undef KGQ_BWD
     const int dd = d * d;
-    reduce_partials_bwd_kernel<<<(dd + 31) / 32, 256, 0, s>>>(partial, grid, dd, dtheta, accumulate);
+    reduce_partials_bwd_kernel<<<(dd + 31) / 32, 1024, 0, s>>>(partial, grid, dd, dtheta, accumulate);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+// kgq_layer_backward_f32 with g_read in compact form (the readout gradient of a
+// training batch touches ~3B of N rows): row r's g_read is gr_rows[gr_map[r]]
+// when gr_map[r] >= 0, else +0.  Saves the dense N x d zero-fill and its reads
+// in every layer.  d = 64 on the tensor-core kernel only (others:
+// KGQ_ERR_INVALID_ARG, the host densifies).
+extern "C" int kgq_layer_backward_rows_f32(const int32_t *gr_map, const float *gr_rows, const float *g_e,
+                                           const uint8_t *mask, const uint8_t *codes, const float *ranges,
+                                           const float *offsets, int64_t rows, int32_t d, int32_t bits,
+                                           const float *theta, float *dh, float *dtheta, void *workspace,
+                                           size_t workspace_bytes, int32_t accumulate, void *stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8 || bits == 32)) return KGQ_ERR_UNSUPPORTED_BITS;
+    if (d != 64 || rows < 1 || !use_tc_backward()) return KGQ_ERR_INVALID_ARG;
+    if (!gr_map || !gr_rows || !mask || !codes || !theta || !dh || !dtheta) return KGQ_ERR_INVALID_ARG;
+    if (bits != 32 && (!ranges || !offsets)) return KGQ_ERR_INVALID_ARG;
+    if (((uintptr_t)mask) & 3u) return KGQ_ERR_MISALIGNED;
+    if ((((uintptr_t)gr_rows) | ((uintptr_t)g_e) | ((uintptr_t)dh)) & 15u) return KGQ_ERR_MISALIGNED;
+    if (((uintptr_t)codes) & (bits == 32 ? 15u : 3u)) return KGQ_ERR_MISALIGNED;
+    if (!workspace || workspace_bytes < kgq_layer_backward_workspace_bytes(rows, d)) return KGQ_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t tiles = (rows + 127) / 128;
+    const int grid = (int)(tiles < kSMs ? tiles : kSMs);
+    float *partial = reinterpret_cast<float *>(workspace);
+    const int st = kgq_launch_layer_backward_tc(nullptr, g_e, reinterpret_cast<const uint32_t *>(mask), codes, ranges,
+                                                offsets, rows, d, bits, theta, dh, partial, grid, s, gr_map, gr_rows);
+    if (st != KGQ_OK) return st;
+    const int dd = d * d;
+    reduce_partials_bwd_kernel<<<(dd + 31) / 32, 1024, 0, s>>>(partial, grid, dd, dtheta, accumulate);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

@@ -60,7 +60,8 @@ constexpr uint32_t kTmAcc = 0, kTmDh = 128, kTmA = 256;
 template <int BITS>
 __global__ void __launch_bounds__(kBtcThreads, 1)
 layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid_constant__ CUtensorMap tm_ge,
-                         int has_gr, int has_ge, const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
+                         int has_gr, int has_ge, const int32_t *__restrict__ gr_map,
+                         const float *__restrict__ gr_rows, const uint32_t *__restrict__ mask, const uint8_t *__restrict__ codes,
                          const float *__restrict__ ranges, const float *__restrict__ offsets,
                          int64_t rows, const float *__restrict__ theta, float *__restrict__ dh,
                          float *__restrict__ partial) {
@@ -159,6 +160,7 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
         float4 pa[4], pe[4];
         float prg = 0.f, pzz = 0.f;
         uint32_t pm = 0u, pcw[NCW];
+        int32_t pslot = -1;                          // compact g_read: this row's slot (-1: zero)
         float4 ph[BITS == 32 ? 4 : 1];
         const uint8_t *instage = sm + BwdTcSmem::INB + g * BwdTcSmem::IN;
         const bool issuer = (warp == 2 * g) && lane == 0;   // first warp of the group
@@ -186,6 +188,7 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
             prg = (ok && BITS != 32) ? __ldg(ranges + row) : 0.f;
             pzz = (ok && BITS != 32) ? __ldg(offsets + row) : 0.f;
             pm = ok ? __ldg(mask + row * 2 + (cq >> 1)) : 0u;        // raw word: bits 16 (cq & 1) ..
+            pslot = (ok && gr_map) ? __ldg(gr_map + row) : -1;
             if constexpr (BITS == 1) {
                 pcw[0] = ok ? (uint32_t)__ldg(reinterpret_cast<const uint16_t *>(codes + row * RB) + cq) : 0u;
             } else if constexpr (BITS != 32) {
@@ -221,6 +224,7 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
         for (int j = 0; j < nj; j++) {
             const float rg = prg, zz = pzz;
             const uint32_t mw = (pm >> (16 * (cq & 1))) & 0xFFFFu;
+            const int32_t grs = pslot;                   // compact g_read slot of this row
             uint32_t cw[NCW];
 #pragma unroll
             for (int w = 0; w < NCW; w++) cw[w] = pcw[w];
@@ -237,7 +241,9 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     const uint32_t o = bx * 8192 + tma::box_off(r_unit, 16 * (cq & 1) + 4 * i);
-                    pa[i] = has_gr ? *reinterpret_cast<const float4 *>(instage + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    pa[i] = has_gr ? *reinterpret_cast<const float4 *>(instage + o)
+                          : (grs >= 0 ? __ldg(reinterpret_cast<const float4 *>(gr_rows + (int64_t)grs * D) + 4 * cq + i)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f));
                     pe[i] = has_ge ? *reinterpret_cast<const float4 *>(instage + 16384 + o) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
@@ -272,7 +278,8 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
                     for (int e = 0; e < 4; e++) {
                         const int c = 4 * i + e;                 // column inside the 16-column slice
                         // g = g_read + g_e in the reference's routing order (tape.py:204-209)
-                        const float gv = (has_gr && has_ge) ? __fadd_rn(av[e], ev[e]) : (has_gr ? av[e] : ev[e]);
+                        const bool read = has_gr || gr_map;          // compact g_read: absent rows are +0
+                        const float gv = (read && has_ge) ? __fadd_rn(av[e], ev[e]) : (read ? av[e] : ev[e]);
                         const float gj = ((mw >> c) & 1u) ? gv : 0.0f;   // relu backward (sign of 0 immaterial: GEMM operand)
                         float hv;
                         if constexpr (BITS == 32) {
@@ -641,10 +648,11 @@ using namespace kgq;
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t d, int32_t bits, const float *theta, float *dh,
-                                 float *partial, int grid, cudaStream_t s) {
+                                 float *partial, int grid, cudaStream_t s, const int32_t *gr_map,
+                                 const float *gr_rows) {
     static bool attr[33] = {false}, attr128[33] = {false};
     CUtensorMap tgr, tge;
-    const float *any = g_read ? g_read : g_e;
+    const float *any = g_read ? g_read : (g_e ? g_e : gr_rows);    // an unused map still needs an address
     const uint32_t box_rows = d == 128 ? (uint32_t)kT8U : 64u;
     if (!tma::make_rowmajor_f32(&tgr, g_read ? g_read : any, (uint64_t)rows, (uint64_t)d, box_rows) ||
         !tma::make_rowmajor_f32(&tge, g_e ? g_e : any, (uint64_t)rows, (uint64_t)d, box_rows))
@@ -680,8 +688,9 @@ int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const ui
             if (e != cudaSuccess) return kgq_set_cuda_error(e);                                    \
             attr[B] = true;                                                                        \
         }                                                                                          \
-        layer_backward_tc_kernel<B><<<grid, kBtcThreads, BwdTcSmem::bytes, s>>>(tgr, tge, hr, he, mask, codes, \
-                                                                        ranges, offsets, rows, theta, dh, partial); \
+        layer_backward_tc_kernel<B><<<grid, kBtcThreads, BwdTcSmem::bytes, s>>>(tgr, tge, hr, he, gr_map, gr_rows, \
+                                                                        mask, codes, ranges, offsets, rows, theta, dh, \
+                                                                        partial); \
     } while (0)
     switch (bits) {
         case 1: KGQ_BTC(1); break;

@@ -183,7 +183,8 @@ scatter_rows_multi_kernel(const int64_t *__restrict__ order, const int32_t *__re
 // all L1/L2-resident for a training batch (m = 3B).
 __global__ void __launch_bounds__(256)
 scatter_rows_multi_nosort_kernel(const int32_t *__restrict__ idx, int64_t m, ListEnds list_end, int n_lists,
-                                 const float *__restrict__ g, int d, float *__restrict__ out) {
+                                 const float *__restrict__ g, int d, float *__restrict__ out,
+                                 int32_t *__restrict__ rowmap = nullptr) {
     constexpr int NF = 4;                           // features per lane: d <= 128
     extern __shared__ int32_t sidx[];               // the whole id list (m <= 16384), staged once per CTA
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) sidx[k] = __ldg(idx + k);
@@ -269,11 +270,44 @@ scatter_rows_multi_nosort_kernel(const int32_t *__restrict__ idx, int64_t m, Lis
             acc[k] = 0.0f;
         }
     }
+    // dense: out[row]; compact (rowmap != null): out[i] and rowmap[row] = i
+    float *orow = rowmap ? out + i * d : out + (int64_t)row * d;
+    if (rowmap && lane == 0) rowmap[row] = (int32_t)i;
 #pragma unroll
     for (int k = 0; k < NF; k++) {
         const int f = lane + 32 * k;
-        if (f < d) out[(int64_t)row * d + f] = total[k];
+        if (f < d) orow[f] = total[k];
     }
+}
+
+// Compact form of kgq_scatter_rows_multi_f32 (sort-free kernel only): the
+// summed row of each distinct id goes to rows[i], i = its first position in
+// the concatenated lists, and rowmap[id] = i (rowmap pre-filled with -1 by
+// the caller: the rows never touched stay -1, i.e. zero gradient).
+extern "C" int kgq_scatter_rows_multi_sparse_f32(const int32_t *idx, int64_t m, const int64_t *list_end,
+                                                 int32_t n_lists, const float *g, int32_t d, float *rows,
+                                                 int32_t *rowmap, void *stream) {
+    if (m < 0 || d < 1 || d > 128 || m > 16384 || n_lists < 1 || n_lists > kMaxScatterLists || !list_end)
+        return KGQ_ERR_INVALID_ARG;
+    if (m == 0) return KGQ_OK;
+    if (!idx || !g || !rows || !rowmap) return KGQ_ERR_INVALID_ARG;
+    ListEnds ends;
+    for (int i = 0; i < kMaxScatterLists; i++) ends.e[i] = i < n_lists ? list_end[i] : m;
+    const int64_t blocks = (m * 32 + 255) / 256;
+    const size_t smem = (size_t)m * sizeof(int32_t);
+    if (smem > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(scatter_rows_multi_nosort_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            if (e != cudaSuccess) return kgq_set_cuda_error(e);
+            attr = true;
+        }
+    }
+    scatter_rows_multi_nosort_kernel<<<(int)blocks, 256, smem, (cudaStream_t)stream>>>(idx, m, ends, n_lists, g, d,
+                                                                                     rows, rowmap);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
 }
 
 extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx, int64_t m,
@@ -342,6 +376,30 @@ extern "C" int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_term
     int64_t blocks = (total + 255) / 256;
     if (blocks > (int64_t)kSMs * 8) blocks = (int64_t)kSMs * 8;
     gather_rows_sum_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(t, n_terms, idx, n_idx, d, out);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+// The BPR batch's three gather index lists from one [B][3] (user, pos item,
+// neg item) int32 batch: node ids users / num_users + pos / num_users + neg,
+// as int32 (the gather contexts, tape.py:143-152) and int64 (the gathers).
+__global__ void batch_indices_kernel(const int32_t *__restrict__ batch, int64_t B, int64_t num_users,
+                                     int32_t *__restrict__ idx32, int64_t *__restrict__ idx64) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * B; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t list = i / B, r = i % B;
+        const int64_t v = (int64_t)__ldg(batch + 3 * r + list) + (list ? num_users : 0);
+        idx32[i] = (int32_t)v;
+        idx64[i] = v;
+    }
+}
+
+extern "C" int kgq_batch_indices(const int32_t *batch, int64_t B, int64_t num_users, int32_t *idx32,
+                                 int64_t *idx64, void *stream) {
+    if (B < 0 || num_users < 0) return KGQ_ERR_INVALID_ARG;
+    if (B == 0) return KGQ_OK;
+    if (!batch || !idx32 || !idx64) return KGQ_ERR_INVALID_ARG;
+    const int64_t n = 3 * B, blocks = (n + 255) / 256 < 4 * kSMs ? (n + 255) / 256 : 4 * kSMs;
+    batch_indices_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(batch, B, num_users, idx32, idx64);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }

@@ -227,3 +227,20 @@ extern "C" int kgq_adam_step_dev_f32(float *param, const float *grad, float *m, 
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
+
+// A captured step's device counters advanced in one launch: *a += da,
+// *b += db, *c += dc (step index, Adam step, tensor-id base; null = skip).
+__global__ void counters_add_kernel(int64_t *a, int64_t da, int64_t *b, int64_t db, int64_t *c, int64_t dc) {
+    if (threadIdx.x == 0) {
+        if (a) *a += da;
+        if (b) *b += db;
+        if (c) *c += dc;
+    }
+}
+
+extern "C" int kgq_counters_add(int64_t *a, int64_t da, int64_t *b, int64_t db, int64_t *c, int64_t dc,
+                                void *stream) {
+    counters_add_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a, da, b, db, c, dc);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}

@@ -236,12 +236,82 @@ def dequant_gemm_tn(q: QuantizedTensor, g: torch.Tensor, out: torch.Tensor | Non
     return out
 
 
+class SparseRows:
+    """A row-sparse gradient: row r is ``rows[rowmap[r]]`` when rowmap[r] >= 0,
+    else +0 -- the readout gradient of a training batch (the scatter of the
+    B-row gathers, ~3B of N rows) as kgq_scatter_rows_multi_sparse_f32 leaves
+    it.  ``dense()`` materializes the N x d tensor (once, cached) for the
+    consumers that need it; the tensor-core layer backward reads it as is."""
+
+    def __init__(self, rowmap: torch.Tensor, rows: torch.Tensor, n_rows: int):
+        self.rowmap, self.rows, self.n_rows = rowmap, rows, int(n_rows)
+        self._dense = None
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.rows.shape[1])
+
+    @property
+    def device(self):
+        return self.rows.device
+
+    def dense(self) -> torch.Tensor:
+        if self._dense is None:           # gather with a zero row in front: no host sync
+            ext = torch.cat([self.rows.new_zeros((1, self.rows.shape[1])), self.rows])
+            self._dense = ext.index_select(0, (self.rowmap + 1).to(torch.int64))
+        return self._dense
+
+
+def scatter_rows_multi_sparse(src_rows: int, idxs, gs):
+    """scatter_rows_multi in compact form (SparseRows); None when the
+    sort-free kernel does not apply (the caller takes the dense path)."""
+    d = gs[0].shape[1]
+    m = sum(int(i.numel()) for i in idxs)
+    if m == 0 or m > 16384 or d > 128 or len(idxs) > 8 or not gs[0].is_cuda:
+        return None
+    dev = gs[0].device
+    idx = torch.cat([i.reshape(-1).to(torch.int32) for i in idxs])
+    g = torch.cat([x.reshape(-1, d).to(torch.float32) for x in gs]).contiguous()
+    ends = np.ascontiguousarray(np.cumsum([i.numel() for i in idxs]), dtype=np.int64)
+    rows = torch.empty((m, d), dtype=torch.float32, device=dev)
+    rowmap = torch.full((src_rows,), -1, dtype=torch.int32, device=dev)
+    st = _lib.load().kgq_scatter_rows_multi_sparse_f32(idx.data_ptr(), m, ends.ctypes.data, len(idxs), g.data_ptr(),
+                                                       d, rows.data_ptr(), rowmap.data_ptr(), _lib.stream_ptr(dev))
+    _lib.check(st, "kgq_scatter_rows_multi_sparse_f32")
+    return SparseRows(rowmap, rows, src_rows)
+
+
 def layer_backward(g_read, g_e, mask: BitMask, q: QuantizedTensor, theta: torch.Tensor):
     """Fused layer backward (tape.py:217-225): returns (dtheta, dh) for
     g_j = (g_read + g_e) * mask, dh = g_j theta^T, dtheta = Hhat^T g_j, with
     the dequantized H never materialized.  Falls back to the separate ops for
-    d not in (32, 64, 128) or pass-through contexts."""
+    d not in (32, 64, 128) or pass-through contexts.  ``g_read`` may be a
+    SparseRows (read compactly by the d = 64 tensor-core kernel)."""
     from .tensorops import mask_apply, mm_theta
+    if isinstance(g_read, SparseRows):
+        d = g_read.shape[1]
+        if d == 64 and (q.bits == PASSTHROUGH_BITS or q.group_size == d) and \
+                not (q.bits == PASSTHROUGH_BITS and q.raw is None):
+            passthrough = q.bits == PASSTHROUGH_BITS
+            dev = g_read.device
+            rows = g_read.n_rows
+            dh = torch.empty((rows, d), dtype=torch.float32, device=dev)
+            dth = torch.empty((d, d), dtype=torch.float32, device=dev)
+            L = _lib.load()
+            ws_bytes = int(L.kgq_layer_backward_workspace_bytes(rows, d))
+            ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+            ge = None if g_e is None else g_e.contiguous()
+            codes_ptr = q.raw.contiguous().data_ptr() if passthrough else q.codes.data_ptr()
+            st = L.kgq_layer_backward_rows_f32(g_read.rowmap.data_ptr(), g_read.rows.data_ptr(), _lib.ptr(ge),
+                                               mask.packed.data_ptr(), codes_ptr, _lib.ptr(q.ranges),
+                                               _lib.ptr(q.offsets), rows, d, q.bits, theta.contiguous().data_ptr(),
+                                               dh.data_ptr(), dth.data_ptr(), ws.data_ptr(), ws_bytes, 0,
+                                               _lib.stream_ptr(dev))
+            if st == _lib.KGQ_OK:
+                return dth, dh
+            if st != _lib.KGQ_ERR_INVALID_ARG:
+                _lib.check(st, "kgq_layer_backward_rows_f32")
+        g_read = g_read.dense()
     src = g_read if g_read is not None else g_e
     d = src.shape[1]
     passthrough = q.bits == PASSTHROUGH_BITS
