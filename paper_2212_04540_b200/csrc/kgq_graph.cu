@@ -100,6 +100,7 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     const int fa = rg_f4a<D, NOISE_LAYOUT>(gl), fb = rg_f4b<D, NOISE_LAYOUT>(gl);
+    f32x2 ap[4] = {pk2(acc[0].x, acc[0].y), pk2(acc[0].z, acc[0].w), pk2(acc[1].x, acc[1].y), pk2(acc[1].z, acc[1].w)};
     int32_t nx_col = 0;
     float nx_val = 0.0f;
     if (gl < len) {
@@ -131,19 +132,23 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 if (t + u < cnt) {
+                    // acc = acc + a * x with separate roundings: scalar products,
+                    // packed adds (FADD2, the same per-lane rounding); a packed
+                    // multiply would be contracted into FFMA2 by ptxas
                     const float a = av[u];
-                    acc[0].x = __fadd_rn(acc[0].x, __fmul_rn(a, xa[u].x));
-                    acc[0].y = __fadd_rn(acc[0].y, __fmul_rn(a, xa[u].y));
-                    acc[0].z = __fadd_rn(acc[0].z, __fmul_rn(a, xa[u].z));
-                    acc[0].w = __fadd_rn(acc[0].w, __fmul_rn(a, xa[u].w));
-                    acc[1].x = __fadd_rn(acc[1].x, __fmul_rn(a, xb[u].x));
-                    acc[1].y = __fadd_rn(acc[1].y, __fmul_rn(a, xb[u].y));
-                    acc[1].z = __fadd_rn(acc[1].z, __fmul_rn(a, xb[u].z));
-                    acc[1].w = __fadd_rn(acc[1].w, __fmul_rn(a, xb[u].w));
+                    ap[0] = add2_rn(ap[0], pk2(__fmul_rn(a, xa[u].x), __fmul_rn(a, xa[u].y)));
+                    ap[1] = add2_rn(ap[1], pk2(__fmul_rn(a, xa[u].z), __fmul_rn(a, xa[u].w)));
+                    ap[2] = add2_rn(ap[2], pk2(__fmul_rn(a, xb[u].x), __fmul_rn(a, xb[u].y)));
+                    ap[3] = add2_rn(ap[3], pk2(__fmul_rn(a, xb[u].z), __fmul_rn(a, xb[u].w)));
                 }
             }
         }
     }
+    uint32_t w0, w1;
+    upk2u(ap[0], w0, w1); acc[0].x = __uint_as_float(w0); acc[0].y = __uint_as_float(w1);
+    upk2u(ap[1], w0, w1); acc[0].z = __uint_as_float(w0); acc[0].w = __uint_as_float(w1);
+    upk2u(ap[2], w0, w1); acc[1].x = __uint_as_float(w0); acc[1].y = __uint_as_float(w1);
+    upk2u(ap[3], w0, w1); acc[1].z = __uint_as_float(w0); acc[1].w = __uint_as_float(w1);
 }
 
 // ---------------------------------------------------------------------------
