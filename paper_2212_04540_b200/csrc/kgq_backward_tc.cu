@@ -301,11 +301,7 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
                 // smem: logical chunk (2 pr + u) ^ sw at instruction u
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
-#ifdef KGQ_BWD_NOSWAP
-                    const int src = u;
-#else
                     const int src = u ^ sw;                        // which chunk's registers (0/1 of the pair)
-#endif
                     const int col = cbase + 4 * (2 * pr + src);    // its first column in the block
                     const uint32_t o = tc::b32_off(r_unit, col, 64) / 4;
                     auto pick = [&](const float *v) {
