@@ -77,10 +77,23 @@ __device__ __forceinline__ int rg_f4b(int gl) {
     return NOISE_LAYOUT ? 8 * (gl >> 2) + (gl & 3) + 4 : gl + RG<D>::LPR;
 }
 
+#ifndef KGQ_SPMM_BATCH
+#define KGQ_SPMM_BATCH 1    // neighbour rows per batch in the light path: 1 (48 registers, 5 CTAs/SM)
+                            // measured 13 % faster than 4 and 2 (tools/spmm_ab.py A/B builds)
+#endif
+#ifdef KGQ_SPMM_NOALLOC
+// gathered rows are almost never re-hit in L1 (4 % hit rate): do not allocate
+__device__ __forceinline__ float4 ldg_noalloc(const float4 *p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+#endif
 // seg_beg / seg_end (both or neither): the row's nonzeros [seg_beg[row],
 // seg_end[row]) only, continuing the running sums the caller put in acc
 // (a source-block phase of the pipelined SpMM); else the whole row from 0.
-template <int D, bool NOISE_LAYOUT = true>
+template <int D, bool NOISE_LAYOUT = true, int BATCH = 4>
 __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
                                             const int32_t *__restrict__ indices,
                                             const float *__restrict__ vals,
@@ -116,21 +129,26 @@ __device__ __forceinline__ void rg_spmm_row(const int32_t *__restrict__ indptr,
             nx_val = KGQ_LD_STREAM(vals + beg + base + LPR + gl);
         }
 #pragma unroll
-        for (int t = 0; t < LPR; t += 4) {
-            float4 xa[4], xb[4];
-            float av[4];
+        for (int t = 0; t < LPR; t += BATCH) {
+            float4 xa[BATCH], xb[BATCH];
+            float av[BATCH];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < BATCH; u++) {
                 const int32_t col = __shfl_sync(0xffffffffu, my_col, t + u, LPR);
                 av[u] = __shfl_sync(0xffffffffu, my_val, t + u, LPR);
                 if (t + u < cnt) {
                     const float4 *xr = reinterpret_cast<const float4 *>(x + (int64_t)col * D);
+#ifdef KGQ_SPMM_NOALLOC
+                    xa[u] = ldg_noalloc(xr + fa);
+                    xb[u] = ldg_noalloc(xr + fb);
+#else
                     xa[u] = __ldg(xr + fa);
                     xb[u] = __ldg(xr + fb);
+#endif
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < BATCH; u++) {
                 if (t + u < cnt) {
                     // acc = acc + a * x with separate roundings: scalar products,
                     // packed adds (FADD2, the same per-lane rounding); a packed
@@ -235,7 +253,7 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
 }
 
 #ifndef KGQ_SPMM_MINB
-#define KGQ_SPMM_MINB 4     // 4 CTAs/SM (<= 64 registers): the gather is latency-bound
+#define KGQ_SPMM_MINB 3     // register cap 80; with KGQ_SPMM_BATCH 1 ptxas needs 48 (5 CTAs/SM resident)
 #endif
 // SEG: one source-block phase of the pipelined SpMM -- each scheduled row
 // continues its ascending-column chain over its nonzeros [seg_beg, seg_end)
@@ -275,8 +293,8 @@ spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indi
             acc[0] = active ? o[fa] : make_float4(0.f, 0.f, 0.f, 0.f);
             acc[1] = active ? o[fb] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        rg_spmm_row<D, false>(indptr, indices, vals, x, row, active, gl, acc, SEG ? seg_beg : nullptr,
-                              SEG ? seg_end : nullptr);
+        rg_spmm_row<D, false, KGQ_SPMM_BATCH>(indptr, indices, vals, x, row, active, gl, acc,
+                                              SEG ? seg_beg : nullptr, SEG ? seg_end : nullptr);
         if (active) {
             float4 *o = reinterpret_cast<float4 *>(out + row * D);
             KGQ_ST_STREAM(o + fa, acc[0]);
