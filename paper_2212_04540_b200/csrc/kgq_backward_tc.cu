@@ -259,7 +259,12 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
             float lut[BITS <= 2 ? (1 << BITS) : 1];
             if constexpr (BITS <= 2) {
 #pragma unroll
-                for (int c = 0; c < (1 << BITS); c++) lut[c] = lut_entry<BITS>(rg, zz, c);
+                for (int c = 0; c < (1 << BITS); c++)
+#ifdef KGQ_BWD_LUT_FMA
+                    lut[c] = __fmaf_rn((float)c, rb, zz);
+#else
+                    lut[c] = lut_entry<BITS>(rg, zz, c);
+#endif
             }
             // slot free (dtheta MMAs of the previous tile done), TMEM A buffer free (dH of tile j-2 done)
             if (j >= 1) tc::mbar_wait(empty + g, (uint32_t)((j - 1) & 1));
