@@ -254,17 +254,15 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
             }
             // b <= 2: the row's 2^b IEEE dequantized values (K2's arithmetic) once,
             // then a select per element; b = 4 / 8: Hhat = Z + c * (R / B) with one
-            // FFMA per element (a GEMM operand, <= 2 ulp from K2's value).
+            // FFMA per element (<= 2 ulp from K2's value).  The FFMA form at b <= 2
+            // is 2 % faster but its errors are coherent across rows (same code, same
+            // error): Last-FM theta after 10 steps drifts 5e-5 from the reference vs
+            // 2e-6 with the exact values, so b <= 2 keeps them.
             const float rb = __fmul_rn(rg, 1.0f / (float)((1u << (BITS < 32 ? BITS : 1)) - 1u));
             float lut[BITS <= 2 ? (1 << BITS) : 1];
             if constexpr (BITS <= 2) {
 #pragma unroll
-                for (int c = 0; c < (1 << BITS); c++)
-#ifdef KGQ_BWD_LUT_FMA
-                    lut[c] = __fmaf_rn((float)c, rb, zz);
-#else
-                    lut[c] = lut_entry<BITS>(rg, zz, c);
-#endif
+                for (int c = 0; c < (1 << BITS); c++) lut[c] = lut_entry<BITS>(rg, zz, c);
             }
             // slot free (dtheta MMAs of the previous tile done), TMEM A buffer free (dH of tile j-2 done)
             if (j >= 1) tc::mbar_wait(empty + g, (uint32_t)((j - 1) & 1));

@@ -29,12 +29,14 @@ def can_fuse(cfg: QuantConfig, d: int) -> bool:
     return d in FUSED_DIMS and (cfg.passthrough or cfg.group is None or cfg.group == d)
 
 
-# None = by the size of the gathered table: split while E fits in L2 (Amazon
-# shape d=64: fused 229 us vs split 202 us per layer; d=128: 782 vs 488 us),
-# fused when E streams from HBM (industry shard, 28 GB table: the gather is
-# HBM-latency-bound and hides the epilogue; fused 41 vs split ~48 ms per
-# layer).  KGQ_SPLIT_LAYER=0/1 forces one path.
-SPLIT_L2_BYTES = 96 << 20
+# None = by the size of the gathered table (split at or below SPLIT_L2_BYTES).
+# Round 1 chose fused beyond L2 (industry shard, 28 GB table: fused 41 vs
+# split ~48 ms per layer); with the round-2 SpMM (one neighbour per batch,
+# 5 CTAs/SM) and epilogues the split path wins at every measured size:
+# Amazon d=64 223 vs 149 us per layer, d=128 715 vs 411 us, industry rank 7
+# step 267 vs 251 ms (peak memory 90 -> 124 GB: the H buffer), so the limit
+# is now unbounded.  KGQ_SPLIT_LAYER=0/1 forces one path.
+SPLIT_L2_BYTES = 1 << 62
 _env_split = os.environ.get("KGQ_SPLIT_LAYER")
 SPLIT_LAYER_DEFAULT = None if _env_split is None else _env_split == "1"
 
