@@ -913,15 +913,16 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
 
 // The rare exact path of layer_epilogue_tc64_kernel: one row's codes with the
 // checked division (div_a), x re-read from the SWIZZLE_128B stage.
-template <int BITS, int MODE>
+template <int BITS, int MODE, int D = 64, int C0 = 0, int NC = 8>
 __device__ __noinline__ void tc64_row_codes_exact(const uint8_t *hst, int r, float z, DivR dv, FastKey fk,
                                                  uint64_t gglob, uint64_t seed, uint64_t tid, uint32_t *cw) {
-    constexpr int D = 64, NW = 2 * BITS;
+    // calls [C0, C0 + NC) -> code words [(C0 / 4) BITS, ...) of the row, written from cw[0]
+    constexpr int NW = NC * BITS / 4, W0 = (C0 / 4) * BITS;
     constexpr float Bf = (float)((1u << BITS) - 1u);
     const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
     for (int w = 0; w < NW; w++) cw[w] = 0u;
 #pragma unroll 1
-    for (int c = 0; c < 8; c++) {
+    for (int c = C0; c < C0 + NC; c++) {
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)c);
         const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
@@ -942,7 +943,7 @@ __device__ __noinline__ void tc64_row_codes_exact(const uint8_t *hst, int r, flo
                 acc += code_bits<MODE>(sv, uf, cw64[el] >> 11) << (BITS * el);
             }
             const int bit = k0 * BITS;
-            cw[bit >> 5] |= (acc - magic_sum4<BITS>()) << (bit & 31);
+            cw[(bit >> 5) - W0] |= (acc - magic_sum4<BITS>()) << (bit & 31);
         }
     }
 }
@@ -1299,7 +1300,7 @@ static int launch_layer(int rounding, const int32_t *indptr, const int32_t *indi
 // environment selects the FFMA epilogue (bit-identical to the fused kernel).
 static bool epi_use_tc(int d) {
     const char *e = getenv("KGQ_EPI_FFMA");      // read per launch (host side, cheap)
-    return !(e && e[0] == '1') && (d == 32 || d == 64);
+    return !(e && e[0] == '1') && (d == 32 || d == 64 || d == 128);
 }
 
 
@@ -1329,6 +1330,290 @@ static int launch_epilogue_tc64(int rounding, const float *h, int64_t n_rows, co
     const int grid = (int)(tiles < kSMs ? tiles : kSMs);
     kern<<<grid, kE2Threads, Epi64Smem::bytes, s>>>(tm_h, n_rows, theta, seed, tid, tid_base, row_offset, codes,
                                                     ranges, offsets, tm_out, mask);
+    KGQ_LAUNCH_CHECK();
+    return KGQ_OK;
+}
+
+
+// K6t at d = 128 (`layer_epilogue_tc128_kernel`).  theta^T (hi | lo) cannot
+// sit in smem beside the tiles (128 KB), so J is computed transposed,
+// J^T = theta^T . H^T, with theta^T hi | lo as the TMEM A operand (loaded once
+// per CTA, lane = output column n) and H itself as the B operand: the TMA
+// stage (two 64 KB... four 128-row x 32-column SWIZZLE_128B boxes) *is* a
+// K-major SW128 operand, read as hi by the MMA (kind::tf32 ignores the low
+// mantissa bits), so only H_lo = H - trunc_tf32(H) is written, by the row
+// warps.  3 passes (theta_lo.H, theta_hi.H_lo, theta_hi.H) x 16 K steps, M =
+// 128 (n), N = 128 (rows), into one of two TMEM accumulators.
+// Warps: 0 TMA, 1 MMA, 2-9 row warps (thread = row: min / max in a first pass
+// over the stage, then the quantization of the row -- same arithmetic and
+// noise words as light_row_quantize / K1 -- streaming float4s from the stage,
+// and H_lo), 6-9 drain warps (thread = output column n: each tcgen05.ld gives
+// 32 rows of J for that column; relu; the mask words by ballot over the 32
+// columns of the warp; E' rows stored 128 B per warp instruction).
+constexpr int kE8Threads = 448;
+struct Epi128Smem {
+    static constexpr uint32_t HS = 128 * 128 * 4;        // one H tile (64 KB): 4 boxes of 16 KB
+    static constexpr uint32_t LO = 2 * HS;               // H_lo (64 KB) after the 2-stage ring
+    static constexpr uint32_t BAR = 3 * HS;
+    static constexpr size_t bytes = (size_t)BAR + 96 + 2 * 512 * 4 + 1024;
+};
+constexpr uint32_t kE8Th = 0, kE8J = 256;             // TMEM: theta^T hi [0,128) lo [128,256); J^T 2 x 128
+
+template <int BITS, int MODE>
+__global__ void __launch_bounds__(kE8Threads, 1)
+layer_epilogue_tc128_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_rows, const float *__restrict__ theta,
+                            uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base, int64_t row_offset,
+                            uint8_t *__restrict__ codes, float *__restrict__ ranges, float *__restrict__ offsets,
+                            float *__restrict__ e_next, uint32_t *__restrict__ mask) {
+    constexpr int D = 128, M = 128, RB = D * BITS / 8;
+    constexpr int NW = BITS >= 32 ? 1 : 4 * BITS;                 // 32-bit code words per row
+    constexpr float Bf = (float)((1u << (BITS < 32 ? BITS : 1)) - 1u);
+    using S = Epi128Smem;
+    extern __shared__ uint8_t e8_raw[];
+    uint8_t *sm = e8_raw + ((1024u - (tc::smem_u32(e8_raw) & 1023u)) & 1023u);
+    uint8_t *lo_buf = sm + S::LO;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S::BAR);
+    uint64_t *hfull = bar, *hempty = bar + 2, *lofull = bar + 4, *loempty = bar + 5, *jfull = bar + 6, *jempty = bar + 8;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 10);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int i = 0; i < 2; i++) { tc::mbar_init(hfull + i, 1); tc::mbar_init(hempty + i, 1); }
+        tc::mbar_init(lofull, 256);
+        tc::mbar_init(loempty, 1);
+        for (int i = 0; i < 2; i++) { tc::mbar_init(jfull + i, 1); tc::mbar_init(jempty + i, 128); }
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    // theta^T hi | lo into TMEM: lane n holds A(n, k) = theta[k][n], k = 0..127
+    if (warp >= 2 && warp < 6) {
+        const int n = 32 * (warp & 3) + lane;
+        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + kE8Th;
+#pragma unroll 1
+        for (int kb = 0; kb < D; kb += 8) {
+            float hi[8], lo[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) tc::split_tf32_fast(__ldg(theta + (kb + e) * D + n), hi[e], lo[e]);
+            tc::tmem_st8(ta + (uint32_t)kb, hi);
+            tc::tmem_st8(ta + 128u + (uint32_t)kb, lo);
+        }
+        tc::tmem_st_wait();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const int64_t n_tiles = (n_rows + M - 1) / M;
+    const int nj = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);   // >= 1 (grid <= n_tiles)
+    auto tile_of = [&](int j) { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            for (int j = 0; j < nj; j++) {
+                const int st = j & 1;
+                if (j >= 2) tc::mbar_wait_sleep(hempty + st, (uint32_t)(((j >> 1) - 1) & 1));
+                uint8_t *dst = sm + st * S::HS;
+                tma::expect_tx(hfull + st, S::HS);
+                const int r0 = (int)(tile_of(j) * M);
+#pragma unroll
+                for (int bx = 0; bx < 4; bx++) tma::load_2d(dst + bx * (S::HS / 4), &tm_h, 32 * bx, r0, hfull + st);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer ------------------------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
+            const uint32_t lob = tc::smem_u32(lo_buf);
+            for (int j = 0; j < nj; j++) {
+                const int st = j & 1, b = j & 1;
+                tc::mbar_wait(hfull + st, (uint32_t)((j >> 1) & 1));
+                tc::mbar_wait(lofull, (uint32_t)(j & 1));
+                if (j >= 2) tc::mbar_wait(jempty + b, (uint32_t)(((j >> 1) - 1) & 1));
+                tc::fence_after();
+                const uint32_t hb = tc::smem_u32(sm + st * S::HS);
+                const uint32_t dd = tmem + kE8J + 128u * b;
+#pragma unroll
+                for (int p = 0; p < 3; p++) {                 // theta_lo.H, theta_hi.H_lo, theta_hi.H
+                    const uint32_t ta = tmem + kE8Th + (p == 0 ? 128u : 0u);
+                    const uint32_t bsrc = p == 1 ? lob : hb;
+#pragma unroll
+                    for (int ks = 0; ks < D / 8; ks++)
+                        tc::mma_tf32_ts(dd, ta + 8u * ks, tc::kmajor_sw128_desc(bsrc, ks, M), idesc, (p | ks) != 0);
+                }
+                tc::commit(hempty + st);
+                tc::commit(loempty);
+                tc::commit(jfull + b);
+            }
+        }
+        __syncwarp();
+    } else if (warp < 10) {
+        // ------------------- row warps (thread = half a row: 64 columns) -------------------
+        const int q = warp & 3, half = (warp - 2) >> 2, r = 32 * q + lane;
+        constexpr int HW = NW / 2 > 0 ? NW / 2 : 1;                     // code words per half row
+        float *mm = reinterpret_cast<float *>(bar + 12);               // [2 parity][2 half][2 min|max][128]
+        if (tid_base) tid += __ldg(tid_base);
+        const FastKey fk = make_fast_key(seed, tid);
+        for (int j = 0; j < nj; j++) {
+            const int st = j & 1;
+            const int64_t row = tile_of(j) * M + r;
+            const bool active = row < n_rows;
+            tc::mbar_wait(hfull + st, (uint32_t)((j >> 1) & 1));
+            const uint8_t *hst = sm + st * S::HS;
+            float x[64];
+#pragma unroll
+            for (int c4 = 0; c4 < 16; c4++) {
+                const int k = 64 * half + 4 * c4;
+                const float4 v = *reinterpret_cast<const float4 *>(hst + (k >> 5) * (S::HS / 4) + tma::box_off(r, k & 31));
+                x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+            }
+            if (j >= 1) tc::mbar_wait(loempty, (uint32_t)((j - 1) & 1));      // MMA of j-1 read H_lo
+#pragma unroll
+            for (int c4 = 0; c4 < 16; c4++) {                              // H_lo for the MMA (H is the hi operand)
+                const int k = 64 * half + 4 * c4;
+                float lo4[4];
+#pragma unroll
+                for (int el = 0; el < 4; el++) {
+                    const float xv = x[4 * c4 + el];
+                    lo4[el] = __fsub_rn(xv, __uint_as_float(__float_as_uint(xv) & 0xFFFFE000u));
+                }
+                *reinterpret_cast<float4 *>(lo_buf + (k >> 5) * (S::HS / 4) + tma::box_off(r, k & 31)) =
+                    make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(lofull);
+            if constexpr (BITS != 32) {
+                // min / max of the half (exact, order-free), then of the row through smem
+                float mn4[4], mx4[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) { mn4[u] = x[u]; mx4[u] = x[u]; }
+#pragma unroll
+                for (int k = 4; k < 64; k++) { mn4[k & 3] = fminf(mn4[k & 3], x[k]); mx4[k & 3] = fmaxf(mx4[k & 3], x[k]); }
+                float *mp = mm + (j & 1) * 512;
+                mp[half * 256 + r] = fminf(fminf(mn4[0], mn4[1]), fminf(mn4[2], mn4[3]));
+                mp[half * 256 + 128 + r] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+                tma::named_sync(1, 256);
+                const float z = fminf(mp[r], mp[256 + r]);
+                const float rr = __fsub_rn(fmaxf(mp[128 + r], mp[384 + r]), z);
+                const DivR dv = make_div(rr);
+                const uint64_t gglob = (uint64_t)(row_offset + row);
+                uint32_t cw[HW];
+#pragma unroll
+                for (int w = 0; w < HW; w++) cw[w] = 0u;
+                if (rr > 0.0f) {
+                    bool slow = !dv.fast;
+                    const uint32_t kc = MODE == KGQ_ROUND_SR_FAST ? carrier_const() : 0u;
+#pragma unroll
+                    for (int cc = 0; cc < 8; cc++) {         // fast-noise call c = 8 half + cc
+                        const int c = 8 * half + cc;
+                        uint4 rnd = make_uint4(0, 0, 0, 0);
+                        if (MODE == KGQ_ROUND_SR_FAST) rnd = fast_call(fk, gglob, (uint32_t)c);
+                        const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const int kl = 32 * (cc >> 2) + 4 * (cc & 3) + 16 * h;   // column within the half
+                            u64x4 r64 = {0, 0, 0, 0};
+                            if (MODE == KGQ_ROUND_SR_COMPAT)
+                                r64 = philox4x64_10(gglob * (uint64_t)(D / 4) + (uint64_t)((64 * half + kl) >> 2) + 1ull,
+                                                    0, 0, 0, seed, tid);
+                            const uint64_t cw64[4] = {r64.x, r64.y, r64.z, r64.w};
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int el = 0; el < 4; el++) {
+                                const float a = __fsub_rn(x[kl + el], z);
+                                slow |= (__float_as_uint(a) - 1u) < dv.thr_m1;      // 0 < a < threshold
+                                const float sv = __fmul_rn(div_a_unguarded(dv, a), Bf);
+                                const float uf = h ? u16_carrier_hi(rw[el], kc) : u16_carrier_lo(rw[el], kc);
+                                acc += code_bits<MODE>(sv, uf, cw64[el] >> 11) << (BITS * el);
+                            }
+                            const int bit = kl * BITS;
+                            cw[bit >> 5] |= (acc - magic_sum4<BITS>()) << (bit & 31);
+                        }
+                    }
+                    if (slow) {
+                        if (half == 0) tc64_row_codes_exact<BITS, MODE, 128, 0, 8>(hst, r, z, dv, fk, gglob, seed, tid, cw);
+                        else tc64_row_codes_exact<BITS, MODE, 128, 8, 8>(hst, r, z, dv, fk, gglob, seed, tid, cw);
+                    }
+                }
+                if (active) {
+                    uint32_t *crow = reinterpret_cast<uint32_t *>(codes + row * RB) + HW * half;
+                    if constexpr (HW % 4 == 0) {
+#pragma unroll
+                        for (int w = 0; w < HW; w += 4)
+                            *reinterpret_cast<uint4 *>(crow + w) = make_uint4(cw[w], cw[w + 1], cw[w + 2], cw[w + 3]);
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < HW; w += 2)
+                            *reinterpret_cast<uint2 *>(crow + w) = make_uint2(cw[w], cw[w + 1]);
+                    }
+                    if (half == 0) {
+                        ranges[row] = rr;
+                        offsets[row] = z;
+                    }
+                }
+            }
+        }
+    } else {
+        // --------------------------- drain warps (thread = column n) ---------------------------
+        const int q = warp & 3, n = 32 * q + lane;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        for (int j = 0; j < nj; j++) {
+            const int b = j & 1;
+            tc::mbar_wait(jfull + b, (uint32_t)((j >> 1) & 1));
+            tc::fence_after();
+            const int64_t r0 = tile_of(j) * M;
+#pragma unroll 1
+            for (int cb = 0; cb < M; cb += 32) {
+                float v[32];
+                tc::tmem_ld32(tmem + lane_addr + kE8J + 128u * b + (uint32_t)cb, v);
+                if (cb == M - 32) {
+                    tc::fence_before();
+                    tc::mbar_arrive(jempty + b);
+                }
+                uint32_t myword = 0;
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, v[i] > 0.0f);   // row r0+cb+i, columns 32q..
+                    if (lane == i) myword = bal;
+                    const int64_t row = r0 + cb + i;
+                    if (row < n_rows) e_next[row * D + n] = relu_nan(v[i]);
+                }
+                const int64_t row = r0 + cb + lane;
+                if (row < n_rows) mask[row * (D / 32) + q] = myword;
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free(tmem, 512);
+}
+
+template <int BITS>
+static int launch_epilogue_tc128(int rounding, const float *h, int64_t n_rows, const float *theta, uint64_t seed,
+                                 uint64_t tid, const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,
+                                 float *ranges, float *offsets, float *e_next, uint32_t *mask, cudaStream_t s) {
+    void (*kern)(const CUtensorMap, int64_t, const float *, uint64_t, uint64_t, const uint64_t *, int64_t,
+                 uint8_t *, float *, float *, float *, uint32_t *);
+    switch (rounding) {
+        case KGQ_ROUND_NEAREST: kern = layer_epilogue_tc128_kernel<BITS, KGQ_ROUND_NEAREST>; break;
+        case KGQ_ROUND_SR_FAST: kern = layer_epilogue_tc128_kernel<BITS, KGQ_ROUND_SR_FAST>; break;
+        case KGQ_ROUND_SR_COMPAT: kern = layer_epilogue_tc128_kernel<BITS, KGQ_ROUND_SR_COMPAT>; break;
+        default: return KGQ_ERR_INVALID_ARG;
+    }
+    static bool smem_set[3] = {false, false, false};
+    if (!smem_set[rounding]) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Epi128Smem::bytes);
+        if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+        smem_set[rounding] = true;
+    }
+    CUtensorMap tm_h;
+    if (!tma::make_rowmajor_f32(&tm_h, h, (uint64_t)n_rows, 128, 128)) return KGQ_ERR_CUDA;
+    const int64_t tiles = (n_rows + 127) / 128;
+    const int grid = (int)(tiles < kSMs ? tiles : kSMs);
+    kern<<<grid, kE8Threads, Epi128Smem::bytes, s>>>(tm_h, n_rows, theta, seed, tid, tid_base, row_offset, codes,
+                                                     ranges, offsets, e_next, mask);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
 }
@@ -1378,6 +1663,11 @@ static int launch_epilogue(int rounding, const float *h, int64_t n_rows, const f
     if constexpr (D == 32 || D == 64) {
         if (epi_use_tc(D))
             return launch_epilogue_tc<D, BITS>(rounding, h, n_rows, theta, seed, tid, tid_base, row_offset,
+                                               codes, ranges, offsets, e_next, mask, s);
+    }
+    if constexpr (D == 128) {
+        if (epi_use_tc(D) && ((((uintptr_t)h) | ((uintptr_t)codes)) & 15u) == 0)
+            return launch_epilogue_tc128<BITS>(rounding, h, n_rows, theta, seed, tid, tid_base, row_offset,
                                                codes, ranges, offsets, e_next, mask, s);
     }
     const size_t smem = EpiTile<D>::smem;

@@ -175,7 +175,7 @@ def test_split_layer_bit_identical_to_fused(d):
     """spmm_kernel + the FFMA epilogue (KGQ_EPI_FFMA=1) produce the same bytes
     as the single fused kernel: E_next, codes, ranges, offsets, mask, at every
     bit width and rounding mode, with hub (CTA-path) rows and a row offset.
-    The default split epilogue at d <= 64 computes J on tcgen05 (K6t): the
+    The default split epilogue computes J on tcgen05 (K6t, every d): the
     quantized context is still bit-identical (it depends on H only); E_next
     agrees to fp32 rounding and the mask only differs where J is ~0."""
     import os
