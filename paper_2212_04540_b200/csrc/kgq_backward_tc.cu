@@ -208,16 +208,37 @@ layer_backward_tc_kernel(const __grid_constant__ CUtensorMap tm_gr, const __grid
             uint32_t v[16];
             tc::tmem_ld16_nowait(tmem + lane_addr + kTmDh + 64u * b + 16u * cq, v);
             tc::tmem_ld_wait();
-            const int64_t row = ((int64_t)blockIdx.x + (int64_t)jj * gridDim.x) * M + r_tile;
-            if (row < rows) {
-                float4 *dst = reinterpret_cast<float4 *>(dh + row * D) + 4 * cq;
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-                    dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                         __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-            }
             tc::fence_before();
             tc::mbar_arrive(dhempty + b);
+            // 4 x 4 transpose of 16-byte chunks inside each quad of lanes (two
+            // xor-shuffle rounds): lane 4a + k then holds chunk k of rows
+            // 4a .. 4a + 3, so each store instruction writes 8 rows x 64
+            // contiguous bytes (8 L1 tag lookups instead of 32 for thread = row)
+            const int k = lane & 3;
+#pragma unroll
+            for (int rd = 2; rd >= 1; rd >>= 1) {
+                const bool up = (k & rd) != 0;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    if (c & rd) continue;                       // pairs (c, c + rd)
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const uint32_t send = up ? v[4 * c + e] : v[4 * (c + rd) + e];
+                        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, rd);
+                        if (up) v[4 * c + e] = recv;
+                        else v[4 * (c + rd) + e] = recv;
+                    }
+                }
+            }
+            const int64_t row0 = ((int64_t)blockIdx.x + (int64_t)jj * gridDim.x) * M + 32 * q + (lane & ~3);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int64_t row = row0 + i;
+                if (row < rows)
+                    reinterpret_cast<float4 *>(dh + row * D)[4 * cq + k] =
+                        make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                    __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+            }
         };
         if (issuer) issue_in(0);
         load_small(0);

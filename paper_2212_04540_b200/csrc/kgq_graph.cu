@@ -1388,14 +1388,17 @@ layer_epilogue_tc128_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
     // theta^T hi | lo into TMEM: lane n holds A(n, k) = theta[k][n], k = 0..127
-    if (warp >= 2 && warp < 6) {
-        const int n = 32 * (warp & 3) + lane;
-        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + kE8Th;
-#pragma unroll 1
-        for (int kb = 0; kb < D; kb += 8) {
+    if (warp >= 2 && warp < 10) {                    // 8 warps: lane quadrant warp % 4, k half (warp - 2) / 4
+        const int n = 32 * (warp & 3) + lane, k0 = 64 * ((warp - 2) >> 2);
+        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + kE8Th + (uint32_t)k0;
+        float tv[64];                                // all loads in flight at once (L2 latency once)
+#pragma unroll
+        for (int e = 0; e < 64; e++) tv[e] = __ldg(theta + (k0 + e) * D + n);
+#pragma unroll
+        for (int kb = 0; kb < 64; kb += 8) {
             float hi[8], lo[8];
 #pragma unroll
-            for (int e = 0; e < 8; e++) tc::split_tf32_fast(__ldg(theta + (kb + e) * D + n), hi[e], lo[e]);
+            for (int e = 0; e < 8; e++) tc::split_tf32_fast(tv[kb + e], hi[e], lo[e]);
             tc::tmem_st8(ta + (uint32_t)kb, hi);
             tc::tmem_st8(ta + 128u + (uint32_t)kb, lo);
         }
