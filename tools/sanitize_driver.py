@@ -54,7 +54,7 @@ for d in (32, 64, 128):
     kgq.spmm(A, e)
     kgq.relu(e)
 
-# K6 / K6s fused layer forward (fused and split), K7 backward (tcgen05 d=64, FFMA d=32/128),
+# K6 fused layer forward and the split epilogues (K6t tcgen05 d=32/64/128), K7 backward (tcgen05 d=64/128, FFMA d=32),
 # BPR, scatter/gather, Adam + health check: a few training steps of a toy model
 from paper_2212_04540_b200 import data as D  # noqa: E402
 ds = D.reference_dataset("default")
