@@ -219,7 +219,7 @@ using namespace kgq;
 
 // d = 64 and 128: the tcgen05 kernels (kgq_backward_tc.cu) by default;
 // KGQ_BWD_TC=0 selects the FFMA kernel below (read once).  Amazon shape,
-// inside the training step: 38.6 us vs 110 us (d = 64); 105 vs 337 us (d = 128).
+// inside the training step: 31.1 us vs 110 us (d = 64); 105 vs 337 us (d = 128).
 int kgq_launch_layer_backward_tc(const float *g_read, const float *g_e, const uint32_t *mask,
                                  const uint8_t *codes, const float *ranges, const float *offsets,
                                  int64_t rows, int32_t d, int32_t bits, const float *theta, float *dh,
