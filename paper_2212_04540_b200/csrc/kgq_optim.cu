@@ -21,8 +21,30 @@ __global__ void __launch_bounds__(256)
 adam_vec_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
                 float4 *__restrict__ v, int64_t n4, AdamScalars a, const int64_t *__restrict__ status) {
     if (status && *(volatile const int64_t *)status) return;   // a step failed: no update
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    // two float4 of each array per thread per iteration (8 loads in flight)
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + nthr < n4; i += 2 * nthr) {
+        float4 pp[2], mm[2], vv[2], gg[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            pp[u] = p[i + u * nthr];
+            mm[u] = m[i + u * nthr];
+            vv[u] = v[i + u * nthr];
+            gg[u] = ldg_stream(g + i + u * nthr);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            adam_elem(pp[u].x, gg[u].x, mm[u].x, vv[u].x, a);
+            adam_elem(pp[u].y, gg[u].y, mm[u].y, vv[u].y, a);
+            adam_elem(pp[u].z, gg[u].z, mm[u].z, vv[u].z, a);
+            adam_elem(pp[u].w, gg[u].w, mm[u].w, vv[u].w, a);
+            p[i + u * nthr] = pp[u];
+            m[i + u * nthr] = mm[u];
+            v[i + u * nthr] = vv[u];
+        }
+    }
+    if (i < n4) {
         float4 pp = p[i], mm = m[i], vv = v[i];
         const float4 gg = ldg_stream(g + i);
         adam_elem(pp.x, gg.x, mm.x, vv.x, a);
@@ -47,8 +69,30 @@ adam_vec_dev_kernel(float4 *__restrict__ p, const float4 *__restrict__ g, float4
     const int64_t t = __ldg(step_ptr);
     a.c1 = __ldg(c12 + 2 * t);
     a.c2 = __ldg(c12 + 2 * t + 1);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    // two float4 of each array per thread per iteration (8 loads in flight)
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + nthr < n4; i += 2 * nthr) {
+        float4 pp[2], mm[2], vv[2], gg[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            pp[u] = p[i + u * nthr];
+            mm[u] = m[i + u * nthr];
+            vv[u] = v[i + u * nthr];
+            gg[u] = ldg_stream(g + i + u * nthr);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            adam_elem(pp[u].x, gg[u].x, mm[u].x, vv[u].x, a);
+            adam_elem(pp[u].y, gg[u].y, mm[u].y, vv[u].y, a);
+            adam_elem(pp[u].z, gg[u].z, mm[u].z, vv[u].z, a);
+            adam_elem(pp[u].w, gg[u].w, mm[u].w, vv[u].w, a);
+            p[i + u * nthr] = pp[u];
+            m[i + u * nthr] = mm[u];
+            v[i + u * nthr] = vv[u];
+        }
+    }
+    if (i < n4) {
         float4 pp = p[i], mm = m[i], vv = v[i];
         const float4 gg = ldg_stream(g + i);
         adam_elem(pp.x, gg.x, mm.x, vv.x, a);
@@ -99,9 +143,22 @@ check_finite_kernel(CheckList L, int count, int code0, const int64_t *__restrict
         bool any = false;
         if ((((uintptr_t)x) & 15u) == 0) {
             const int64_t n4 = n >> 2;
-            for (int64_t i = tid0; i < n4; i += nthr) {
-                const float4 v = ldg_stream(reinterpret_cast<const float4 *>(x) + i);
-                // x - x is NaN exactly for inf / NaN inputs
+            const float4 *x4 = reinterpret_cast<const float4 *>(x);
+            // x - x is NaN exactly for inf / NaN inputs; 8 independent loads in
+            // flight per thread (one per iteration left the scan latency-bound)
+            constexpr int U = 8;
+            int64_t i = tid0;
+            for (; i + (U - 1) * nthr < n4; i += U * nthr) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) v[u] = ldg_stream(x4 + i + u * nthr);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    any |= !(__fsub_rn(v[u].x, v[u].x) == 0.0f) | !(__fsub_rn(v[u].y, v[u].y) == 0.0f) |
+                           !(__fsub_rn(v[u].z, v[u].z) == 0.0f) | !(__fsub_rn(v[u].w, v[u].w) == 0.0f);
+            }
+            for (; i < n4; i += nthr) {
+                const float4 v = ldg_stream(x4 + i);
                 any |= !(__fsub_rn(v.x, v.x) == 0.0f) | !(__fsub_rn(v.y, v.y) == 0.0f) |
                        !(__fsub_rn(v.z, v.z) == 0.0f) | !(__fsub_rn(v.w, v.w) == 0.0f);
             }
