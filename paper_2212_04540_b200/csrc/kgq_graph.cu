@@ -1068,6 +1068,21 @@ layer_epilogue_tc64_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_r
                 const float4 v = *reinterpret_cast<const float4 *>(hst + (c4 >> 3) * (S::HS / 2) + tma::box_off(r, 4 * c4));
                 x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
             }
+            // ---- H hi | lo into TMEM (A of J), first, so the MMAs run while the row is quantized ----
+            {
+                const uint32_t ta = tmem + lane_addr + kE2A + 128u * s;
+#pragma unroll
+                for (int cb = 0; cb < D; cb += 8) {
+                    float hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; e++) tc::split_tf32_fast(x[cb + e], hi[e], lo[e]);
+                    tc::tmem_st8(ta + (uint32_t)cb, hi);
+                    tc::tmem_st8(ta + 64u + (uint32_t)cb, lo);
+                }
+                tc::tmem_st_wait();
+                tc::fence_before();
+                tc::mbar_arrive(afull + s);
+            }
             if constexpr (BITS != 32) {
                 // ---- quantize the row (light_row_quantize's arithmetic and noise) ----
                 // min / max as a tree (exact, order-free); the division as the
@@ -1136,21 +1151,6 @@ layer_epilogue_tc64_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_r
                 }
             }
             tc::mbar_arrive(hempty + st);                 // the stage is no longer read
-            // ---- H hi | lo into TMEM (A of J), then the MMA warp takes it ----
-            {
-                const uint32_t ta = tmem + lane_addr + kE2A + 128u * s;
-#pragma unroll
-                for (int cb = 0; cb < D; cb += 8) {
-                    float hi[8], lo[8];
-#pragma unroll
-                    for (int e = 0; e < 8; e++) tc::split_tf32_fast(x[cb + e], hi[e], lo[e]);
-                    tc::tmem_st8(ta + (uint32_t)cb, hi);
-                    tc::tmem_st8(ta + 64u + (uint32_t)cb, lo);
-                }
-                tc::tmem_st_wait();
-                tc::fence_before();
-                tc::mbar_arrive(afull + s);
-            }
             // ---- drain J: relu, mask words, E' into the box stage ----
             if (leader) tma::store_wait_read<0>();          // previous tile's E' store has read the stage
             tma::named_sync(1 + s, 128);
