@@ -1480,7 +1480,11 @@ layer_epilogue_tc128_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_
 #pragma unroll
                 for (int el = 0; el < 4; el++) {
                     const float xv = x[4 * c4 + el];
-                    lo4[el] = __fsub_rn(xv, __uint_as_float(__float_as_uint(xv) & 0xFFFFE000u));
+                    // x - trunc_tf32(x) has up to 13 significant bits; rounded to
+                    // tf32 here so the MMA does not truncate it again (2^-22 |x|
+                    // per product instead of 2^-20)
+                    const float r = __fsub_rn(xv, __uint_as_float(__float_as_uint(xv) & 0xFFFFE000u));
+                    lo4[el] = __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
                 }
                 *reinterpret_cast<float4 *>(lo_buf + (k >> 5) * (S::HS / 4) + tma::box_off(r, k & 31)) =
                     make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
