@@ -457,6 +457,46 @@ def test_fused_layer_backward_matches_fp64(d, bits, terms):
     np.testing.assert_allclose(dth.cpu().numpy(), ref_dth, rtol=1e-4, atol=1e-4 * np.sqrt(rows))
 
 
+@pytest.mark.parametrize("d,bits,sparse", [(64, 2, False), (64, 2, True), (64, 32, False), (64, 32, True),
+                                           (128, 2, False), (128, 8, False), (128, 32, False)])
+def test_fused_layer_backward_many_tiles_per_cta(d, bits, sparse):
+    """The persistent tcgen05 layer backward (K7) where every CTA walks
+    several tiles (slot / TMEM double buffers and barrier phases wrap) with a
+    partial last tile, dense or compact (SparseRows) g_read: dH and dtheta vs
+    float64, and bit-identical on a second call (fixed-order reductions)."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import functional as F
+    rng = np.random.default_rng(d + bits)
+    rows = 148 * 128 * 4 + 77
+    x = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    if bits == 32:
+        q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=32), None)
+    else:
+        q = kgq.quantize_tensor(x, kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(1), tensor_id=2)
+    j = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    _, mask = kgq.relu(j)
+    ge = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    th = torch.from_numpy((rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
+    if sparse:              # a batch's readout gradient: ~3 % of the rows, the rest +0
+        touched = torch.from_numpy(np.sort(rng.choice(rows, rows // 32, replace=False))).cuda()
+        rowmap = torch.full((rows,), -1, dtype=torch.int32, device="cuda")
+        rowmap[touched] = torch.arange(len(touched), dtype=torch.int32, device="cuda")
+        vals = torch.from_numpy(rng.standard_normal((len(touched), d), dtype=np.float32)).cuda()
+        gr = F.SparseRows(rowmap, vals, rows)
+        gr_dense = torch.zeros((rows, d), device="cuda")
+        gr_dense[touched] = vals
+    else:
+        gr = gr_dense = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).cuda()
+    dth, dh = F.layer_backward(gr, ge, mask, q, th)
+    dth2, dh2 = F.layer_backward(gr, ge, mask, q, th)
+    assert torch.equal(dth, dth2) and torch.equal(dh, dh2)
+    gj = ((gr_dense + ge) * (j > 0)).double()
+    hh = (x if bits == 32 else kgq.dequantize_tensor(q)).double()
+    np.testing.assert_allclose(dh.cpu().numpy(), (gj @ th.double().t()).cpu().numpy(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(dth.cpu().numpy(), (hh.t() @ gj).cpu().numpy(), rtol=1e-4,
+                               atol=1e-4 * np.sqrt(rows))
+
+
 @pytest.mark.gpu
 def test_industry_generator_on_device_matches_host_adjacency():
     """industry.IndustryGraph on cuda at a small shape: degrees and row blocks
