@@ -137,6 +137,35 @@ def test_spmm_hub_rows_bit_exact(d):
     assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("name", ["amazon", "lastfm"])
+@pytest.mark.parametrize("d", [64, 128])
+def test_spmm_full_dataset_bit_exact(name, d):
+    """K4 at BASELINE sizes (the Amazon-book and Last-FM adjacency as the
+    reference builds them: 6.43M / 5.37M nnz, hub rows up to 4,644 / 8,324
+    nonzeros) == the C oracle's ascending-column fp32 chain, bit for bit; and
+    the split layer's quantized context == a standalone K1 quantize of that H
+    (the epilogue's codes / R / Z at every row of the dataset)."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import functional as F
+    ds = D.reference_dataset(name)
+    ip, ix, vv = D.adjacency_arrays(ds)
+    A = D.build_adjacency(ds, "cuda")
+    x = np.random.default_rng(d).standard_normal((len(ip) - 1, d), dtype=np.float32)
+    xt = torch.from_numpy(x).cuda()
+    out = kgq.spmm(A, xt).cpu().numpy()
+    ref = orc.spmm_csr(ip, ix, vv, x)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+    th = torch.from_numpy((np.random.default_rng(1).standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)).cuda()
+    cfg = kgq.QuantConfig(bits=2, rng="fast")
+    _, _, q1, h1 = F.graph_conv_forward(A, xt, th, cfg, kgq.RandomStream(3), 4, split=True, want_h=True)
+    assert np.array_equal(h1.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    q2 = kgq.quantize_tensor(h1, cfg, kgq.RandomStream(3), tensor_id=4)
+    assert torch.equal(q1.codes, q2.codes)
+    assert torch.equal(q1.ranges.view(torch.int32), q2.ranges.view(torch.int32))
+    assert torch.equal(q1.offsets.view(torch.int32), q2.offsets.view(torch.int32))
+
+
 def test_fused_layer_matches_unfused_and_oracle():
     """The fused kernel's H is the bit-exact SpMM and its codes equal a
     standalone quantize of that H; J within fp32 GEMM tolerance."""
