@@ -259,7 +259,7 @@ __device__ __forceinline__ float heavy_spmm_row(const int32_t *__restrict__ indp
 // continues its ascending-column chain over its nonzeros [seg_beg, seg_end)
 // from the running sums already in out (zeroed before the first phase), so
 // the last phase leaves exactly the chain of the whole row.
-template <int D, bool SEG = false>
+template <int D, bool SEG = false, int BATCH = KGQ_SPMM_BATCH>
 __global__ void __launch_bounds__(256, KGQ_SPMM_MINB)
 spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indices,
             const float *__restrict__ vals, int64_t n_rows, const int32_t *__restrict__ row_order,
@@ -293,7 +293,7 @@ spmm_kernel(const int32_t *__restrict__ indptr, const int32_t *__restrict__ indi
             acc[0] = active ? o[fa] : make_float4(0.f, 0.f, 0.f, 0.f);
             acc[1] = active ? o[fb] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        rg_spmm_row<D, false, KGQ_SPMM_BATCH>(indptr, indices, vals, x, row, active, gl, acc,
+        rg_spmm_row<D, false, BATCH>(indptr, indices, vals, x, row, active, gl, acc,
                                               SEG ? seg_beg : nullptr, SEG ? seg_end : nullptr);
         if (active) {
             float4 *o = reinterpret_cast<float4 *>(out + row * D);
@@ -1193,6 +1193,22 @@ layer_epilogue_tc64_kernel(const __grid_constant__ CUtensorMap tm_h, int64_t n_r
 
 using namespace kgq;
 
+#ifndef KGQ_SPMM_BATCH_BIG
+#define KGQ_SPMM_BATCH_BIG 2
+#endif
+// The gathered table is taken to be HBM-resident when the output block alone
+// exceeds 96 MB (the table is at least the block); KGQ_SPMM_BIG=0/1 forces
+// the choice (read once).
+static bool spmm_big_table(int64_t n_rows, int d) {
+    static int force = -2;
+    if (force == -2) {
+        const char *e = getenv("KGQ_SPMM_BIG");
+        force = e ? (e[0] == '1' ? 1 : 0) : -1;
+    }
+    if (force >= 0) return force == 1;
+    return n_rows * (int64_t)d * 4 > ((int64_t)96 << 20);
+}
+
 static inline int light_blocks(int64_t n_light, int rpw, int per_sm) {
     int64_t warps = (n_light + rpw - 1) / rpw;
     int64_t b = (warps + 7) / 8;
@@ -1214,13 +1230,25 @@ static int launch_spmm(const int32_t *indptr, const int32_t *indices, const floa
                        float *out, cudaStream_t s, const int32_t *seg_beg = nullptr,
                        const int32_t *seg_end = nullptr) {
     const size_t smem = n_heavy ? RG<D>::ring_bytes : 0;
-    static size_t smem_set = 0;
+    static size_t smem_set = 0, smem_set_big = 0;
+    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 16);
+    if (spmm_big_table(n_rows, D)) {
+        // gathered rows come from HBM, not L2: keep more neighbour rows in
+        // flight per row group (Little's law on the DRAM latency)
+        if (smem > smem_set_big) {
+            cudaError_t ea = ensure_smem(spmm_kernel<D, SEG, KGQ_SPMM_BATCH_BIG>, smem);
+            if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
+            smem_set_big = smem;
+        }
+        spmm_kernel<D, SEG, KGQ_SPMM_BATCH_BIG><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order,
+                                                                       n_heavy, x, out, seg_beg, seg_end);
+        return KGQ_OK;
+    }
     if (smem > smem_set) {
         cudaError_t ea = ensure_smem(spmm_kernel<D, SEG>, smem);
         if (ea != cudaSuccess) return kgq_set_cuda_error(ea);
         smem_set = smem;
     }
-    const int grid = (int)n_heavy + light_blocks(n_rows - n_heavy, RG<D>::RPW, 16);
     spmm_kernel<D, SEG><<<grid, 256, smem, s>>>(indptr, indices, vals, n_rows, row_order, n_heavy, x, out,
                                                 seg_beg, seg_end);
     return KGQ_OK;

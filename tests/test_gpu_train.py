@@ -677,6 +677,35 @@ print("ok")
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+def test_spmm_big_table_variant_bit_exact_subprocess():
+    """The SpMM instantiation for HBM-resident tables (2 neighbour rows in
+    flight per row group, chosen when the output block exceeds 96 MB;
+    KGQ_SPMM_BIG=1 forces it) == the C oracle bit for bit, hub rows included,
+    on a fresh process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+import paper_2212_04540_b200 as kgq
+from oracle import oracle as orc
+from tests.test_gpu_train import _hub_graph
+for d in (32, 64, 128):
+    a = _hub_graph(4000, d)
+    A = kgq.CSR.from_scipy(a)
+    x = np.random.default_rng(d).standard_normal((4000, d), dtype=np.float32)
+    out = kgq.spmm(A, torch.from_numpy(x).cuda()).cpu().numpy()
+    ref = orc.spmm_csr(a.indptr, a.indices, a.data, x)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32)), d
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KGQ_SPMM_BIG="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_scatter_rows_multi_edge_cases():
     """Empty lists, rows owned elsewhere (-1, skipped), a single list, d = 1
     and d = 128: bit-identical to the numpy reference sums."""
