@@ -411,6 +411,13 @@ __device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const flo
     DivR dB;
     if (BITS == 8) dB = make_div(Bf);
     const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
+    if (BITS == 8 && rfast) {
+        const Dq8 k8 = make_dq8(r, z, dB.y);
+#pragma unroll
+        for (int i = 0; i < NB; i++)
+            stg_stream(dst + 4 * i + j, dq8_word(k8, *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j)));
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
         uint32_t piece;
@@ -676,7 +683,8 @@ static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_gr
 // and stalls on the store queue).  The group's code words are loaded once
 // (coalesced u32) and each lane takes its 4*BITS bits with one shuffle; the
 // 2^b reconstruction values (b <= 4) come from a per-warp smem table built
-// with the same IEEE lut_entry; b = 8 divides per element exactly as K2 does.
+// with the same IEEE lut_entry; b = 8 uses the packed-pair Markstein division
+// (dq8_word, bit-identical to K2's scalar sequence).
 template <int G, int BITS>
 __global__ void __launch_bounds__(kThreads)
 dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
@@ -702,6 +710,7 @@ dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restric
         zn = __ldg(offsets + gg);
     };
     if (g < n_groups) fetch(g);
+    const float yB8 = BITS == 8 ? make_div(Bf).y : 0.0f;   // the reciprocal K2 uses
     for (; g < n_groups; g += stride) {
         uint32_t w[WPL];
 #pragma unroll
@@ -712,10 +721,15 @@ dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restric
             __syncwarp();
         }
         if (g + stride < n_groups) fetch(g + stride);
-        DivR dB;
-        if (BITS == 8) dB = make_div(Bf);
         const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
         float4 *dst = reinterpret_cast<float4 *>(out) + g * (G / 4);
+        if (BITS == 8 && rfast) {
+            // warp-uniform (one group per warp): packed pairs, the lane's own words
+            const Dq8 k8 = make_dq8(r, z, yB8);
+#pragma unroll
+            for (int h = 0; h < H; h++) stg_stream(dst + lane + 32 * h, dq8_word(k8, w[h < WPL ? h : 0]));
+            continue;
+        }
 #pragma unroll
         for (int h = 0; h < H; h++) {
             const int e0 = 4 * (lane + 32 * h);          // first element of my float4
@@ -733,15 +747,7 @@ dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restric
                     o[e] = z;
                 } else {
                     const float t = __fmul_rn(r, __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f));
-                    float qv;
-                    if (rfast) {
-                        const float q0 = __fmul_rn(t, dB.y);
-                        const float er = __fmaf_rn(-Bf, q0, t);
-                        qv = __fmaf_rn(dB.y, er, q0);
-                    } else {
-                        qv = __fdiv_rn(t, Bf);
-                    }
-                    o[e] = __fadd_rn(qv, z);
+                    o[e] = __fadd_rn(__fdiv_rn(t, Bf), z);     // R outside the Markstein window
                 }
             }
             stg_stream(dst + lane + 32 * h, make_float4(o[0], o[1], o[2], o[3]));

@@ -1,7 +1,8 @@
 """BASELINE configs[1] sweep (not the headline bench line): quantize and
 dequantize throughput for fp32 rows in {1M, 4M, 16M, 64M} x cols {64, 128},
-INT2/INT4/INT8, group 64/256, fast noise; algorithmic bytes / CUDA-event time
-vs the measured HBM peak.  Output: one JSON document."""
+INT2/INT4/INT8, group 64/256, fast noise (plus quantize with the reference's
+Philox4x64-10 stream, rng="compat"); algorithmic bytes / CUDA-event time vs
+the measured HBM peak.  Output: one JSON document."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -40,11 +41,22 @@ for rows in (1 << 20, 4 << 20, 16 << 20, 64 << 20):
                 torch.cuda.synchronize()
                 tq, td = a.elapsed_time(b) / reps, b.elapsed_time(c) / reps
                 gq, gd = n * bpe / tq / 1e6, n * bpe / td / 1e6
+                ccfg = kgq.QuantConfig(bits=bits, group=group, rng="compat")
+                creps = max(2, reps // 4)
+                q = kgq.quantize_tensor(x, ccfg, st, tensor_id=0)
+                torch.cuda.synchronize()
+                a.record()
+                for r in range(creps):
+                    q = kgq.quantize_tensor(x, ccfg, st, tensor_id=1 + r)
+                b.record()
+                torch.cuda.synchronize()
+                gc = n * bpe / (a.elapsed_time(b) / creps) / 1e6
                 res.append({"rows": rows, "cols": cols, "bits": bits, "group": group,
                             "quantize_GBps": round(gq, 1), "quantize_frac": round(gq / peak, 4),
-                            "dequantize_GBps": round(gd, 1), "dequantize_frac": round(gd / peak, 4)})
+                            "dequantize_GBps": round(gd, 1), "dequantize_frac": round(gd / peak, 4),
+                            "quantize_compat_GBps": round(gc, 1), "quantize_compat_frac": round(gc / peak, 4)})
                 print(res[-1], flush=True)
                 del q, out
         del x
         torch.cuda.empty_cache()
-print(json.dumps({"peak_GBps": peak, "rng": "fast", "sweep": res}))
+print(json.dumps({"peak_GBps": peak, "rng": "fast (quantize_compat_*: rng=compat)", "sweep": res}))
