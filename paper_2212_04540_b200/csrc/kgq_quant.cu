@@ -677,7 +677,7 @@ static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_gr
     return false;
 }
 
-// K2 for wide groups (G = 128 / 256): a warp per group, lane l owns float4
+// K2 for wide groups (G = 256, b <= 4): a warp per group, lane l owns float4
 // l + 32h (h < G/128), so every store instruction writes 512 contiguous bytes
 // (the 4-lanes-per-group kernel scatters 64-byte pieces 1 KB apart at G = 256
 // and stalls on the store queue).  The group's code words are loaded once
@@ -763,13 +763,15 @@ static bool dispatch_dequant_bits(int bits, const uint8_t *codes, const float *r
 #ifndef KGQ_DQ_WIDE
 #define KGQ_DQ_WIDE 1
 #endif
-    if (KGQ_DQ_WIDE && G >= 128) {
+    // warp per group only where it measured faster (A/B, 16M x 128): G = 256
+    // at b <= 4; G = 128 and b = 8 run faster 4 lanes per group (8 groups per
+    // warp tile: more bytes in flight per warp; G=128 INT8 61 % -> 94 %)
+    if (KGQ_DQ_WIDE && G >= 256 && bits <= 4) {
         const int grid = grid_for(n_groups, kWarps, 8);
         switch (bits) {
             case 1: dequantize_wide_kernel<G, 1><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
             case 2: dequantize_wide_kernel<G, 2><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
             case 4: dequantize_wide_kernel<G, 4><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-            case 8: dequantize_wide_kernel<G, 8><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
         }
         return false;
     }
