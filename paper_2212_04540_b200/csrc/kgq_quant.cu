@@ -24,7 +24,6 @@ namespace kgq {
 #endif
 constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;
-constexpr int kGroupsPerWarp = 8;      // dequantize: 4 threads per group
 
 // Thread geometry of the fast quantizer: a G-element group is handled by T
 // threads (T = 2 or 4); thread j owns float4 q in [j*Q, j*Q+Q) (Q = 4/T) of
@@ -402,10 +401,10 @@ quantize_generic_kernel(const float *__restrict__ x, int64_t n_groups, int G, in
 // bits == 8: arithmetic with the hoisted-reciprocal division.
 // ---------------------------------------------------------------------------
 // Per-group outputs of one warp tile (8 groups) from staged codes + table.
-template <int G, int BITS>
+template <int G, int BITS, int T>
 __device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const float *lt, float r, float z,
                                                    float4 *dst, int j) {
-    constexpr int NB = G / 16;
+    constexpr int NB = G / (4 * T);     // float4 per thread: thread j owns float4 T*i + j
     constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;
     constexpr float Bf = (float)PackInfo<BITS>::B;
     DivR dB;
@@ -415,16 +414,17 @@ __device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const flo
         const Dq8 k8 = make_dq8(r, z, dB.y);
 #pragma unroll
         for (int i = 0; i < NB; i++)
-            stg_stream(dst + 4 * i + j, dq8_word(k8, *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j)));
+            stg_stream(dst + T * i + j, dq8_word(k8, *reinterpret_cast<const uint32_t *>(gst + 4 * (T * i + j))));
         return;
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
+        const int f = T * i + j;        // float4 index in the group: codes 4f .. 4f+3
         uint32_t piece;
-        if (BITS == 8) piece = *reinterpret_cast<const uint32_t *>(gst + 16 * i + 4 * j);
-        else if (BITS == 4) piece = *reinterpret_cast<const uint16_t *>(gst + 8 * i + 2 * j);
-        else if (BITS == 2) piece = gst[4 * i + j];
-        else piece = (gst[2 * i + (j >> 1)] >> (4 * (j & 1))) & 0xFu;
+        if (BITS == 8) piece = *reinterpret_cast<const uint32_t *>(gst + 4 * f);
+        else if (BITS == 4) piece = *reinterpret_cast<const uint16_t *>(gst + 2 * f);
+        else if (BITS == 2) piece = gst[f];
+        else piece = (gst[f >> 1] >> (4 * (f & 1))) & 0xFu;
         float o[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -446,29 +446,34 @@ __device__ __forceinline__ void dequant_tile_store(const uint8_t *gst, const flo
                 o[e] = __fadd_rn(qv, z);
             }
         }
-        stg_stream(dst + 4 * i + j, make_float4(o[0], o[1], o[2], o[3]));
+        stg_stream(dst + f, make_float4(o[0], o[1], o[2], o[3]));
     }
 }
 
-template <int G, int BITS>
+// K2: T lanes per group (T = 4 at G <= 128, 8 at G = 256), 32/T groups per
+// warp tile; thread j of a group owns float4 T*i + j, so one store
+// instruction writes T*16-byte pieces of 32/T groups (T = 8 at G = 256: whole
+// 128-byte lines).
+template <int G, int BITS, int T>
 __global__ void __launch_bounds__(kThreads)
 dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
                      const float *__restrict__ offsets, int64_t n_groups, float *__restrict__ out) {
+    constexpr int GPW = 32 / T;                         // groups per warp tile
     constexpr int GB = G * BITS / 8;
-    constexpr int TB = kGroupsPerWarp * GB;             // code bytes per warp tile
+    constexpr int TB = GPW * GB;             // code bytes per warp tile
     constexpr int NCH = TB / 16;                        // uint4 chunks per tile
     constexpr int CPL = (NCH + 31) / 32;                // chunks per lane
     constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;   // table entries per group
     constexpr int LS = (NL == 16) ? 17 : NL;            // padded stride (bank spread)
     __shared__ __align__(16) uint8_t stage[kWarps][TB];
-    __shared__ float lut[kWarps][kGroupsPerWarp * LS];
+    __shared__ float lut[kWarps][GPW * LS];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = lane & 3, gw = lane >> 2;
+    const int j = lane % T, gw = lane / T;
     uint8_t *st = stage[warp];
     float *lt = lut[warp] + gw * LS;
 
-    const int64_t n_full = n_groups / kGroupsPerWarp;   // full tiles (software-pipelined)
+    const int64_t n_full = n_groups / GPW;   // full tiles (software-pipelined)
     const int64_t stride = (int64_t)gridDim.x * kWarps;
     int64_t tile = (int64_t)blockIdx.x * kWarps + warp;
 
@@ -480,8 +485,8 @@ dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict_
 #pragma unroll
         for (int k = 0; k < CPL; k++)
             if (lane + 32 * k < NCH) cw[k] = __ldg(src + lane + 32 * k);
-        r_n = __ldg(ranges + t * kGroupsPerWarp + gw);
-        z_n = __ldg(offsets + t * kGroupsPerWarp + gw);
+        r_n = __ldg(ranges + t * GPW + gw);
+        z_n = __ldg(offsets + t * GPW + gw);
     };
     if (tile < n_full) prefetch(tile);
     for (; tile < n_full; tile += stride) {
@@ -491,19 +496,19 @@ dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict_
         const float r = r_n, z = z_n;
         if (NL > 1) {
 #pragma unroll
-            for (int c = j; c < NL; c += 4) lt[c] = lut_entry<BITS>(r, z, c);
+            for (int c = j; c < NL; c += T) lt[c] = lut_entry<BITS>(r, z, c);
         }
         // prefetch after the table: a slow-path division call would otherwise
         // force the in-flight loads to retire
         if (tile + stride < n_full) prefetch(tile + stride);
         __syncwarp();
-        const int64_t g = tile * kGroupsPerWarp + gw;
-        dequant_tile_store<G, BITS>(st + gw * GB, lt, r, z, reinterpret_cast<float4 *>(out) + g * (G / 4), j);
+        const int64_t g = tile * GPW + gw;
+        dequant_tile_store<G, BITS, T>(st + gw * GB, lt, r, z, reinterpret_cast<float4 *>(out) + g * (G / 4), j);
         __syncwarp();
     }
     // the last partial tile (at most one in the grid)
-    if (n_groups % kGroupsPerWarp && (int64_t)blockIdx.x * kWarps + warp == n_full % stride) {
-        const int64_t g0 = n_full * kGroupsPerWarp;
+    if (n_groups % GPW && (int64_t)blockIdx.x * kWarps + warp == n_full % stride) {
+        const int64_t g0 = n_full * GPW;
         const int nvalid = (int)(n_groups - g0);
         const uint8_t *srcc = codes + g0 * GB;
         for (int b = lane * 4; b < nvalid * GB; b += 32 * 4)
@@ -512,11 +517,11 @@ dequantize_t4_kernel(const uint8_t *__restrict__ codes, const float *__restrict_
         const float r = valid ? __ldg(ranges + g0 + gw) : 0.f;
         const float z = valid ? __ldg(offsets + g0 + gw) : 0.f;
         if (NL > 1) {
-            for (int c = j; c < NL; c += 4) lt[c] = lut_entry<BITS>(r, z, c);
+            for (int c = j; c < NL; c += T) lt[c] = lut_entry<BITS>(r, z, c);
         }
         __syncwarp();
         if (valid)
-            dequant_tile_store<G, BITS>(st + gw * GB, lt, r, z,
+            dequant_tile_store<G, BITS, T>(st + gw * GB, lt, r, z,
                                         reinterpret_cast<float4 *>(out) + (g0 + gw) * (G / 4), j);
     }
 }
@@ -677,111 +682,25 @@ static bool dispatch_quant_bits(int bits, int mode, const float *x, int64_t n_gr
     return false;
 }
 
-// K2 for wide groups (G = 256, b <= 4): a warp per group, lane l owns float4
-// l + 32h (h < G/128), so every store instruction writes 512 contiguous bytes
-// (the 4-lanes-per-group kernel scatters 64-byte pieces 1 KB apart at G = 256
-// and stalls on the store queue).  The group's code words are loaded once
-// (coalesced u32) and each lane takes its 4*BITS bits with one shuffle; the
-// 2^b reconstruction values (b <= 4) come from a per-warp smem table built
-// with the same IEEE lut_entry; b = 8 uses the packed-pair Markstein division
-// (dq8_word, bit-identical to K2's scalar sequence).
-template <int G, int BITS>
-__global__ void __launch_bounds__(kThreads)
-dequantize_wide_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ ranges,
-                       const float *__restrict__ offsets, int64_t n_groups, float *__restrict__ out) {
-    constexpr int GB = G * BITS / 8;                     // code bytes per group
-    constexpr int NW = GB / 4;                           // code words per group
-    constexpr int WPL = (NW + 31) / 32;                  // words per lane
-    constexpr int H = G / 128;                           // float4 per lane
-    constexpr int NL = (BITS <= 4) ? (1 << BITS) : 1;
-    constexpr float Bf = (float)PackInfo<BITS>::B;
-    __shared__ float lut[kWarps][NL];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t stride = (int64_t)gridDim.x * kWarps;
-    int64_t g = (int64_t)blockIdx.x * kWarps + warp;
-    uint32_t cw[WPL];
-    float rn = 0.f, zn = 0.f;
-    auto fetch = [&](int64_t gg) {
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(codes + gg * GB);
-#pragma unroll
-        for (int k = 0; k < WPL; k++)
-            cw[k] = (lane + 32 * k < NW) ? __ldg(src + lane + 32 * k) : 0u;
-        rn = __ldg(ranges + gg);
-        zn = __ldg(offsets + gg);
-    };
-    if (g < n_groups) fetch(g);
-    const float yB8 = BITS == 8 ? make_div(Bf).y : 0.0f;   // the reciprocal K2 uses
-    for (; g < n_groups; g += stride) {
-        uint32_t w[WPL];
-#pragma unroll
-        for (int k = 0; k < WPL; k++) w[k] = cw[k];
-        const float r = rn, z = zn;
-        if (NL > 1) {
-            if (lane < NL) lut[warp][lane] = lut_entry<BITS>(r, z, lane);
-            __syncwarp();
-        }
-        if (g + stride < n_groups) fetch(g + stride);
-        const bool rfast = (r >= 0x1p-100f) && (r <= 0x1p100f);
-        float4 *dst = reinterpret_cast<float4 *>(out) + g * (G / 4);
-        if (BITS == 8 && rfast) {
-            // warp-uniform (one group per warp): packed pairs, the lane's own words
-            const Dq8 k8 = make_dq8(r, z, yB8);
-#pragma unroll
-            for (int h = 0; h < H; h++) stg_stream(dst + lane + 32 * h, dq8_word(k8, w[h < WPL ? h : 0]));
-            continue;
-        }
-#pragma unroll
-        for (int h = 0; h < H; h++) {
-            const int e0 = 4 * (lane + 32 * h);          // first element of my float4
-            const int bit = e0 * BITS;                   // 4*BITS bits, inside one word
-            const int wi = bit >> 5;                     // < 32 except b = 8 (then = lane + 32h)
-            const uint32_t word = __shfl_sync(0xffffffffu, w[BITS == 8 ? (h < WPL ? h : 0) : 0], wi & 31);
-            const uint32_t piece = word >> (bit & 31);
-            float o[4];
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const uint32_t c = (piece >> (BITS * e)) & PackInfo<BITS>::B;
-                if (NL > 1) {
-                    o[e] = lut[warp][c];
-                } else if (r == 0.0f) {
-                    o[e] = z;
-                } else {
-                    const float t = __fmul_rn(r, __fsub_rn(__uint_as_float(0x4B000000u | c), 8388608.0f));
-                    o[e] = __fadd_rn(__fdiv_rn(t, Bf), z);     // R outside the Markstein window
-                }
-            }
-            stg_stream(dst + lane + 32 * h, make_float4(o[0], o[1], o[2], o[3]));
-        }
-        if (NL > 1) __syncwarp();
-    }
-}
-
 template <int G>
 static bool dispatch_dequant_bits(int bits, const uint8_t *codes, const float *ranges,
                                   const float *offsets, int64_t n_groups, float *out,
                                   cudaStream_t s) {
-#ifndef KGQ_DQ_WIDE
-#define KGQ_DQ_WIDE 1
+    // lanes per group, from A/B runs on 16M x 128: 8 at G = 256 (whole 128-byte
+    // lines per store instruction; beats both 4 lanes, which scatter 64-byte
+    // pieces 1 KB apart and stall on the store queue, and a warp per group,
+    // which has too little work per warp in flight), 4 below
+#ifndef KGQ_DQ_T256
+#define KGQ_DQ_T256 8
 #endif
-    // warp per group only where it measured faster (A/B, 16M x 128): G = 256
-    // at b <= 4; G = 128 and b = 8 run faster 4 lanes per group (8 groups per
-    // warp tile: more bytes in flight per warp; G=128 INT8 61 % -> 94 %)
-    if (KGQ_DQ_WIDE && G >= 256 && bits <= 4) {
-        const int grid = grid_for(n_groups, kWarps, 8);
-        switch (bits) {
-            case 1: dequantize_wide_kernel<G, 1><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-            case 2: dequantize_wide_kernel<G, 2><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-            case 4: dequantize_wide_kernel<G, 4><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-        }
-        return false;
-    }
-    const int64_t tiles = (n_groups + kGroupsPerWarp - 1) / kGroupsPerWarp;
+    constexpr int T = G >= 256 ? KGQ_DQ_T256 : 4;
+    const int64_t tiles = (n_groups + 32 / T - 1) / (32 / T);
     const int grid = grid_for(tiles, kWarps, 8);
     switch (bits) {
-        case 1: dequantize_t4_kernel<G, 1><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-        case 2: dequantize_t4_kernel<G, 2><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-        case 4: dequantize_t4_kernel<G, 4><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
-        case 8: dequantize_t4_kernel<G, 8><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 1: dequantize_t4_kernel<G, 1, T><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 2: dequantize_t4_kernel<G, 2, T><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 4: dequantize_t4_kernel<G, 4, T><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
+        case 8: dequantize_t4_kernel<G, 8, T><<<grid, kThreads, 0, s>>>(codes, ranges, offsets, n_groups, out); return true;
     }
     return false;
 }
