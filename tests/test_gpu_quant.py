@@ -312,3 +312,24 @@ def test_configs1_whole_tensor_bit_exact(rows, cols, bits, group, mode):
     deq = kgq.dequantize_tensor(q).cpu().numpy().reshape(-1, group)
     ref = orc.dequantize(codes, ranges, offsets, group, bits, threads=threads)
     assert np.array_equal(deq.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("extra", [1, 2, 3, 5, 7])
+@pytest.mark.parametrize("group", [64, 128, 256])
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_dequantize_partial_tiles_every_lane_layout(group, bits, extra):
+    """K2 runs T lanes per group (4 at G <= 128, 8 at G = 256) over 32/T-group
+    warp tiles; group counts that leave a partial last tile, with constant
+    (R == 0), 1e-30- and 1e30-scaled groups (INT8's packed-pair fast path vs
+    the per-element division outside the Markstein window), must dequantize
+    bit-exactly like the oracle."""
+    kgq = _kgq()
+    n_groups = 8 * 37 + extra
+    x = _edge_big(n_groups, group, 1000 * bits + group + extra)
+    q = kgq.quantize_tensor(_to_dev(x), kgq.QuantConfig(bits=bits, rng="fast"), kgq.RandomStream(5),
+                            tensor_id=9)
+    codes, ranges, offsets = orc.quantize(x, group, bits, orc.MODE_SR_FAST, 5, 9)
+    _assert_q_equal(q, codes, ranges, offsets)
+    deq = kgq.dequantize_tensor(q).cpu().numpy()
+    ref = orc.dequantize(codes, ranges, offsets, group, bits)
+    assert np.array_equal(deq.view(np.uint32), ref.view(np.uint32))

@@ -36,9 +36,13 @@ for g in (32, 64, 128, 256):
     xm.copy_(x)
     q = kgq.quantize_tensor(xm, kgq.QuantConfig(bits=2, rng="fast"), kgq.RandomStream(1), tensor_id=3)
     kgq.dequantize_tensor(q)
-# a partial last tile (rows not a multiple of the warp tile)
-kgq.dequantize_tensor(kgq.quantize_tensor(torch.randn(1001, 64, device=dev), kgq.QuantConfig(bits=2, rng="fast"),
-                                          kgq.RandomStream(1), tensor_id=4))
+# a partial last tile (rows not a multiple of the warp tile), 4 and 8 lanes per group
+for g in (64, 256):
+    for bits in (2, 8):
+        xt = torch.randn(1001, g, device=dev)
+        xt[5] = 1.5                                        # a zero-range group (K2's R == 0 path)
+        kgq.dequantize_tensor(kgq.quantize_tensor(xt, kgq.QuantConfig(bits=bits, rng="fast"),
+                                                  kgq.RandomStream(1), tensor_id=4))
 
 # K4 SpMM with hub rows (CTA-per-row path) + K5 relu/mask
 n = 3000
