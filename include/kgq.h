@@ -265,6 +265,13 @@ KGQ_API int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *idx,
 KGQ_API int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
                             int64_t n_idx, int32_t d, float *out, void *stream);
 
+/* The same gather added onto a running sum: out = ((base + t_0[idx]) +
+ * t_1[idx]) + ... with base an n_idx x d row block (may alias out): the sum
+ * readout accumulated term by term as each layer output dies
+ * (model.forward_all(readout_rows=...)), bit-identical to gathering the sum. */
+KGQ_API int kgq_gather_rows_acc_f32(const float *base, const float *const *terms, int32_t n_terms,
+                            const int64_t *idx, int64_t n_idx, int32_t d, float *out, void *stream);
+
 /* One source-block phase of the pipelined SpMM (the partitioned step's
  * exchange overlap, parallel.partitioned_step overlap=True): for the n_slots
  * rows row_order[0..n_slots) (the first n_heavy get a CTA each), continue the

@@ -67,6 +67,7 @@ SIGNATURES = {
     "kgq_bpr_backward_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I32, ctypes.c_float, _P, _P, _P, _P]),
     "kgq_scatter_rows_multi_f32": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _P, _I32, _P, _P]),
     "kgq_gather_rows_sum_f32": (ctypes.c_int, [_P, _I32, _P, _I64, _I32, _P, _P]),
+    "kgq_gather_rows_acc_f32": (ctypes.c_int, [_P, _P, _I32, _P, _I64, _I32, _P, _P]),
     "kgq_topk_rows_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _P, _P]),
     "kgq_spmm_csr_seg_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _P, _P, _I32, _P, _P]),
     "kgq_batch_indices": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _P]),

@@ -351,21 +351,24 @@ extern "C" int kgq_scatter_rows_multi_f32(const int64_t *order, const int32_t *i
 constexpr int kMaxSumTerms = 8;
 struct SumTerms { const float *t[kMaxSumTerms]; };
 
-__global__ void gather_rows_sum_kernel(SumTerms terms, int n_terms, const int64_t *__restrict__ idx, int64_t n_idx,
-                                       int d, float *__restrict__ out) {
+// base (optional, n_idx x d, may alias out): a running sum of earlier terms'
+// gathered rows, added first -- ((base + t_0[idx]) + t_1[idx]) + ... -- so a
+// readout can be accumulated term by term as each layer output dies.
+__global__ void gather_rows_sum_kernel(const float *base, SumTerms terms, int n_terms,
+                                       const int64_t *__restrict__ idx, int64_t n_idx, int d, float *out) {
     const int64_t total = n_idx * d;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / d;
         const int f = (int)(e - i * d);
         const int64_t r = __ldg(idx + i);
-        float acc = __ldg(terms.t[0] + r * d + f);
-        for (int k = 1; k < n_terms; k++) acc = __fadd_rn(acc, __ldg(terms.t[k] + r * d + f));
+        float acc = base ? base[e] : __ldg(terms.t[0] + r * d + f);
+        for (int k = base ? 0 : 1; k < n_terms; k++) acc = __fadd_rn(acc, __ldg(terms.t[k] + r * d + f));
         out[e] = acc;
     }
 }
 
-extern "C" int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
-                                       int64_t n_idx, int32_t d, float *out, void *stream) {
+static int launch_gather_rows_sum(const float *base, const float *const *terms, int32_t n_terms, const int64_t *idx,
+                                  int64_t n_idx, int32_t d, float *out, void *stream) {
     if (n_terms < 1 || n_terms > kMaxSumTerms || n_idx < 0 || d < 1 || !terms) return KGQ_ERR_INVALID_ARG;
     if (n_idx == 0) return KGQ_OK;
     if (!idx || !out) return KGQ_ERR_INVALID_ARG;
@@ -375,9 +378,20 @@ extern "C" int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_term
     const int64_t total = n_idx * d;
     int64_t blocks = (total + 255) / 256;
     if (blocks > (int64_t)kSMs * 8) blocks = (int64_t)kSMs * 8;
-    gather_rows_sum_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(t, n_terms, idx, n_idx, d, out);
+    gather_rows_sum_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(base, t, n_terms, idx, n_idx, d, out);
     KGQ_LAUNCH_CHECK();
     return KGQ_OK;
+}
+
+extern "C" int kgq_gather_rows_sum_f32(const float *const *terms, int32_t n_terms, const int64_t *idx,
+                                       int64_t n_idx, int32_t d, float *out, void *stream) {
+    return launch_gather_rows_sum(nullptr, terms, n_terms, idx, n_idx, d, out, stream);
+}
+
+extern "C" int kgq_gather_rows_acc_f32(const float *base, const float *const *terms, int32_t n_terms,
+                                       const int64_t *idx, int64_t n_idx, int32_t d, float *out, void *stream) {
+    if (!base) return KGQ_ERR_INVALID_ARG;
+    return launch_gather_rows_sum(base, terms, n_terms, idx, n_idx, d, out, stream);
 }
 
 // The BPR batch's three gather index lists from one [B][3] (user, pos item,

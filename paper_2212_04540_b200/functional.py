@@ -417,6 +417,21 @@ def gather_rows_sum(terms, idx64: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def gather_rows_acc(base: torch.Tensor, terms, idx64: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """((base + terms[0][idx]) + terms[1][idx]) + ... into ``out`` (default:
+    in place on ``base``) with kgq_gather_rows_acc_f32: a gathered sum readout
+    accumulated term by term, bit-identical to gather_rows_sum over all the
+    terms."""
+    d = base.shape[1]
+    out = base if out is None else out
+    ptrs = (ctypes.c_void_p * len(terms))(*[t.data_ptr() for t in terms])
+    st = _lib.load().kgq_gather_rows_acc_f32(base.data_ptr(), ctypes.cast(ptrs, ctypes.c_void_p), len(terms),
+                                             idx64.contiguous().data_ptr(), idx64.shape[0], d, out.data_ptr(),
+                                             _lib.stream_ptr(base.device))
+    _lib.check(st, "kgq_gather_rows_acc_f32")
+    return out
+
+
 def topk_rows(scores: torch.Tensor, k: int) -> torch.Tensor:
     """Indices of the k best entries of every row of a fp32 score block, best
     first, ties by ascending column (kgq_topk_rows_f32; the stable

@@ -1247,3 +1247,62 @@ def test_pipelined_spmm_by_source_block_is_bit_identical(d, world):
                                                      row_offset=part.lo)
         assert torch.equal(e1, e2) and torch.equal(m1.packed, m2.packed)
         assert torch.equal(q1.codes, q2.codes) and torch.equal(q1.ranges, q2.ranges)
+
+
+@pytest.mark.parametrize("layers,d,bits", [(3, 64, 2), (2, 128, 8), (3, 32, 32), (1, 64, 4)])
+def test_retired_readout_step_is_bit_identical(layers, d, bits):
+    """forward_all(readout_rows=...) reduces each layer output to the batch's
+    readout rows once the next layer has read it; the step's loss, every
+    gradient, the tensor ids and the ledger are bit-identical to the step
+    that keeps all layer outputs, and the retired readout refuses to
+    materialize."""
+    kgq = _kgq()
+    from paper_2212_04540_b200 import data as D
+    from paper_2212_04540_b200 import train as T
+    from paper_2212_04540_b200.model import ModelConfig, forward_all, init_params
+    from paper_2212_04540_b200.tape import Tape, TapeUsageError
+    ds = D.synth_kg(D.SynthShape(600, 400, 1500, relations=5, interactions_per_user=20.0), seed=3)
+    adj = D.build_adjacency(ds)
+    q = kgq.QuantConfig(bits=bits, rng="fast")
+    mcfg = ModelConfig(layers=layers, dim=d, quant=q)
+    cfg = T.TrainConfig(batch_size=256, quant=q)
+    params = init_params(ds.num_nodes, mcfg, 0)
+    batch = torch.from_numpy(D.sample_negatives(ds, np.random.default_rng(1))[:256]).cuda().contiguous()
+    assert batch.dtype == torch.int32
+    outs = []
+    for retire in (True, False):
+        st = kgq.RandomStream(0)
+        if retire:                                   # the training step's path (readout_rows given)
+            tape, grads, peaks = T._record_step(ds, adj, params, mcfg, cfg, st, batch, True)
+        else:                                        # the same step with every layer output kept
+            tape = Tape(q, st)
+            readout = forward_all(tape, params, adj, mcfg, fused=True)
+            u = tape.record_gather(readout, batch[:, 0].long(), checked=True)
+            p = tape.record_gather(readout, ds.num_users + batch[:, 1].long(), checked=True)
+            n = tape.record_gather(readout, ds.num_users + batch[:, 2].long(), checked=True)
+            tape.record_bpr_loss(u, p, n, cfg.l2)
+            peaks = (tape.peak_context_bytes, tape.peak_fp32_equiv_bytes, tape.adjacency_bytes)
+            grads = tape.backward()
+        outs.append((tape.loss_tensor.clone(), {k: v.clone() for k, v in grads.items()}, peaks, st._next_tensor_id))
+    (l0, g0, p0, t0), (l1, g1, p1, t1) = outs
+    assert torch.equal(l0, l1) and p0 == p1 and t0 == t1
+    for k in g1:
+        assert torch.equal(g0[k], g1[k]), k
+    if layers > 1:
+        tape = Tape(q, kgq.RandomStream(0))
+        idx = torch.arange(10, dtype=torch.int64, device="cuda")
+        readout = forward_all(tape, params, adj, mcfg, fused=True, readout_rows=idx)
+        assert tuple(readout.index_select_rows(idx).shape) == (10, d)
+        with pytest.raises(TapeUsageError):
+            readout.value
+        with pytest.raises(TapeUsageError):
+            readout.index_select_rows(torch.arange(5, dtype=torch.int64, device="cuda"))
+    # the accumulate form of the readout gather == the one-shot sum, bit for bit
+    from paper_2212_04540_b200 import functional as F
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ts = [torch.randn(999, d, device="cuda", generator=g) * 10.0 ** k for k in range(4)]
+    idx = torch.randint(0, 999, (3000,), device="cuda", generator=g)
+    one = F.gather_rows_sum(ts, idx)
+    acc = F.gather_rows_sum(ts[:1], idx)
+    F.gather_rows_acc(acc, ts[1:3], idx)
+    assert torch.equal(F.gather_rows_acc(acc, ts[3:], idx, out=torch.empty_like(acc)), one)
