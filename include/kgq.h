@@ -223,7 +223,9 @@ KGQ_API int kgq_layer_forward_f32(const int32_t *indptr, const int32_t *indices,
  *   ctx = quantize(H) (group = d); J = H @ theta; E_next = relu(J); mask.
  * Bit-identical to the fused kernel (same lanes, noise calls, FFMA order);
  * spmm + epilogue keeps the gather kernel at full occupancy, which is faster
- * when H is L2-resident.  d in {32, 64, 128}. */
+ * when H is L2-resident.  d in {32, 64, 128}.  For bits != 32, e_next may
+ * equal h (E' written over H in place: every tile's H rows are read before
+ * its E' rows are stored); for bits == 32 H is the context and must stay. */
 KGQ_API int kgq_layer_epilogue_f32(const float *h, int64_t n_rows, int32_t d, const float *theta,
                            int32_t bits, int32_t rounding, uint64_t seed, uint64_t tensor_id,
                            const uint64_t *tid_base, int64_t row_offset, uint8_t *codes,

@@ -645,10 +645,10 @@ struct EpiTile {
 #endif
 template <int D, int BITS, int MODE>
 __global__ void KGQ_EPI_BOUNDS
-layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
+layer_epilogue_kernel(const float *hin, int64_t n_rows, const float *__restrict__ theta,
                       uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
                       int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
-                      float *__restrict__ offsets, float *__restrict__ e_next,
+                      float *__restrict__ offsets, float *e_next,
                       uint32_t *__restrict__ mask) {
     using ET = EpiTile<D>;
     constexpr int LPR = RG<D>::LPR, RPW = RG<D>::RPW, ROWS = ET::ROWS, RS = ET::RS, TC = ET::TC;
@@ -673,8 +673,8 @@ layer_epilogue_kernel(const float *__restrict__ hin, int64_t n_rows, const float
         const int64_t rw = tl * ROWS + (ps * 8 + warp) * RPW + grp;
         if (tl < n_tiles && rw < n_rows) {
             const float4 *src = reinterpret_cast<const float4 *>(hin + rw * D);
-            nh[0] = __ldg(src + fa);
-            nh[1] = __ldg(src + fb);
+            nh[0] = __ldcg(src + fa);       // coherent loads: E' may be written over H
+            nh[1] = __ldcg(src + fb);       // (functional.EPILOGUE_IN_PLACE), tile by tile
         } else {
             nh[0] = nh[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -762,7 +762,7 @@ struct EpiTc {
 
 template <int D, int BITS, int MODE>
 __global__ void __launch_bounds__(256)
-layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const float *__restrict__ theta,
+layer_epilogue_tc_kernel(const float *hin, int64_t n_rows, const float *__restrict__ theta,
                          uint64_t seed, uint64_t tid, const uint64_t *__restrict__ tid_base,
                          int64_t row_offset, uint8_t *__restrict__ codes, float *__restrict__ ranges,
                          float *__restrict__ offsets, const __grid_constant__ CUtensorMap tm_out,
@@ -810,8 +810,8 @@ layer_epilogue_tc_kernel(const float *__restrict__ hin, int64_t n_rows, const fl
         const int64_t rw = tl * M + (ps * 8 + warp) * RPW + grp;
         if (tl < n_tiles && rw < n_rows) {
             const float4 *src = reinterpret_cast<const float4 *>(hin + rw * D);
-            nh[0] = __ldg(src + fa);
-            nh[1] = __ldg(src + fb);
+            nh[0] = __ldcg(src + fa);       // coherent loads: E' may be written over H
+            nh[1] = __ldcg(src + fb);       // (functional.EPILOGUE_IN_PLACE), tile by tile
         } else {
             nh[0] = nh[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }

@@ -41,6 +41,14 @@ _env_split = os.environ.get("KGQ_SPLIT_LAYER")
 SPLIT_LAYER_DEFAULT = None if _env_split is None else _env_split == "1"
 
 
+# The split layer's epilogue (kgq_layer_epilogue_f32) may write E' over H:
+# every epilogue variant is row-local and reads a tile's H rows before it
+# stores that tile's E' rows (TMA or plain loads, then the J tile, then the
+# stores), so the quantized layer needs one N x d buffer instead of two.  Not
+# for b = 32, where H itself is the context.
+EPILOGUE_IN_PLACE = True
+
+
 def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig,
                        stream: RandomStream | None, tensor_id: int | None = None,
                        row_offset: int = 0, want_h: bool = False, split: bool | None = None):
@@ -76,12 +84,15 @@ def graph_conv_forward(adj: CSR, e: torch.Tensor, theta: torch.Tensor, cfg: Quan
     codes = torch.empty((n_rows, packed_group_bytes(d, cfg.bits)), dtype=torch.uint8, device=dev)
     ranges = torch.empty(n_rows, dtype=torch.float32, device=dev)
     offsets = torch.empty(n_rows, dtype=torch.float32, device=dev)
-    e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
     if split is None:
         split = (SPLIT_LAYER_DEFAULT if SPLIT_LAYER_DEFAULT is not None
                  else e.numel() * e.element_size() <= SPLIT_L2_BYTES)
     h = torch.empty((n_rows, d), dtype=torch.float32, device=dev) if (want_h or split) else None
+    # split: E' is written over H (row-local epilogue: every tile reads its H
+    # rows before it stores E'; H is scratch once quantized) unless H is wanted
+    e_next = h if (split and not want_h and EPILOGUE_IN_PLACE) else \
+        torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     if split:
         L = _lib.load()
         st = L.kgq_spmm_csr_f32(adj.indptr.data_ptr(), adj.indices.data_ptr(), adj.data.data_ptr(), n_rows,
@@ -167,10 +178,10 @@ def _split_epilogue(h: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig, stre
     """The split layer's part 2 on a given H (kgq_layer_epilogue_f32)."""
     n_rows, d = h.shape
     dev = h.device
-    e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     mask = torch.empty(((n_rows * d + 7) // 8 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
     L = _lib.load()
     if cfg.passthrough:
+        e_next = torch.empty((n_rows, d), dtype=torch.float32, device=dev)
         st = L.kgq_layer_epilogue_f32(h.data_ptr(), n_rows, d, theta.data_ptr(), PASSTHROUGH_BITS, 0, 0, 0, None,
                                       row_offset, None, None, None, e_next.data_ptr(), mask.data_ptr(),
                                       _lib.stream_ptr(dev))
@@ -188,6 +199,8 @@ def _split_epilogue(h: torch.Tensor, theta: torch.Tensor, cfg: QuantConfig, stre
     codes = torch.empty((n_rows, packed_group_bytes(d, cfg.bits)), dtype=torch.uint8, device=dev)
     ranges = torch.empty(n_rows, dtype=torch.float32, device=dev)
     offsets = torch.empty(n_rows, dtype=torch.float32, device=dev)
+    # H is this function's scratch: E' over it
+    e_next = h if EPILOGUE_IN_PLACE else torch.empty((n_rows, d), dtype=torch.float32, device=dev)
     st = L.kgq_layer_epilogue_f32(
         h.data_ptr(), n_rows, d, theta.data_ptr(), cfg.bits, cfg.mode, seed,
         int(tensor_id) & 0xFFFFFFFFFFFFFFFF, stream.tid_base_ptr() if stream is not None else None,

@@ -1306,3 +1306,45 @@ def test_retired_readout_step_is_bit_identical(layers, d, bits):
     acc = F.gather_rows_sum(ts[:1], idx)
     F.gather_rows_acc(acc, ts[1:3], idx)
     assert torch.equal(F.gather_rows_acc(acc, ts[3:], idx, out=torch.empty_like(acc)), one)
+
+
+@pytest.mark.parametrize("epi", ["default", "ffma", "tc1"])
+@pytest.mark.parametrize("d", [32, 64, 128])
+@pytest.mark.parametrize("bits,mode", [(1, 1), (2, 1), (2, 2), (4, 0), (8, 1)])
+def test_split_epilogue_in_place_is_bit_identical(epi, d, bits, mode, monkeypatch):
+    """The split layer writes E' over H (functional.EPILOGUE_IN_PLACE): every
+    epilogue variant (tcgen05 K6t, the older tcgen05 d=64 kernel, the FFMA
+    K6s) must give the same E', mask, codes and R / Z as with a separate
+    E' buffer, on a graph with hub rows and a partial last tile."""
+    if epi == "tc1" and d != 64:
+        pytest.skip("KGQ_EPI_TC1 selects a d = 64 kernel")
+    kgq = _kgq()
+    import scipy.sparse as sp
+    from paper_2212_04540_b200 import functional as F
+    if epi == "ffma":
+        monkeypatch.setenv("KGQ_EPI_FFMA", "1")
+    elif epi == "tc1":
+        monkeypatch.setenv("KGQ_EPI_TC1", "1")
+    n = 3001
+    a = sp.random(n, n, density=0.004, random_state=d + bits, format="lil", dtype=np.float32)
+    a[7, :] = 0.5
+    a = a.tocsr()
+    a = (a + a.T + sp.eye(n, dtype=np.float32)).tocsr()
+    a.sum_duplicates()
+    a.sort_indices()
+    A = kgq.CSR.from_scipy(a)
+    rng = np.random.default_rng(d * 10 + bits)
+    e = torch.from_numpy(rng.standard_normal((n, d), dtype=np.float32)).cuda()
+    theta = torch.from_numpy(rng.standard_normal((d, d), dtype=np.float32) * 0.1).cuda()
+    cfg = kgq.QuantConfig(bits=bits, rounding="nearest" if mode == 0 else "stochastic", rng={0: "fast", 1: "fast", 2: "compat"}[mode])
+    outs = []
+    for inplace in (True, False):
+        monkeypatch.setattr(F, "EPILOGUE_IN_PLACE", inplace)
+        en, mask, q, _ = F.graph_conv_forward(A, e, theta, cfg, kgq.RandomStream(4), tensor_id=3, split=True)
+        outs.append((en.clone(), mask.packed.clone(), q.codes.clone(), q.ranges.clone(), q.offsets.clone()))
+    for x, y in zip(*outs):
+        assert torch.equal(x.view(torch.uint8) if x.dtype == torch.float32 else x,
+                           y.view(torch.uint8) if y.dtype == torch.float32 else y)
+    # the H context does not depend on the epilogue: same codes / R / Z as the fused kernel
+    _, _, q_f, _ = F.graph_conv_forward(A, e, theta, cfg, kgq.RandomStream(4), tensor_id=3, split=False)
+    assert torch.equal(q_f.codes, outs[0][2]) and torch.equal(q_f.ranges, outs[0][3])
