@@ -277,6 +277,24 @@ class SparseRows:
         return self._dense
 
 
+def _rows_concat(parts, d: int) -> torch.Tensor:
+    """torch.cat of fp32 row blocks, or a view when they already lie back to
+    back in one buffer in this order (the BPR gradients, bpr_backward)."""
+    parts = [x.reshape(-1, d) for x in parts]
+    p0 = parts[0]
+    if all(x.dtype == torch.float32 and x.is_contiguous() for x in parts):
+        base, off, ok = p0.untyped_storage().data_ptr(), p0.data_ptr(), True
+        for x in parts:
+            if x.untyped_storage().data_ptr() != base or x.data_ptr() != off:
+                ok = False
+                break
+            off += x.numel() * 4
+        if ok:
+            n = sum(x.shape[0] for x in parts)
+            return p0.as_strided((n, d), (d, 1))
+    return torch.cat([x.to(torch.float32) for x in parts]).contiguous()
+
+
 def scatter_rows_multi_sparse(src_rows: int, idxs, gs):
     """scatter_rows_multi in compact form (SparseRows); None when the
     sort-free kernel does not apply (the caller takes the dense path)."""
@@ -286,7 +304,7 @@ def scatter_rows_multi_sparse(src_rows: int, idxs, gs):
         return None
     dev = gs[0].device
     idx = torch.cat([i.reshape(-1).to(torch.int32) for i in idxs])
-    g = torch.cat([x.reshape(-1, d).to(torch.float32) for x in gs]).contiguous()
+    g = _rows_concat(gs, d)
     ends = np.ascontiguousarray(np.cumsum([i.numel() for i in idxs]), dtype=np.int64)
     rows = torch.empty((m, d), dtype=torch.float32, device=dev)
     rowmap = torch.full((src_rows,), -1, dtype=torch.int32, device=dev)
@@ -375,7 +393,10 @@ def bpr_backward(g, margins, uh, ph, nh, l2: float, batch: int):
     elementwise kernel (kgq_bpr_backward_f32); g is a 0-d device tensor."""
     d = uh.shape[1]
     dev = uh.device
-    gu, gp, gn = (torch.empty_like(t) for t in (uh, ph, nh))
+    # one buffer, negatives first: the backward scatters the gathers' gradients
+    # in reverse record order (n, p, u), which then need no concatenation
+    buf = torch.empty((3,) + tuple(uh.shape), dtype=torch.float32, device=dev)
+    gn, gp, gu = buf[0], buf[1], buf[2]
     g = g.reshape(()).to(device=dev, dtype=torch.float32).contiguous()
     reg = float(np.float32(2.0 * l2 / batch))
     st = _lib.load().kgq_bpr_backward_f32(g.data_ptr(), margins.contiguous().data_ptr(), uh.contiguous().data_ptr(),
