@@ -457,21 +457,34 @@ def quality_bench(args, shape=None):
     written by datasets/run_reference_training.py in the build container)."""
     from paper_2212_04540_b200 import data as D
     import paper_2212_04540_b200 as kgq
-    from paper_2212_04540_b200.model import ModelConfig
-    from paper_2212_04540_b200.train import TrainConfig, train_run
+    import torch
+    from paper_2212_04540_b200.model import ModelConfig, embed
+    from paper_2212_04540_b200.train import TrainConfig, evaluate, train_run
     shape = shape or args.train_shape
     ds = D.reference_dataset(shape)
     adj = D.build_adjacency(ds)
     out = {"epochs": args.quality_epochs, "dataset": f"{shape}_seed0 (reference generator)"}
     for name, bits, rng in (("int2_fast", 2, "fast"), ("int2_compat", 2, "compat"), ("fp32", 32, "fast")):
         q = kgq.QuantConfig(bits=bits, rng=rng)
-        _, rep = train_run(ds, ModelConfig(layers=3, dim=64, quant=q),
-                           TrainConfig(epochs=args.quality_epochs, quant=q), adjacency=adj, graphs=True)
+        mcfg = ModelConfig(layers=3, dim=64, quant=q)
+        params, rep = train_run(ds, mcfg, TrainConfig(epochs=args.quality_epochs, quant=q), adjacency=adj,
+                                graphs=True)
         m = rep["metrics"]
+        # train_run's eval_seconds is one call (whichever run comes first pays the
+        # process's one-time setup); the steady-state cost: 3 more calls, median
+        readout = embed(params, adj, mcfg)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.monotonic()
+            evaluate(ds, readout, 20)
+            torch.cuda.synchronize()
+            ts.append(time.monotonic() - t0)
         out[name] = {"recall_at_20": round(m["recall_at_20"], 5), "ndcg_at_20": round(m["ndcg_at_20"], 5),
                      "loss_curve": [round(v, 6) for v in rep["loss_curve"]],
                      "epoch_s": [round(v, 3) for v in rep["timing"]["epoch_seconds"]],
                      "eval_s": round(rep["timing"]["eval_seconds"], 4),
+                     "eval_s_steady": round(float(np.median(ts)), 4),
                      "activation_bytes_peak": rep["memory"]["activation_bytes_peak"]}
     ref_path = os.path.join(ROOT, "datasets", f"{shape}_seed0_reference_runs.json")
     if os.path.exists(ref_path):
